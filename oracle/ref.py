@@ -1,0 +1,165 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes wrapper of oracle/_ref/libecono_ref.so,
+the unmodified reference simulator compiled by oracle/Makefile."""
+import ctypes as C
+import os
+
+import numpy as np
+
+from paper_2411_06364_b200 import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "libecono_ref.so")
+_lib = None
+
+
+def available():
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(LIB_PATH)
+        L.ref_create.argtypes = [C.c_void_p, C.c_int64, C.POINTER(abi.Options),
+                                 C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+        L.ref_destroy.argtypes = [C.c_void_p]
+        L.ref_step.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int32), C.c_char_p, C.c_size_t]
+        L.ref_events.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.ref_events.restype = C.c_int64
+        L.ref_event_detail.argtypes = [C.c_void_p, C.c_int64, C.c_char_p, C.c_size_t]
+        L.ref_samples.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.ref_samples.restype = C.c_int64
+        L.ref_finalize.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(abi.Report),
+                                   C.c_char_p, C.c_size_t]
+        L.ref_report_json.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, C.c_int]
+        L.ref_report_json.restype = C.c_int64
+        L.ref_scalars.argtypes = [C.c_void_p, C.POINTER(abi.Scalars)]
+        L.ref_snapshot.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.ref_snapshot.restype = C.c_int64
+        L.ref_generate_trace.argtypes = [C.c_int64, C.c_double, C.POINTER(abi.LengthDist),
+                                         C.POINTER(abi.LengthDist), C.c_uint64, C.c_void_p,
+                                         C.c_char_p, C.c_size_t]
+        L.ref_trace_hash.argtypes = [C.c_void_p, C.c_int64]
+        L.ref_trace_hash.restype = C.c_uint64
+        L.ref_fast_ingest.argtypes = [C.c_void_p]
+        L.ref_fast_ingest.restype = C.c_int64
+        L.ref_idle_to_first_arrival.argtypes = [C.c_void_p]
+        L.ref_time_steps.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+        L.ref_time_steps.restype = C.c_double
+        L.ref_time_steps_parallel.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.c_int64,
+                                              C.c_void_p]
+        L.ref_time_steps_parallel.restype = C.c_double
+        _lib = L
+    return _lib
+
+
+class EngineError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+def generate_trace(n, rate, prompt, rl, seed):
+    out = np.zeros(n, dtype=abi.TRACE_DTYPE)
+    err = C.create_string_buffer(512)
+    rc = lib().ref_generate_trace(n, rate, C.byref(abi.LengthDist(*prompt)),
+                                  C.byref(abi.LengthDist(*rl)), seed, out.ctypes.data, err, 512)
+    if rc:
+        raise EngineError(rc, err.value.decode())
+    return out
+
+
+def trace_hash(trace):
+    t = abi.trace_array(trace)
+    return int(lib().ref_trace_hash(t.ctypes.data, len(t)))
+
+
+class RefEngine:
+    """econosim::Engine (engine.hpp:79-145), the reference itself."""
+
+    def __init__(self, trace, opts):
+        self.trace = abi.trace_array(trace)
+        self.opts = opts
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = lib().ref_create(self.trace.ctypes.data, len(self.trace), C.byref(opts),
+                              C.byref(h), err, 1024)
+        if rc:
+            raise EngineError(rc, err.value.decode())
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_destroy(self.h)
+            self.h = None
+
+    def step(self, n=1):
+        more = C.c_int32()
+        err = C.create_string_buffer(1024)
+        rc = lib().ref_step(self.h, n, C.byref(more), err, 1024)
+        if rc:
+            raise EngineError(rc, err.value.decode())
+        return bool(more.value)
+
+    def run(self):
+        while self.step(1 << 30):
+            pass
+        return self.report()
+
+    def events(self):
+        n = lib().ref_events(self.h, None, 0)
+        out = np.zeros(n, dtype=abi.EVENT_DTYPE)
+        lib().ref_events(self.h, out.ctypes.data, n)
+        return out
+
+    def event_detail(self, i):
+        buf = C.create_string_buffer(256)
+        lib().ref_event_detail(self.h, i, buf, 256)
+        k, d = buf.value.decode().split("|", 1)
+        return k, d
+
+    def samples(self):
+        n = lib().ref_samples(self.h, None, 0)
+        out = np.zeros(n, dtype=abi.SAMPLE_DTYPE)
+        lib().ref_samples(self.h, out.ctypes.data, n)
+        return out
+
+    def finalize(self):
+        recs = np.zeros(len(self.trace), dtype=abi.RECORD_DTYPE)
+        rep = abi.Report()
+        err = C.create_string_buffer(1024)
+        rc = lib().ref_finalize(self.h, recs.ctypes.data, len(recs), C.byref(rep), err, 1024)
+        if rc:
+            raise EngineError(rc, err.value.decode())
+        return recs, rep
+
+    def report(self):
+        return self.finalize()
+
+    def report_json(self, with_records=True):
+        n = lib().ref_report_json(self.h, None, 0, int(with_records))
+        buf = C.create_string_buffer(n + 1)
+        lib().ref_report_json(self.h, buf, n + 1, int(with_records))
+        return buf.value.decode()
+
+    def scalars(self):
+        s = abi.Scalars()
+        lib().ref_scalars(self.h, C.byref(s))
+        return s
+
+    def snapshot(self):
+        n = lib().ref_snapshot(self.h, None, 0)
+        out = np.zeros(n, dtype=np.int64)
+        lib().ref_snapshot(self.h, out.ctypes.data, n)
+        return out
+
+    def fast_ingest(self):
+        return lib().ref_fast_ingest(self.h)
+
+    def idle_to_first_arrival(self):
+        return lib().ref_idle_to_first_arrival(self.h)
+
+    def time_steps(self, steps):
+        pt = C.c_int64()
+        secs = lib().ref_time_steps(self.h, steps, C.byref(pt))
+        return secs, pt.value
