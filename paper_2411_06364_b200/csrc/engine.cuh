@@ -1,0 +1,1617 @@
+// engine.cuh — EconoServe's per-iteration scheduling step, B200-native.
+//
+// One warp owns one serving instance and runs its whole Engine::step() loop
+// on-device (engine.hpp:104-116). All state lives in HBM as structure-of-
+// arrays (layout: DESIGN.md §3); the per-instance scalar block `Inst` is
+// staged in shared memory for the duration of a launch.
+//
+// The code is written warp-cooperatively against a tiny portability layer
+// (W lanes, LANE, BALLOT, WSYNC...). nvcc builds it with W = 32 for sm_100a;
+// the test-only host build (tests/hostsim) compiles the very same source with
+// W = 1 so logic can be checked against the oracle on a CPU-only box. The
+// product library is always the nvcc build — there is no CPU path in it.
+//
+// Reference data structures are replaced, not translated:
+//   PtQueue sorted vector (queues.hpp:80-108)  -> ordered: per-(deadline bucket,
+//       prompt) FIFO class lists + two-level bitmaps; FIFO: 32-ary min tree
+//       over request ids. Greedy skip-fit (queues.hpp:279-299) becomes
+//       O(takes) bitmap / tree queries instead of an O(|Q_P|) walk.
+//   GtQueue vector of groups (queues.hpp:125-204) -> group pool + key-sorted
+//       slot array + RL->group map + per-group cached demand sums.
+//   KvcAllocator std::map free list (kvc.hpp:334-401) -> address-sorted array
+//       of live regions; free gaps are its complement (always maximal in the
+//       reference: give_back coalesces both sides, take leaves an adjacent
+//       rest), so first-fit is a warp ballot over gaps and compact() a scan.
+//   HostingSlot vector (kvc.hpp:17-24) -> per-hosted-request slot fields +
+//       an insertion-ordered list of hosted ids.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#include "econoserve_b200.h"
+
+#ifdef __CUDACC__
+#define EDEV __device__ __forceinline__
+#define EDEVNI __device__ __noinline__
+#define EHD __host__ __device__ __forceinline__
+#define W 32
+#define LANE ((int)(threadIdx.x & 31))
+#define WSYNC() __syncwarp()
+#define BALLOT(p) __ballot_sync(0xffffffffu, (p))
+#define MATCH_ANY(v) __match_any_sync(0xffffffffu, (v))
+#define FFS(m) (__ffs(m) - 1)
+#define POPC(m) __popc(m)
+#define LANEMASK_LT ((1u << LANE) - 1u)
+#define CLZ64(x) __clzll((long long)(x))
+#define CLZ32(x) __clz((int)(x))
+template <class T> EDEV T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+template <class T> EDEV T shfl_xor(T v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+EHD uint64_t umulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * (unsigned __int128)b) >> 64);
+#endif
+}
+#else
+#define EDEV static inline
+#define EDEVNI static
+#define EHD static inline
+#define W 1
+#define LANE 0
+#define WSYNC() ((void)0)
+#define BALLOT(p) ((p) ? 1u : 0u)
+#define MATCH_ANY(v) 1u
+#define FFS(m) ((m) ? 0 : -1)
+#define POPC(m) ((m) ? 1 : 0)
+#define LANEMASK_LT 0u
+#define CLZ64(x) __builtin_clzll(x)
+#define CLZ32(x) __builtin_clz(x)
+template <class T> static inline T shfl(T v, int) { return v; }
+template <class T> static inline T shfl_xor(T v, int) { return v; }
+static inline uint64_t umulhi64(uint64_t a, uint64_t b) {
+  return (uint64_t)(((__uint128_t)a * (__uint128_t)b) >> 64);
+}
+#endif
+
+#define LANE0(stmt) \
+  do {              \
+    if (LANE == 0) { stmt; } \
+    WSYNC();        \
+  } while (0)
+
+namespace econo {
+
+typedef int64_t Tok;
+static const int32_t INF32 = 0x7fffffff;
+
+enum { ST_WAITING_PT = 0, ST_RUNNING = 1, ST_WAITING_GT = 2, ST_PREEMPTED = 3, ST_DONE = 4 };
+enum { F_HOSTED = 1, F_WAS_PREEMPTED = 2, F_ALLOC_FAIL = 4, F_HAS_RESERVED = 8, F_HAS_SLOT = 16,
+       F_PREFILL_FIN = 32, F_CAND = 64 };
+enum {
+  ERR_NONE = 0, ERR_ALLOC_FAIL, ERR_RESERVED_DRAW, ERR_SLOT_OUTSIDE, ERR_STUCK,
+  ERR_RELEASE_UNKNOWN, ERR_TABLE_OVERFLOW, ERR_INFEASIBLE_KVC, ERR_INFEASIBLE_RESERVE,
+  ERR_ARRIVAL_ORDER
+};
+enum { STATUS_RUN = 0, STATUS_DRAIN = 1 };
+
+// Per-instance scalar block + SoA pointers. Kept in shared memory while a
+// launch runs (one warp per instance), written back on exit.
+struct Inst {
+  // ---- configuration (immutable after create) ----
+  int32_t n, policy, ordered, grouping, full, pred_model;
+  int32_t nbd, nbk, record_events, record_samples;
+  int32_t pmax, nbuckets, bm_words, bm_l2;    // PT class table (ordered mode)
+  int32_t tree_levels, rl_cap;
+  int32_t tree_off[8], tree_len[8];            // 32-ary min tree (FIFO mode)
+  int32_t reg_cap, grp_cap, slot_cap, run_cap, ptiter_cap, adm_cap, scr_cap, hist_cap;
+  int64_t tfs, capacity, block, reserve_cap, general_cap, pred_quantum;
+  double t_base, t_token, over_rate, reserve_penalty, pen_free, pen_offload, sched_cost;
+  double pred_sigma, pred_accuracy, pred_tol, pred_pad, slo_scale, buffer_ratio;
+  double dbounds[ECONO_MAX_BOUNDS];
+  int64_t kbounds[ECONO_MAX_BOUNDS];
+  // ---- dynamic scalars ----
+  double clock, t_p, t_g;
+  int64_t iter, completed, arrival_cursor, free_total, reserved_used, written_total, exam_count;
+  int64_t hosted_total, hosted_overruns, alloc_failures, steps, executed, pt_dispatched, gt_scheduled;
+  uint64_t next_group_id, gt_next_seq;
+  int32_t pt_count, G, R, n_slots, n_regions, n_ptiter, n_adm, pts_admitted_iter, pt_admittable;
+  int32_t reg_free_top, grp_free_top, n_sel, n_selg, n_hosts_members;
+  int32_t error, err_id, status, mt_i, pmt_i, _pad0;
+  int64_t err_val, ev_n, ev_cap, sm_n, sm_cap, ev_total;
+  double agg_written, agg_allocated;
+  int64_t agg_fs, agg_tfs_hits, agg_pt_iters;
+  // ---- per-request SoA (n entries) ----
+  const double* arrival;
+  const int32_t* prompt;
+  const int32_t* true_rl;
+  int32_t *predicted, *padded, *generated, *occupied, *allowance, *gen_epoch, *prefill_done;
+  int32_t *preempt_count, *reserve_draws, *held, *reg_head, *reg_tail, *reg_cnt, *reserved, *written;
+  int32_t *slot_host, *slot_off, *slot_len, *slot_abs, *pt_next, *gt_next, *dem;
+  uint8_t *state, *flags;
+  double *slo, *waiting, *preempt_t, *exec_t, *dispatch_t, *first_tok, *compl_clock, *last_enq;
+  double *penalty, *sched_share;
+  // ---- KVC region pool (reg_cap) ----
+  int32_t *rg_start, *rg_len, *rg_owner, *rg_next, *reg_free, *addr;
+  // ---- PT queue ----
+  int32_t *cls_head, *cls_tail, *cls_cnt;
+  uint64_t *bm1, *bm2;
+  int32_t* tree;
+  // ---- GT groups (grp_cap) ----
+  uint64_t *gr_id, *gr_seq;
+  int32_t *gr_rl, *gr_head, *gr_tail, *gr_cnt, *gr_db, *gr_kb, *gr_maxocc, *grp_free, *gq, *rl_map;
+  double *gr_formed, *gr_mindl;
+  int64_t* gr_dem;
+  // ---- ordered lists ----
+  int32_t *run, *slots, *ptiter_id, *ptiter_tok, *adm;
+  // ---- scratch ----
+  int32_t *sel_ids, *selg_start, *selg_rl;            // GT selection output
+  int32_t *wa_w, *wa_b, *wa_l, *wa_u, *wb_w, *wb_b, *wb_l, *wb_u;  // planner regions
+  int32_t *cd_ri, *cd_abs, *cd_use, *cd_len, *assigned;   // planner candidates
+  int32_t *os_host, *os_hosted, *os_off, *os_len, *os_abs;  // planner output slots
+  int32_t *tmp_a, *tmp_b, *tmp_c;
+  // ---- RNG (mt19937_64 x2) ----
+  uint64_t *mt, *pmt;
+  // ---- outputs ----
+  EconoEvent* ev;
+  EconoSample* sm;
+  int64_t* hist;
+};
+
+// ------------------------------------------------------------------------
+// scalar helpers (common.hpp:26-35; std::min/max semantics kept for doubles)
+// ------------------------------------------------------------------------
+EDEV Tok block_round(Tok t, Tok b) { return t <= 0 ? 0 : (t + b - 1) / b * b; }
+EDEV Tok ceil_tokens(double v) { return (Tok)ceil(v - 1e-9); }
+EDEV double dmax(double a, double b) { return (a < b) ? b : a; }
+EDEV double dmin(double a, double b) { return (b < a) ? b : a; }
+EDEV Tok tmax(Tok a, Tok b) { return (a < b) ? b : a; }
+EDEV Tok tmin(Tok a, Tok b) { return (b < a) ? b : a; }
+
+EDEV double iteration_time(const Inst& I, Tok fs) {  // engine.hpp:46-51
+  const Tok base = tmin(fs, I.tfs);
+  const Tok over = tmax(0, fs - I.tfs);
+  return I.t_base + I.t_token * (double)base + I.over_rate * (double)over;
+}
+
+template <class T>
+EDEV T wmin(T v) {
+  for (int o = W / 2; o > 0; o >>= 1) {
+    T x = shfl_xor(v, o);
+    v = x < v ? x : v;
+  }
+  return v;
+}
+template <class T>
+EDEV T wsum(T v) {
+  for (int o = W / 2; o > 0; o >>= 1) v += shfl_xor(v, o);
+  return v;
+}
+
+// Shift a[pos..n) right by one and store v at pos (room for n+1 required).
+template <class T>
+EDEV void arr_insert(T* a, int32_t n, int32_t pos, T v) {
+  for (int32_t hi = n; hi > pos; hi -= W) {
+    const int32_t i = hi - 1 - LANE;
+    const bool ok = i >= pos;
+    T x = T();
+    if (ok) x = a[i];
+    WSYNC();
+    if (ok) a[i + 1] = x;
+    WSYNC();
+  }
+  LANE0(a[pos] = v);
+}
+// Remove a[pos..pos+k) from an n-element array.
+template <class T>
+EDEV void arr_erase(T* a, int32_t n, int32_t pos, int32_t k) {
+  for (int32_t lo = pos; lo < n - k; lo += W) {
+    const int32_t i = lo + LANE;
+    const bool ok = i < n - k;
+    T x = T();
+    if (ok) x = a[i + k];
+    WSYNC();
+    if (ok) a[i] = x;
+    WSYNC();
+  }
+}
+// Position of the first element equal to v (or -1), warp ballot scan.
+EDEV int32_t arr_find(const int32_t* a, int32_t n, int32_t v) {
+  for (int32_t base = 0; base < n; base += W) {
+    const int32_t i = base + LANE;
+    const unsigned m = BALLOT(i < n && a[i] == v);
+    if (m) return base + FFS(m);
+  }
+  return -1;
+}
+
+// ------------------------------------------------------------------------
+// events / errors
+// ------------------------------------------------------------------------
+EDEV void logev(Inst& I, int kind, int32_t id, int64_t a, int64_t b) {  // engine.hpp:211-214
+  if (LANE == 0) {
+    I.ev_total++;
+    if (I.record_events) {
+      if (I.ev_n < I.ev_cap) {
+        EconoEvent& e = I.ev[I.ev_n];
+        e.iter = I.iter;
+        e.clock = I.clock;
+        e.kind = kind;
+        e.id = id;
+        e.a = a;
+        e.b = b;
+      }
+      I.ev_n++;
+    }
+  }
+}
+EDEV void set_error(Inst& I, int code, int32_t id, int64_t val) {
+  if (LANE == 0 && I.error == ERR_NONE) {
+    I.error = code;
+    I.err_id = id;
+    I.err_val = val;
+  }
+  WSYNC();
+}
+
+// ------------------------------------------------------------------------
+// RNG: std::mt19937_64 and the libstdc++ 13 distributions the path uses.
+// Called by lane 0 only (one sequential stream per instance).
+// ------------------------------------------------------------------------
+EHD uint64_t mt_next(uint64_t* x, int32_t& idx) {
+  if (idx >= 312) {
+    const uint64_t up = 0xFFFFFFFF80000000ULL, lo = 0x7FFFFFFFULL;
+    for (int k = 0; k < 312; ++k) {
+      const int k1 = k + 1 == 312 ? 0 : k + 1;
+      const int km = k + 156 >= 312 ? k + 156 - 312 : k + 156;
+      const uint64_t y = (x[k] & up) | (x[k1] & lo);
+      x[k] = x[km] ^ (y >> 1) ^ ((y & 1) ? 0xB5026F5AA96619E9ULL : 0);
+    }
+    idx = 0;
+  }
+  uint64_t z = x[idx++];
+  z ^= (z >> 29) & 0x5555555555555555ULL;
+  z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+  z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+  z ^= (z >> 43);
+  return z;
+}
+EHD void mt_seed(uint64_t* x, int32_t& idx, uint64_t s) {
+  x[0] = s;
+  for (int i = 1; i < 312; ++i) x[i] = 6364136223846793005ULL * (x[i - 1] ^ (x[i - 1] >> 62)) + (uint64_t)i;
+  idx = 312;
+}
+// uniform_int_distribution::_S_nd (uniform_int_dist.h:257-282), Lemire with a
+// 128-bit product split into umulhi/lo.
+EHD uint64_t lemire(uint64_t* x, int32_t& idx, uint64_t range) {
+  uint64_t r = mt_next(x, idx);
+  uint64_t lo = r * range, hi = umulhi64(r, range);
+  if (lo < range) {
+    const uint64_t thr = (0 - range) % range;
+    while (lo < thr) {
+      r = mt_next(x, idx);
+      lo = r * range;
+      hi = umulhi64(r, range);
+    }
+  }
+  return hi;
+}
+EHD uint64_t uniform_u64(uint64_t* x, int32_t& idx, uint64_t a, uint64_t b) {
+  const uint64_t urange = b - a;
+  if (urange < 0xFFFFFFFFFFFFFFFFULL) return lemire(x, idx, urange + 1) + a;
+  return mt_next(x, idx) + a;
+}
+EHD double canonical(uint64_t* x, int32_t& idx) {  // random.tcc:3349-3380
+  double r = (double)mt_next(x, idx) / 18446744073709551616.0;
+  if (r >= 1.0) r = 0.99999999999999989;  // nextafter(1, 0)
+  return r;
+}
+// A fresh normal_distribution per call (workload.hpp:233): polar method,
+// random.tcc:1811-1844; the cached second variate is discarded.
+EDEV double normal_fresh(uint64_t* x, int32_t& idx, double stddev) {
+  double a, b, r2;
+  do {
+    a = 2.0 * canonical(x, idx) - 1.0;
+    b = 2.0 * canonical(x, idx) - 1.0;
+    r2 = a * a + b * b;
+  } while (r2 > 1.0 || r2 == 0.0);
+  const double mult = sqrt(-2 * log(r2) / r2);
+  double ret = b * mult;
+  return ret * stddev + 0.0;
+}
+EDEV Tok quantize_up(Tok v, Tok q) { return q <= 1 ? v : block_round(v, q); }
+// predict_rl (workload.hpp:228-264)
+EDEV Tok predict_rl(const Inst& I, Tok true_rl, uint64_t* x, int32_t& idx) {
+  if (I.pred_model == ECONO_PRED_ORACLE) return quantize_up(true_rl, I.pred_quantum);
+  if (I.pred_model == ECONO_PRED_LOGNORMAL) {
+    const double v = (double)true_rl * exp(normal_fresh(x, idx, I.pred_sigma));
+    return quantize_up(tmax(1, (Tok)llround(v)), I.pred_quantum);
+  }
+  const double t = (double)true_rl;
+  const Tok lo_in = tmax(1, ceil_tokens(t * (1.0 - I.pred_tol)));
+  const Tok hi_in = (Tok)floor(t * (1.0 + I.pred_tol) + 1e-9);
+  if (canonical(x, idx) < I.pred_accuracy) {
+    const Tok b = tmax(lo_in, hi_in);
+    return quantize_up((Tok)uniform_u64(x, idx, (uint64_t)lo_in, (uint64_t)b), I.pred_quantum);
+  }
+  const double a = I.pred_tol, bb = 2.0 * I.pred_tol + 0.25;
+  const double u = canonical(x, idx) * (bb - a) + a;
+  Tok v;
+  if (canonical(x, idx) < 0.5) {
+    v = (Tok)llround(t * (1.0 + u));
+    if (v <= hi_in) v = hi_in + 1;
+  } else {
+    v = (Tok)llround(t * (1.0 - u));
+    if (v >= lo_in) v = lo_in - 1;
+    if (v < 1) v = hi_in + 1;
+  }
+  return quantize_up(tmax(1, v), I.pred_quantum);
+}
+EDEV Tok apply_padding(Tok p, double ratio) { return ceil_tokens((double)p * (1.0 + ratio)); }
+
+// ------------------------------------------------------------------------
+// ordering keys (queues.hpp:30-69)
+// ------------------------------------------------------------------------
+EDEV int bucket_d(const Inst& I, double v) {
+  int i = 0;
+  while (i < I.nbd && !(v < I.dbounds[i])) ++i;
+  return i;
+}
+EDEV int bucket_k(const Inst& I, Tok v) {
+  int i = 0;
+  while (i < I.nbk && !(v < I.kbounds[i])) ++i;
+  return i;
+}
+
+// ------------------------------------------------------------------------
+// PT queue — ordered mode: class (deadline bucket b, prompt p) FIFO lists.
+// Queue order (queues.hpp:44-50 with kvc bucket 0 and seq == id) is
+// b ascending, p descending, id ascending.
+// ------------------------------------------------------------------------
+EDEV int32_t cls_of(const Inst& I, int b, int p) { return b * (I.pmax + 1) + p; }
+EDEV uint64_t mask_upto(int r) { return r >= 63 ? ~0ULL : ((1ULL << (r + 1)) - 1); }
+EDEV void bm_set(Inst& I, int b, int p) {  // lane 0
+  I.bm1[(int64_t)b * I.bm_words + (p >> 6)] |= 1ULL << (p & 63);
+  I.bm2[(int64_t)b * I.bm_l2 + (p >> 12)] |= 1ULL << ((p >> 6) & 63);
+}
+EDEV void bm_clear(Inst& I, int b, int p) {  // lane 0
+  uint64_t& w = I.bm1[(int64_t)b * I.bm_words + (p >> 6)];
+  w &= ~(1ULL << (p & 63));
+  if (w == 0) I.bm2[(int64_t)b * I.bm_l2 + (p >> 12)] &= ~(1ULL << ((p >> 6) & 63));
+}
+// Largest nonempty prompt class p <= x in bucket b, or -1.
+EDEV int bm_prev(const Inst& I, int b, int64_t xx) {
+  if (xx < 0) return -1;
+  const int x = (int)(xx > I.pmax ? I.pmax : xx);
+  const uint64_t* b1 = I.bm1 + (int64_t)b * I.bm_words;
+  const uint64_t* b2 = I.bm2 + (int64_t)b * I.bm_l2;
+  const int w = x >> 6;
+  uint64_t word = b1[w] & mask_upto(x & 63);
+  if (word) return (w << 6) + 63 - CLZ64(word);
+  const int w2 = w - 1;
+  if (w2 < 0) return -1;
+  const int s = w2 >> 6;
+  uint64_t sw = b2[s] & mask_upto(w2 & 63);
+  if (!sw) {
+    int found = -1;
+    for (int hi = s - 1; hi >= 0 && found < 0; hi -= W) {
+      const int j = hi - LANE;
+      const unsigned m = BALLOT(j >= 0 && b2[j >= 0 ? j : 0] != 0);
+      if (m) found = hi - FFS(m);
+    }
+    if (found < 0) return -1;
+    sw = b2[found];
+    const int ww = (found << 6) + 63 - CLZ64(sw);
+    return (ww << 6) + 63 - CLZ64(b1[ww]);
+  }
+  const int ww = (s << 6) + 63 - CLZ64(sw);
+  return (ww << 6) + 63 - CLZ64(b1[ww]);
+}
+
+// ------------------------------------------------------------------------
+// PT queue — FIFO mode: 32-ary min tree over request ids (queue order ==
+// arrival order == id order, seq == id). Leaves hold prompt_len or INF.
+// ------------------------------------------------------------------------
+EDEV int32_t tree_at(const Inst& I, int lvl, int64_t i) { return I.tree[I.tree_off[lvl] + i]; }
+// First queued id >= pos whose prompt <= c, or -1.
+EDEV int32_t tree_first(const Inst& I, int64_t pos, int64_t c) {
+  if (c <= 0 || pos >= I.n) return -1;
+  int lvl = 0;
+  int64_t idx = pos, found = -1;
+  for (;;) {
+    const int64_t blk = idx >> 5;
+    const int64_t len = I.tree_len[lvl];
+    for (int j0 = 0; j0 < 32 && found < 0; j0 += W) {
+      const int64_t node = blk * 32 + j0 + LANE;
+      const bool ok = node >= idx && node < len && tree_at(I, lvl, node < len ? node : 0) <= c;
+      const unsigned m = BALLOT(ok);
+      if (m) found = blk * 32 + j0 + FFS(m);
+    }
+    if (found >= 0) break;
+    if (lvl == I.tree_levels - 1) return -1;
+    idx = blk + 1;
+    ++lvl;
+    if (idx >= I.tree_len[lvl]) return -1;
+  }
+  while (lvl > 0) {
+    --lvl;
+    const int64_t blk = found;
+    const int64_t len = I.tree_len[lvl];
+    int64_t f = -1;
+    for (int j0 = 0; j0 < 32 && f < 0; j0 += W) {
+      const int64_t node = blk * 32 + j0 + LANE;
+      const bool ok = node < len && tree_at(I, lvl, node < len ? node : 0) <= c;
+      const unsigned m = BALLOT(ok);
+      if (m) f = blk * 32 + j0 + FFS(m);
+    }
+    found = f;
+  }
+  return (int32_t)found;
+}
+// Recompute ancestors of leaf range [lo, hi] (inclusive).
+EDEV void tree_fix(Inst& I, int64_t lo, int64_t hi) {
+  for (int lvl = 1; lvl < I.tree_levels; ++lvl) {
+    lo >>= 5;
+    hi >>= 5;
+    const int64_t clen = I.tree_len[lvl - 1];
+    if (hi - lo + 1 >= W) {  // many nodes: one lane per node
+      for (int64_t nd = lo + LANE; nd <= hi; nd += W) {
+        int32_t mn = INF32;
+        for (int j = 0; j < 32; ++j) {
+          const int64_t ch = nd * 32 + j;
+          if (ch < clen) {
+            const int32_t v = tree_at(I, lvl - 1, ch);
+            mn = v < mn ? v : mn;
+          }
+        }
+        I.tree[I.tree_off[lvl] + nd] = mn;
+      }
+    } else {  // few nodes: the warp reduces each node's children
+      for (int64_t nd = lo; nd <= hi; ++nd) {
+        int32_t mn = INF32;
+        for (int j = LANE; j < 32; j += W) {
+          const int64_t ch = nd * 32 + j;
+          if (ch < clen) {
+            const int32_t v = tree_at(I, lvl - 1, ch);
+            mn = v < mn ? v : mn;
+          }
+        }
+        mn = wmin(mn);
+        LANE0(I.tree[I.tree_off[lvl] + nd] = mn);
+      }
+    }
+    WSYNC();
+  }
+}
+EDEV void tree_set(Inst& I, int64_t id, int32_t v) {
+  LANE0(I.tree[id] = v);
+  tree_fix(I, id, id);
+}
+
+// ------------------------------------------------------------------------
+// KVC block manager (kvc.hpp:35-424) over the address-sorted region array.
+// ------------------------------------------------------------------------
+EDEV int32_t addr_lower(const Inst& I, Tok start) {  // first position with start >= start
+  int32_t lo = 0, hi = I.n_regions;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (I.rg_start[I.addr[mid]] < start) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+EDEV void addr_insert_region(Inst& I, int32_t r) {
+  const int32_t pos = addr_lower(I, I.rg_start[r]);
+  if (I.n_regions >= I.reg_cap) { set_error(I, ERR_TABLE_OVERFLOW, -1, 1); return; }
+  arr_insert(I.addr, I.n_regions, pos, r);
+  LANE0(I.n_regions++);
+}
+EDEV void addr_remove_region(Inst& I, int32_t r) {
+  const int32_t pos = addr_lower(I, I.rg_start[r]);
+  arr_erase(I.addr, I.n_regions, pos, 1);
+  LANE0(I.n_regions--);
+}
+EDEV int32_t region_new(Inst& I, int32_t owner, Tok start, Tok len) {  // all lanes get the id
+  if (I.reg_free_top <= 0) { set_error(I, ERR_TABLE_OVERFLOW, owner, 2); return -1; }
+  const int32_t r = I.reg_free[I.reg_free_top - 1];
+  WSYNC();
+  if (LANE == 0) {
+    I.reg_free_top--;
+    I.rg_start[r] = (int32_t)start;
+    I.rg_len[r] = (int32_t)len;
+    I.rg_owner[r] = owner;
+    I.rg_next[r] = -1;
+    if (I.reg_cnt[owner] == 0) I.reg_head[owner] = r; else I.rg_next[I.reg_tail[owner]] = r;
+    I.reg_tail[owner] = r;
+    I.reg_cnt[owner]++;
+    I.held[owner] += (int32_t)len;
+  }
+  WSYNC();
+  return r;
+}
+
+// owner_or_slot_host (kvc.hpp:405-410), slots identified by hosted id.
+EDEV bool owner_or_slot_host(const Inst& I, int32_t hosted, int32_t owner) {
+  int32_t h = I.slot_host[hosted];
+  for (int guard = 0; guard < 64; ++guard) {
+    if (h == owner) return true;
+    if (!(I.flags[h] & F_HAS_SLOT)) return false;
+    h = I.slot_host[h];
+  }
+  return false;
+}
+
+// compact() (kvc.hpp:372-401): slide every region down in address order.
+EDEVNI void kvc_compact(Inst& I) {
+  const int32_t L = I.n_regions;
+  int32_t* ns = I.tmp_a;  // new start per address position
+  int32_t carry = 0;
+  for (int32_t base = 0; base < L; base += W) {
+    const int32_t j = base + LANE;
+    int32_t len = j < L ? I.rg_len[I.addr[j]] : 0;
+    int32_t incl = len;
+    for (int o = 1; o < W; o <<= 1) {
+      const int32_t y = shfl(incl, LANE - o >= 0 ? LANE - o : 0);
+      if (LANE >= o) incl += y;
+    }
+    if (j < L) ns[j] = carry + incl - len;
+    carry += shfl(incl, W - 1);
+  }
+  WSYNC();
+  // slots move with the region holding their (pre-move) start
+  for (int32_t base = 0; base < I.n_slots; base += W) {
+    const int32_t si = base + LANE;
+    if (si < I.n_slots) {
+      const int32_t h = I.slots[si];
+      const int32_t abs = I.slot_abs[h];
+      int32_t lo = 0, hi = L;  // last position with start <= abs
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (I.rg_start[I.addr[mid]] <= abs) lo = mid + 1; else hi = mid;
+      }
+      const int32_t pos = lo - 1;
+      if (pos >= 0) {
+        const int32_t r = I.addr[pos];
+        const int32_t os = I.rg_start[r];
+        if (abs < os + I.rg_len[r] && ns[pos] != os && owner_or_slot_host(I, h, I.rg_owner[r]))
+          I.tmp_b[si] = abs + (ns[pos] - os);
+        else
+          I.tmp_b[si] = abs;
+      } else {
+        I.tmp_b[si] = abs;
+      }
+    }
+  }
+  WSYNC();
+  for (int32_t si = LANE; si < I.n_slots; si += W) I.slot_abs[I.slots[si]] = I.tmp_b[si];
+  for (int32_t j = LANE; j < L; j += W) I.rg_start[I.addr[j]] = ns[j];
+  WSYNC();
+}
+
+// take() (kvc.hpp:334-348): first fit over the complement of live regions.
+// Returns the start or -1; *pos receives the address-array insert position.
+EDEVNI Tok kvc_take(Inst& I, Tok need, int32_t* pos_out) {
+  if (need > I.free_total) return -1;
+  const int32_t L = I.n_regions;
+  for (int32_t base = 0; base <= L; base += W) {
+    const int32_t j = base + LANE;
+    Tok gs = 0, gap = -1;
+    if (j <= L) {
+      if (j > 0) {
+        const int32_t pr = I.addr[j - 1];
+        gs = (Tok)I.rg_start[pr] + I.rg_len[pr];
+      }
+      const Tok ge = j < L ? (Tok)I.rg_start[I.addr[j]] : I.general_cap;
+      gap = ge - gs;
+    }
+    const unsigned m = BALLOT(j <= L && gap >= need);
+    if (m) {
+      const int src = FFS(m);
+      *pos_out = base + src;
+      return shfl(gs, src);
+    }
+  }
+  kvc_compact(I);
+  *pos_out = L;
+  return I.general_cap - I.free_total;
+}
+
+// allocate_exact / grow_exact (kvc.hpp:104-131): one new region at the fit.
+EDEVNI bool kvc_alloc_region(Inst& I, int32_t id, Tok length) {
+  const Tok need = block_round(length, I.block);
+  int32_t pos = 0;
+  const Tok s = kvc_take(I, need, &pos);
+  if (s < 0) return false;
+  const int32_t r = region_new(I, id, s, need);
+  if (r < 0) return false;
+  if (I.n_regions >= I.reg_cap) { set_error(I, ERR_TABLE_OVERFLOW, id, 3); return false; }
+  arr_insert(I.addr, I.n_regions, pos, r);
+  LANE0(I.n_regions++; I.free_total -= need);
+  return true;
+}
+
+EDEV bool kvc_draw_reserved(Inst& I, int32_t id, Tok tokens) {  // kvc.hpp:144-150
+  if (I.reserved_used + tokens > I.reserve_cap) return false;
+  LANE0(I.reserved_used += tokens; I.reserved[id] += (int32_t)tokens; I.flags[id] |= F_HAS_RESERVED);
+  return true;
+}
+EDEV void kvc_release_reserved(Inst& I, int32_t id) {  // kvc.hpp:152-159
+  if (!(I.flags[id] & F_HAS_RESERVED)) return;
+  LANE0(I.reserved_used -= I.reserved[id]; I.reserved[id] = 0; I.flags[id] &= ~F_HAS_RESERVED);
+}
+EDEV void kvc_add_written(Inst& I, int32_t id, Tok d) {  // kvc.hpp:87-90 (lane 0 callers)
+  I.written[id] += (int32_t)d;
+  I.written_total += d;
+}
+
+// remove_slot (kvc.hpp:229-243)
+EDEVNI void kvc_remove_slot(Inst& I, int32_t hosted) {
+  if (!(I.flags[hosted] & F_HAS_SLOT)) return;
+  const int32_t oh = I.slot_host[hosted], oo = I.slot_off[hosted];
+  const int32_t oa = I.slot_abs[hosted], ol = I.slot_len[hosted];
+  int32_t mypos = -1;
+  for (int32_t base = 0; base < I.n_slots; base += W) {
+    const int32_t si = base + LANE;
+    const int32_t h = si < I.n_slots ? I.slots[si] : -1;
+    if (h >= 0 && h != hosted && I.slot_host[h] == hosted) {
+      const int32_t a = I.slot_abs[h];
+      if (a >= oa && a + I.slot_len[h] <= oa + ol) {
+        I.slot_host[h] = oh;
+        I.slot_off[h] += oo;
+      }
+    }
+    const unsigned m = BALLOT(h == hosted);
+    if (m && mypos < 0) mypos = base + FFS(m);
+  }
+  WSYNC();
+  if (mypos >= 0) {
+    arr_erase(I.slots, I.n_slots, mypos, 1);
+    LANE0(I.n_slots--);
+  }
+  LANE0(I.flags[hosted] &= ~F_HAS_SLOT);
+}
+
+// release (kvc.hpp:165-217)
+EDEVNI void kvc_release(Inst& I, int32_t id) {
+  const bool had = I.reg_cnt[id] > 0;
+  if (!had && !(I.flags[id] & F_HAS_RESERVED) && !(I.flags[id] & F_HAS_SLOT)) {
+    set_error(I, ERR_RELEASE_UNKNOWN, id, 0);
+    return;
+  }
+  kvc_remove_slot(I, id);
+  if (had) {
+    // promoted slots (host == id), in slot order
+    int32_t np = 0;
+    for (int32_t base = 0; base < I.n_slots; base += W) {
+      const int32_t si = base + LANE;
+      const bool hit = si < I.n_slots && I.slot_host[I.slots[si]] == id;
+      const unsigned m = BALLOT(hit);
+      if (hit) I.tmp_c[np + POPC(m & LANEMASK_LT)] = I.slots[si];
+      np += POPC(m);
+    }
+    WSYNC();
+    // drop the host's regions from the address order
+    Tok freed = 0;
+    for (int32_t r = I.reg_head[id]; r >= 0; r = I.rg_next[r]) {
+      addr_remove_region(I, r);
+      freed += I.rg_len[r];
+      LANE0(I.reg_free[I.reg_free_top++] = r);
+    }
+    LANE0(I.reg_cnt[id] = 0; I.reg_head[id] = -1; I.reg_tail[id] = -1; I.held[id] = 0);
+    for (int32_t k = 0; k < np; ++k) {
+      const int32_t h = I.tmp_c[k];
+      const int32_t r = region_new(I, h, I.slot_abs[h], I.slot_len[h]);
+      if (r < 0) return;
+      addr_insert_region(I, r);
+      freed -= I.slot_len[h];
+    }
+    if (np > 0) {  // erase promoted slots (stable)
+      int32_t w = 0;
+      for (int32_t base = 0; base < I.n_slots; base += W) {
+        const int32_t si = base + LANE;
+        const int32_t h = si < I.n_slots ? I.slots[si] : -1;
+        const bool keep = h >= 0 && I.slot_host[h] != id;
+        const unsigned m = BALLOT(keep);
+        WSYNC();
+        if (keep) I.slots[w + POPC(m & LANEMASK_LT)] = h;
+        if (h >= 0 && !keep) I.flags[h] &= ~F_HAS_SLOT;
+        w += POPC(m);
+        WSYNC();
+      }
+      LANE0(I.n_slots = w);
+    }
+    LANE0(I.free_total += freed);
+  }
+  kvc_release_reserved(I, id);
+  LANE0(I.written_total -= I.written[id]; I.written[id] = 0);
+}
+
+// ------------------------------------------------------------------------
+// GT queue (queues.hpp:125-204)
+// ------------------------------------------------------------------------
+EDEV uint64_t gkey_hi(const Inst& I, int32_t g) {
+  if (!I.ordered) return 0;
+  return ((uint64_t)I.gr_db[g] << 56) | ((uint64_t)(255 - I.gr_kb[g]) << 48) |
+         (0xFFFFFFFFFFFFULL - (uint64_t)I.gr_rl[g]);
+}
+EDEV bool gkey_less(const Inst& I, int32_t a, int32_t b) {
+  const uint64_t ha = gkey_hi(I, a), hb = gkey_hi(I, b);
+  if (ha != hb) return ha < hb;
+  return I.gr_seq[a] < I.gr_seq[b];
+}
+EDEV int32_t gq_upper(const Inst& I, int32_t g) {  // upper_bound by key
+  int32_t lo = 0, hi = I.G;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (gkey_less(I, g, I.gq[mid])) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+EDEV int32_t gq_pos(const Inst& I, int32_t g) {  // position of g (keys unique)
+  int32_t lo = 0, hi = I.G;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (gkey_less(I, I.gq[mid], g)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+EDEV void gq_rekey(Inst& I, int32_t g, double now) {  // place(): make_key (queues.hpp:187-193), lane 0
+  if (I.ordered) {
+    I.gr_db[g] = bucket_d(I, dmax(0.0, I.gr_mindl[g] - now));
+    I.gr_kb[g] = bucket_k(I, I.gr_maxocc[g]);
+  }
+}
+EDEV int32_t rl_find(const Inst& I, int32_t rl) {
+  if (rl >= 0 && rl < I.rl_cap) return I.rl_map[rl];
+  for (int32_t base = 0; base < I.G; base += W) {  // rare: RL beyond the map
+    const int32_t i = base + LANE;
+    const unsigned m = BALLOT(i < I.G && I.gr_rl[I.gq[i < I.G ? i : 0]] == rl);
+    if (m) return I.gq[base + FFS(m)];
+  }
+  return -1;
+}
+EDEV void rl_set(Inst& I, int32_t rl, int32_t g) {  // lane 0
+  if (I.grouping && rl >= 0 && rl < I.rl_cap) I.rl_map[rl] = g;
+}
+EDEV void gq_remove_at(Inst& I, int32_t pos) {  // drops the group from the queue and frees it
+  const int32_t g = I.gq[pos];
+  WSYNC();
+  arr_erase(I.gq, I.G, pos, 1);
+  LANE0(I.G--; rl_set(I, I.gr_rl[g], -1); I.grp_free[I.grp_free_top++] = g);
+}
+EDEV Tok member_demand(const Inst& I, int32_t id) {  // gt_member_demand (engine.hpp:238-247)
+  const Tok target = block_round((Tok)I.prompt[id] + I.generated[id] + I.padded[id], I.block);
+  const Tok delta = target - I.held[id];
+  return delta > 0 ? block_round(delta, I.block) : 0;
+}
+// group_insert_gt (queues.hpp:141-166). A waiting member's demand cannot
+// change while it waits (its holdings and progress are frozen), so it is
+// cached at join time and summed per group.
+EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline, int32_t occ, double now) {
+  const Tok d = member_demand(I, id);
+  LANE0(I.dem[id] = (int32_t)d; I.gt_next[id] = -1);
+  if (I.grouping) {
+    const int32_t g = rl_find(I, padded);
+    if (g >= 0) {
+      const int32_t pos = gq_pos(I, g);
+      arr_erase(I.gq, I.G, pos, 1);
+      LANE0(I.G--;
+            if (I.gr_cnt[g] == 0) I.gr_head[g] = id; else I.gt_next[I.gr_tail[g]] = id;
+            I.gr_tail[g] = id; I.gr_cnt[g]++; I.gr_dem[g] += d;
+            I.gr_mindl[g] = dmin(I.gr_mindl[g], deadline);
+            I.gr_maxocc[g] = (int32_t)tmax(I.gr_maxocc[g], occ);
+            gq_rekey(I, g, now));
+      const int32_t p2 = gq_upper(I, g);
+      arr_insert(I.gq, I.G, p2, g);
+      LANE0(I.G++);
+      return;
+    }
+  }
+  if (I.grp_free_top <= 0 || I.G >= I.grp_cap) { set_error(I, ERR_TABLE_OVERFLOW, id, 4); return; }
+  const int32_t g = I.grp_free[I.grp_free_top - 1];
+  WSYNC();
+  LANE0(I.grp_free_top--;
+        I.gr_id[g] = I.next_group_id++; I.gr_rl[g] = padded; I.gr_head[g] = id; I.gr_tail[g] = id;
+        I.gr_cnt[g] = 1; I.gr_dem[g] = d; I.gr_formed[g] = now; I.gr_mindl[g] = deadline;
+        I.gr_maxocc[g] = occ; I.gr_seq[g] = I.gt_next_seq++; I.gr_db[g] = 0; I.gr_kb[g] = 0;
+        gq_rekey(I, g, now); rl_set(I, padded, g));
+  const int32_t p2 = gq_upper(I, g);
+  arr_insert(I.gq, I.G, p2, g);
+  LANE0(I.G++);
+}
+
+// ------------------------------------------------------------------------
+// engine (engine.hpp:216-994), econoserve family
+// ------------------------------------------------------------------------
+EDEV void begin_gt_run(Inst& I, int32_t id, bool hosted) {  // engine.hpp:350-363 (lane 0)
+  I.flags[id] = hosted ? (I.flags[id] | F_HOSTED) : (I.flags[id] & ~F_HOSTED);
+  I.allowance[id] = I.generated[id] + I.padded[id];
+  I.gen_epoch[id] = I.generated[id];
+  const double wait = dmax(0.0, I.clock - I.last_enq[id]);
+  if (I.flags[id] & F_WAS_PREEMPTED) I.preempt_t[id] += wait; else I.waiting[id] += wait;
+  I.flags[id] &= ~F_WAS_PREEMPTED;
+  I.state[id] = ST_RUNNING;
+  I.run[I.R++] = id;
+  I.adm[I.n_adm++] = id;
+}
+
+// ingest_arrivals (engine.hpp:216-235) for every arrival with t <= clock+1e-12.
+EDEVNI void ingest(Inst& I) {
+  const int64_t first = I.arrival_cursor;
+  const double lim = I.clock + 1e-12;
+  if (first >= I.n || !(I.arrival[first] <= lim)) return;
+  int64_t lo = first + 1, hi = I.n;  // first index with arrival > lim (arrivals nondecreasing)
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (I.arrival[mid] <= lim) lo = mid + 1; else hi = mid;
+  }
+  const int64_t last = lo;
+  const int64_t k = last - first;
+  if (I.record_events) {
+    for (int64_t i = LANE; i < k; i += W) {
+      const int64_t e = I.ev_n + i;
+      if (e < I.ev_cap) {
+        EconoEvent& ev = I.ev[e];
+        ev.iter = I.iter; ev.clock = I.clock; ev.kind = ECONO_EV_ARRIVE; ev.id = (int32_t)(first + i);
+        ev.a = 0; ev.b = 0;
+      }
+    }
+  }
+  if (I.ordered) {
+    // class append in id order: peers of a class inside each warp chunk link
+    // to each other; the lowest links to the class tail, the highest becomes it.
+    for (int64_t base = first; base < last; base += W) {
+      const int64_t id = base + LANE;
+      const bool ok = id < last;
+      int cls = -1 - LANE;
+      int b = 0, p = 0;
+      if (ok) {
+        b = bucket_d(I, dmax(0.0, I.slo[id] - I.clock));
+        p = I.prompt[id];
+        cls = cls_of(I, b, p);
+      }
+      const unsigned grp = MATCH_ANY(cls);
+      int32_t old_tail = -1;
+      if (ok) old_tail = I.cls_tail[cls];
+      WSYNC();
+      if (ok) {
+        const unsigned higher = grp & ~((2u << LANE) - 1u);
+        I.pt_next[id] = higher ? (int32_t)(base + FFS(higher)) : -1;
+        const bool lowest = (grp & LANEMASK_LT) == 0;
+        const bool highest = higher == 0;
+        if (lowest) {
+          if (old_tail >= 0) I.pt_next[old_tail] = (int32_t)id; else I.cls_head[cls] = (int32_t)id;
+          I.cls_cnt[cls] += POPC(grp);
+        }
+        if (highest) I.cls_tail[cls] = (int32_t)id;
+      }
+      WSYNC();
+      for (int l = 0; l < W; ++l) {  // bitmap words are shared between classes
+        const int pb = shfl(p, l), bb = shfl(b, l);
+        const bool okl = shfl((int)ok, l);
+        if (okl && LANE == 0) bm_set(I, bb, pb);
+      }
+      WSYNC();
+    }
+  } else {
+    for (int64_t id = first + LANE; id < last; id += W) I.tree[id] = I.prompt[id];
+    WSYNC();
+    tree_fix(I, first, last - 1);
+  }
+  LANE0(I.arrival_cursor = last; I.pt_count += (int32_t)k; I.ev_total += k;
+        if (I.record_events) I.ev_n += k);
+}
+
+// Takes up to k entries from the head of class (b,p); appends ids to out.
+EDEV int32_t cls_take(Inst& I, int b, int p, int32_t k, int32_t* out, int32_t nout) {
+  const int32_t c = cls_of(I, b, p);
+  if (LANE == 0) {
+    int32_t h = I.cls_head[c];
+    for (int32_t i = 0; i < k; ++i) {
+      out[nout + i] = h;
+      h = I.pt_next[h];
+    }
+    I.cls_head[c] = h;
+    I.cls_cnt[c] -= k;
+    if (I.cls_cnt[c] == 0) {
+      I.cls_tail[c] = -1;
+      I.cls_head[c] = -1;
+      bm_clear(I, b, p);
+    }
+    I.pt_count -= k;
+  }
+  WSYNC();
+  return nout + k;
+}
+
+EDEVNI void dispatch_pts(Inst& I, int32_t npt) {  // dispatch_pt_reserved / _common (engine.hpp:365-381)
+  for (int32_t i = 0; i < npt; ++i) {
+    const int32_t id = I.tmp_a[i];
+    const Tok p = I.prompt[id];
+    if (!kvc_draw_reserved(I, id, p)) { set_error(I, ERR_RESERVED_DRAW, id, 0); return; }
+    if (LANE == 0) {
+      I.state[id] = ST_RUNNING;
+      I.dispatch_t[id] = I.clock;
+      I.waiting[id] += I.clock - I.arrival[id];
+      I.ptiter_id[I.n_ptiter] = id;
+      I.ptiter_tok[I.n_ptiter] = (int32_t)p;
+      I.n_ptiter++;
+      I.adm[I.n_adm++] = id;
+      I.pts_admitted_iter++;
+      I.pt_dispatched++;
+    }
+    logev(I, ECONO_EV_PT_DISPATCH, id, 0, 0);
+    WSYNC();
+  }
+}
+
+EDEVNI void schedule_gt_member(Inst& I, int32_t id) {  // engine.hpp:327-348
+  const Tok prompt = I.prompt[id], gen = I.generated[id], pad = I.padded[id];
+  const Tok target = block_round(prompt + gen + pad, I.block);
+  const Tok held = I.held[id];
+  const Tok resident = prompt + gen;
+  bool ok = true;
+  if (held == 0) ok = kvc_alloc_region(I, id, prompt + gen + pad);
+  else if (held < target) ok = kvc_alloc_region(I, id, target - held);
+  if (I.error) return;
+  if (!ok) { set_error(I, ERR_ALLOC_FAIL, id, 0); return; }
+  kvc_release_reserved(I, id);
+  if (LANE == 0) {
+    const Tok cur = I.written[id];
+    if (cur < resident) kvc_add_written(I, id, resident - cur);
+    I.occupied[id] = (int32_t)resident;
+    begin_gt_run(I, id, false);
+    I.gt_scheduled++;
+  }
+  logev(I, ECONO_EV_GT_SCHEDULE, id, I.padded[id], 0);
+  WSYNC();
+}
+
+// plan_pipeline (kvc_pipeline.hpp:29-136). Host group h's members are
+// I.tmp_b[hs..he) (ids) with write bases I.tmp_c[hs..he). Appends planned
+// slots to the os_* arrays; returns the new count.
+EDEVNI int32_t plan_host_group(Inst& I, int32_t l, int32_t hs, int32_t he, int32_t nout, int64_t* exams) {
+  if (l < 2 || he <= hs) return nout;
+  const Tok b = ceil_tokens(I.buffer_ratio * (double)l);
+  int32_t nr = he - hs;
+  int32_t *rw = I.wa_w, *rb = I.wa_b, *rlen = I.wa_l, *ru = I.wa_u;
+  int32_t *nw = I.wb_w, *nb = I.wb_b, *nlen = I.wb_l, *nu = I.wb_u;
+  for (int32_t i = LANE; i < nr; i += W) {
+    rw[i] = I.tmp_b[hs + i];
+    rb[i] = I.tmp_c[hs + i];
+    rlen[i] = l;
+    ru[i] = 0;
+  }
+  WSYNC();
+  for (int level = 1;; ++level) {
+    const Tok bound = (level >= 62 ? 0 : (Tok)l / ((Tok)1 << level)) - b;
+    if (bound < 1) break;
+    // candidates: second halves of regions with half >= 1, in region order
+    int32_t nc = 0;
+    for (int32_t base = 0; base < nr; base += W) {
+      const int32_t ri = base + LANE;
+      const int32_t half = ri < nr ? rlen[ri] / 2 : 0;
+      const bool ok = ri < nr && half >= 1;
+      const unsigned m = BALLOT(ok);
+      if (ok) {
+        const int32_t o = nc + POPC(m & LANEMASK_LT);
+        I.cd_ri[o] = ri;
+        I.cd_abs[o] = rb[ri] + (rlen[ri] - half);
+        I.cd_use[o] = ru[ri] + (rlen[ri] - half);
+        I.cd_len[o] = half;
+      }
+      nc += POPC(m);
+    }
+    WSYNC();
+    if (nc == 0) break;
+    if (LANE == 0) {  // std::shuffle (stl_algo.h:3719-3795) with the engine rng_
+      const uint64_t n = (uint64_t)nc;
+      auto swp = [&](uint64_t i, uint64_t j) {
+        if (i == j) return;
+        int32_t t;
+        t = I.cd_ri[i]; I.cd_ri[i] = I.cd_ri[j]; I.cd_ri[j] = t;
+        t = I.cd_abs[i]; I.cd_abs[i] = I.cd_abs[j]; I.cd_abs[j] = t;
+        t = I.cd_use[i]; I.cd_use[i] = I.cd_use[j]; I.cd_use[j] = t;
+        t = I.cd_len[i]; I.cd_len[i] = I.cd_len[j]; I.cd_len[j] = t;
+      };
+      uint64_t i = 1;
+      if ((n % 2) == 0) { swp(i, uniform_u64(I.mt, I.mt_i, 0, 1)); ++i; }
+      while (i != n) {
+        const uint64_t sr = i + 1;
+        const uint64_t x = uniform_u64(I.mt, I.mt_i, 0, sr * (sr + 1) - 1);
+        const uint64_t p1 = x / (sr + 1), p2 = x % (sr + 1);
+        swp(i, p1); ++i;
+        swp(i, p2); ++i;
+      }
+    }
+    for (int32_t i = LANE; i < nr; i += W) I.assigned[i] = -1;
+    WSYNC();
+    int32_t next_slot = 0;
+    bool any = false;
+    while (next_slot < nc) {
+      // the group with RL <= bound closest to it; FCFS on ties (kvc_pipeline.hpp:77-86)
+      *exams += I.G;
+      int32_t best = -1, bpos = -1;
+      for (int32_t base = 0; base < I.G; base += W) {
+        const int32_t pi = base + LANE;
+        if (pi < I.G) {
+          const int32_t g = I.gq[pi];
+          if (I.gr_cnt[g] > 0 && I.gr_rl[g] <= bound) {
+            bool better = best < 0;
+            if (!better) {
+              better = I.gr_rl[g] > I.gr_rl[best] ||
+                       (I.gr_rl[g] == I.gr_rl[best] &&
+                        (I.gr_formed[g] < I.gr_formed[best] ||
+                         (I.gr_formed[g] == I.gr_formed[best] && I.gr_id[g] < I.gr_id[best])));
+            }
+            if (better) { best = g; bpos = pi; }
+          }
+        }
+      }
+      for (int o = W / 2; o > 0; o >>= 1) {
+        const int32_t ob = shfl_xor(best, o), op = shfl_xor(bpos, o);
+        if (ob >= 0) {
+          bool better = best < 0;
+          if (!better) {
+            better = I.gr_rl[ob] > I.gr_rl[best] ||
+                     (I.gr_rl[ob] == I.gr_rl[best] &&
+                      (I.gr_formed[ob] < I.gr_formed[best] ||
+                       (I.gr_formed[ob] == I.gr_formed[best] && I.gr_id[ob] < I.gr_id[best])));
+          }
+          if (better) { best = ob; bpos = op; }
+        }
+      }
+      best = shfl(best, 0);
+      bpos = shfl(bpos, 0);
+      if (best < 0) break;
+      any = true;
+      const int32_t take = I.gr_cnt[best] < nc - next_slot ? I.gr_cnt[best] : nc - next_slot;
+      if (LANE == 0) {
+        int32_t m = I.gr_head[best];
+        Tok dsum = 0;
+        for (int32_t i = 0; i < take; ++i) {
+          const int32_t ci = next_slot + i;
+          const int32_t ri = I.cd_ri[ci];
+          I.os_host[nout + i] = rw[ri];
+          I.os_hosted[nout + i] = m;
+          I.os_off[nout + i] = I.cd_use[ci];
+          I.os_len[nout + i] = I.cd_len[ci];
+          I.os_abs[nout + i] = I.cd_abs[ci];
+          I.assigned[ri] = m;
+          dsum += I.dem[m];
+          m = I.gt_next[m];
+        }
+        I.gr_head[best] = m;
+        I.gr_cnt[best] -= take;
+        I.gr_dem[best] -= dsum;
+        if (I.gr_cnt[best] == 0) I.gr_tail[best] = -1;
+      }
+      WSYNC();
+      nout += take;
+      next_slot += take;
+      if (I.gr_cnt[best] == 0) gq_remove_at(I, bpos);
+    }
+    if (!any) break;
+    // halve every region (kvc_pipeline.hpp:540-556 in the reference order)
+    int32_t nn = 0;
+    for (int32_t base = 0; base < nr; base += W) {
+      const int32_t ri = base + LANE;
+      const bool ok = ri < nr;
+      const int32_t half = ok ? rlen[ri] / 2 : 0;
+      const int32_t cnt = ok ? (half < 1 ? 1 : 2) : 0;
+      int32_t incl = cnt;
+      for (int o = 1; o < W; o <<= 1) {
+        const int32_t y = shfl(incl, LANE - o >= 0 ? LANE - o : 0);
+        if (LANE >= o) incl += y;
+      }
+      if (ok) {
+        const int32_t o = nn + incl - cnt;
+        if (half < 1) {
+          nw[o] = rw[ri]; nb[o] = rb[ri]; nlen[o] = rlen[ri]; nu[o] = ru[ri];
+        } else {
+          const int32_t kept = rlen[ri] - half;
+          nw[o] = rw[ri]; nb[o] = rb[ri]; nlen[o] = kept; nu[o] = ru[ri];
+          if (I.assigned[ri] >= 0) {
+            nw[o + 1] = I.assigned[ri]; nb[o + 1] = rb[ri] + kept; nlen[o + 1] = half; nu[o + 1] = 0;
+          } else {
+            nw[o + 1] = rw[ri]; nb[o + 1] = rb[ri] + kept; nlen[o + 1] = half; nu[o + 1] = ru[ri] + kept;
+          }
+        }
+      }
+      nn += shfl(incl, W - 1);
+    }
+    WSYNC();
+    if (nn > I.scr_cap) { set_error(I, ERR_TABLE_OVERFLOW, -1, 5); return nout; }
+    int32_t* t;
+    t = rw; rw = nw; nw = t;
+    t = rb; rb = nb; nb = t;
+    t = rlen; rlen = nlen; nlen = t;
+    t = ru; ru = nu; nu = t;
+    nr = nn;
+  }
+  return nout;
+}
+
+// add_slot containment (kvc.hpp:219-224, 318-332)
+EDEV bool slot_fits(const Inst& I, int32_t host, int32_t abs, int32_t len) {
+  for (int32_t r = I.reg_head[host]; r >= 0; r = I.rg_next[r])
+    if (abs >= I.rg_start[r] && abs + len <= I.rg_start[r] + I.rg_len[r]) return true;
+  if ((I.flags[host] & F_HAS_SLOT) && abs >= I.slot_abs[host] &&
+      abs + len <= I.slot_abs[host] + I.slot_len[host])
+    return true;
+  return false;
+}
+
+EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
+  // ---- select_gt_groups (queues.hpp:220-263) ----
+  int32_t nsel = 0, nselg = 0, whole = 0;
+  if (I.free_total > 0) {
+    Tok remaining = I.free_total;
+    int32_t gi = 0;
+    while (gi < I.G) {
+      const int32_t g = I.gq[gi];
+      LANE0(I.exam_count++);
+      const Tok total = I.gr_dem[g];
+      if (total <= remaining) {
+        remaining -= total;
+        if (LANE == 0) {
+          I.selg_start[nselg] = nsel;
+          I.selg_rl[nselg] = I.gr_rl[g];
+          int32_t m = I.gr_head[g];
+          for (int32_t i = 0; i < I.gr_cnt[g]; ++i) { I.sel_ids[nsel + i] = m; m = I.gt_next[m]; }
+        }
+        WSYNC();
+        nsel += I.gr_cnt[g];
+        nselg++;
+        whole++;
+        gi++;
+        continue;
+      }
+      int32_t taken = 0, m = I.gr_head[g];
+      Tok pd = 0;
+      if (LANE == 0) {
+        while (m >= 0) {
+          const Tok d = I.dem[m];
+          I.exam_count++;
+          if (pd + d > remaining) break;
+          pd += d;
+          I.sel_ids[nsel + taken] = m;
+          taken++;
+          m = I.gt_next[m];
+        }
+      }
+      taken = shfl(taken, 0);
+      m = shfl(m, 0);
+      pd = shfl(pd, 0);
+      if (taken > 0) {
+        LANE0(I.selg_start[nselg] = nsel; I.selg_rl[nselg] = I.gr_rl[g];
+              I.gr_head[g] = m; I.gr_cnt[g] -= taken; I.gr_dem[g] -= pd);
+        nsel += taken;
+        nselg++;
+        remaining -= pd;
+      }
+      break;
+    }
+    if (whole > 0) {
+      for (int32_t i = LANE; i < whole; i += W) {
+        const int32_t g = I.gq[i];
+        rl_set(I, I.gr_rl[g], -1);
+      }
+      WSYNC();
+      if (LANE == 0)
+        for (int32_t i = 0; i < whole; ++i) I.grp_free[I.grp_free_top++] = I.gq[i];
+      WSYNC();
+      arr_erase(I.gq, I.G, 0, whole);
+      LANE0(I.G -= whole);
+    }
+  }
+  LANE0(I.selg_start[nselg] = nsel);
+  for (int32_t i = 0; i < nsel; ++i) {
+    schedule_gt_member(I, I.sel_ids[i]);
+    if (I.error) return;
+  }
+
+  // ---- KVC pipelining (econoserve-full, engine.hpp:273-297) ----
+  if (I.full && nselg > 0) {
+    int32_t nm = 0;  // host members flattened into tmp_b/tmp_c, group bounds in tmp_a
+    for (int32_t gi = 0; gi < nselg; ++gi) {
+      if (LANE == 0) {
+        I.tmp_a[gi] = nm;
+        for (int32_t i = I.selg_start[gi]; i < I.selg_start[gi + 1]; ++i) {
+          const int32_t id = I.sel_ids[i];
+          if (I.generated[id] == 0 && I.reg_cnt[id] == 1) {
+            I.tmp_b[nm] = id;
+            I.tmp_c[nm] = I.rg_start[I.reg_head[id]] + I.prompt[id];
+            nm++;
+          }
+        }
+      }
+      nm = shfl(nm, 0);
+      WSYNC();
+    }
+    LANE0(I.tmp_a[nselg] = nm);
+    if (nm > 0 && I.G > 0) {
+      int64_t exams = 0;
+      int32_t nout = 0;
+      for (int32_t gi = 0; gi < nselg; ++gi) {
+        const int32_t hs = I.tmp_a[gi], he = I.tmp_a[gi + 1];
+        nout = plan_host_group(I, I.selg_rl[gi], hs, he, nout, &exams);
+        if (I.error) return;
+      }
+      LANE0(I.exam_count += exams);
+      for (int32_t i = 0; i < nout; ++i) {
+        const int32_t host = I.os_host[i], hosted = I.os_hosted[i];
+        const int32_t abs = I.os_abs[i], len = I.os_len[i];
+        if (!slot_fits(I, host, abs, len)) { set_error(I, ERR_SLOT_OUTSIDE, hosted, 0); return; }
+        if (I.n_slots >= I.slot_cap) { set_error(I, ERR_TABLE_OVERFLOW, hosted, 6); return; }
+        if (LANE == 0) {
+          I.slot_host[hosted] = host;
+          I.slot_off[hosted] = I.os_off[i];
+          I.slot_len[hosted] = len;
+          I.slot_abs[hosted] = abs;
+          I.flags[hosted] |= F_HAS_SLOT;
+          I.slots[I.n_slots++] = hosted;
+          I.hosted_total++;
+          begin_gt_run(I, hosted, true);
+          I.gt_scheduled++;
+        }
+        logev(I, ECONO_EV_HOSTED, hosted, host, I.os_off[i]);
+        WSYNC();
+      }
+    }
+  }
+
+  // ---- PT batching (engine.hpp:299-324, queues.hpp:279-299) ----
+  const Tok tfs_rem = I.tfs - (Tok)I.R;
+  const Tok rfree = I.reserve_cap - I.reserved_used;
+  const Tok C0 = tmin(tfs_rem, rfree);
+  int32_t npt = 0;
+  if (I.pt_count > 0) {
+    // pt_admittable (engine.hpp:301-307): some queued prompt fits both budgets
+    bool adm = false;
+    if (C0 >= 1) {
+      if (I.ordered) {
+        for (int b = 0; b < I.nbuckets && !adm; ++b) adm = bm_prev(I, b, C0) >= 1;
+      } else {
+        adm = I.tree[I.tree_off[I.tree_levels - 1]] <= C0;
+      }
+    }
+    if (adm) LANE0(I.pt_admittable = 1);
+    if (tfs_rem > 0 && rfree > 0) {
+      LANE0(I.exam_count += I.pt_count);
+      Tok C = C0;  // both budgets drop by p: take iff p <= min(budgets)
+      if (I.ordered) {
+        for (int b = 0; b < I.nbuckets && C > 0; ++b) {
+          Tok x = C;
+          for (;;) {
+            const int p = bm_prev(I, b, x);
+            if (p < 1) break;
+            const int32_t cnt = I.cls_cnt[cls_of(I, b, p)];
+            const Tok fit = C / p;
+            const int32_t k = (int32_t)(fit < cnt ? fit : cnt);
+            npt = cls_take(I, b, p, k, I.tmp_a, npt);
+            C -= (Tok)k * p;
+            x = tmin((Tok)p - 1, C);
+            if (x < 1) break;
+          }
+        }
+      } else {
+        int64_t pos = 0;
+        while (C > 0) {
+          const int32_t id = tree_first(I, pos, C);
+          if (id < 0) break;
+          LANE0(I.tmp_a[npt] = id; I.pt_count--);
+          npt++;
+          C -= I.prompt[id];
+          tree_set(I, id, INF32);
+          pos = (int64_t)id + 1;
+        }
+      }
+    }
+    if (npt == 0 && I.pt_count > 0 && I.R == 0) {  // starvation guard (engine.hpp:314-323)
+      if (I.ordered) {
+        for (int b = 0; b < I.nbuckets; ++b) {
+          const int p = bm_prev(I, b, rfree);
+          if (p >= 1) { npt = cls_take(I, b, p, 1, I.tmp_a, npt); break; }
+        }
+      } else {
+        const int32_t id = tree_first(I, 0, rfree);
+        if (id >= 0) {
+          LANE0(I.tmp_a[0] = id; I.pt_count--);
+          npt = 1;
+          tree_set(I, id, INF32);
+        }
+      }
+    }
+  }
+  dispatch_pts(I, npt);
+}
+
+EDEVNI void vacate_slot(Inst& I, int32_t id, bool* rehomed) {  // engine.hpp:888-902
+  const Tok in_slot = tmin((Tok)I.generated[id] - I.gen_epoch[id], (Tok)I.padded[id]);
+  bool rh = false;
+  if (in_slot > 0 && kvc_draw_reserved(I, id, in_slot)) {
+    rh = true;
+  } else if (in_slot > 0) {
+    LANE0(const Tok w = I.written[id]; const Tok d = tmin(in_slot, w);
+          I.written[id] -= (int32_t)d; I.written_total -= d; I.occupied[id] -= (int32_t)in_slot);
+  }
+  kvc_remove_slot(I, id);
+  LANE0(I.flags[id] &= ~F_HOSTED);
+  *rehomed = rh;
+}
+
+EDEVNI void preempt_and_regroup(Inst& I, int32_t id, int why) {  // engine.hpp:904-928
+  if (LANE == 0) {
+    I.preempt_count[id]++;
+    I.state[id] = ST_PREEMPTED;
+    const Tok remaining = (Tok)I.true_rl[id] - I.generated[id];
+    I.predicted[id] = (int32_t)predict_rl(I, remaining, I.pmt, I.pmt_i);
+    I.padded[id] = (int32_t)apply_padding(I.predicted[id], I.pred_pad);
+    I.flags[id] |= F_WAS_PREEMPTED;
+    I.last_enq[id] = I.clock;
+  }
+  WSYNC();
+  logev(I, ECONO_EV_PREEMPT, id, why, I.padded[id]);
+  LANE0(I.state[id] = ST_WAITING_GT);
+  group_insert_gt(I, id, I.padded[id], I.slo[id], I.occupied[id], I.clock);
+}
+
+EDEVNI void handle_underprediction(Inst& I, int32_t id) {  // engine.hpp:856-873
+  if (kvc_draw_reserved(I, id, I.block)) {
+    LANE0(I.allowance[id] += (int32_t)I.block; I.reserve_draws[id]++;
+          I.penalty[id] += I.reserve_penalty);
+    logev(I, ECONO_EV_RESERVE_TOPUP, id, 0, 0);
+    WSYNC();
+    return;
+  }
+  LANE0(I.flags[id] |= F_ALLOC_FAIL; I.alloc_failures++);
+  bool rehomed = true;
+  if (I.flags[id] & F_HOSTED) vacate_slot(I, id, &rehomed);
+  LANE0(I.penalty[id] += rehomed ? I.pen_free : I.pen_offload);
+  preempt_and_regroup(I, id, 0);
+}
+
+EDEVNI void handle_hosted_overrun(Inst& I, int32_t id) {  // engine.hpp:875-884
+  LANE0(I.hosted_overruns++);
+  bool rehomed = false;
+  vacate_slot(I, id, &rehomed);
+  LANE0(I.penalty[id] += rehomed ? I.pen_free : I.pen_offload; I.flags[id] |= F_ALLOC_FAIL;
+        I.alloc_failures++);
+  logev(I, ECONO_EV_HOSTED_OVERRUN, id, 0, 0);
+  WSYNC();
+  preempt_and_regroup(I, id, 1);
+}
+
+// Stable compaction of the running list to RUNNING requests.
+EDEV void run_compact(Inst& I) {
+  int32_t w = 0;
+  for (int32_t base = 0; base < I.R; base += W) {
+    const int32_t i = base + LANE;
+    const int32_t id = i < I.R ? I.run[i] : -1;
+    const bool keep = id >= 0 && I.state[id] == ST_RUNNING;
+    const unsigned m = BALLOT(keep);
+    WSYNC();
+    if (keep) I.run[w + POPC(m & LANEMASK_LT)] = id;
+    w += POPC(m);
+    WSYNC();
+  }
+  LANE0(I.R = w);
+}
+
+EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
+  const double dt = iteration_time(I, fs) + 0.0;
+  LANE0(I.clock += dt; I.iter++);
+  const double sched = (double)I.exam_count * I.sched_cost;
+  if (I.n_adm > 0 && sched > 0.0) {
+    const double share = sched / (double)I.n_adm;
+    for (int32_t i = LANE; i < I.n_adm; i += W) I.sched_share[I.adm[i]] += share;
+  }
+  // prefill + decode progress (per-request updates are independent)
+  Tok wsum_pt = 0;
+  for (int32_t i = LANE; i < I.n_ptiter; i += W) {
+    const int32_t id = I.ptiter_id[i];
+    const int32_t tk = I.ptiter_tok[i];
+    I.exec_t[id] += dt;
+    I.prefill_done[id] += tk;
+    I.written[id] += tk;
+    I.occupied[id] += tk;
+    wsum_pt += tk;
+    if (I.prefill_done[id] >= I.prompt[id]) I.flags[id] |= F_PREFILL_FIN;
+  }
+  for (int32_t i = LANE; i < I.R; i += W) {
+    const int32_t id = I.run[i];
+    I.exec_t[id] += dt;
+    const int32_t g = ++I.generated[id];
+    I.occupied[id]++;
+    I.written[id]++;
+    if (g == 1 && I.first_tok[id] < 0.0) I.first_tok[id] = I.clock;
+  }
+  wsum_pt = wsum(wsum_pt);
+  LANE0(I.written_total += wsum_pt + I.R);
+  EconoSample s;
+  s.iter = I.iter;
+  s.clock = I.clock;
+  s.dt = dt;
+  s.forward_size = fs;
+  s.kvc_written_frac = (double)I.written_total / (double)I.capacity;
+  s.kvc_allocated_frac = (double)((I.general_cap - I.free_total) + I.reserved_used) / (double)I.capacity;
+  s.completed = 0;
+  s.pts_admitted = I.pts_admitted_iter;
+  s.pt_admittable = I.pt_admittable;
+  s._pad = 0;
+  s.idle_repeat = 0;
+  // completions, in running order (engine.hpp:784-791)
+  int32_t completed_now = 0;
+  for (int32_t base = 0; base < I.R; base += W) {
+    const int32_t i = base + LANE;
+    const int32_t id = i < I.R ? I.run[i] : -1;
+    unsigned m = BALLOT(id >= 0 && I.generated[id] >= I.true_rl[id]);
+    while (m) {
+      const int l = FFS(m);
+      m &= m - 1;
+      const int32_t cid = shfl(id, l);
+      LANE0(I.state[cid] = ST_DONE; I.compl_clock[cid] = I.clock);
+      kvc_release(I, cid);
+      if (I.error) return;
+      LANE0(I.occupied[cid] = 0; I.completed++);
+      logev(I, ECONO_EV_COMPLETE, cid, I.generated[cid], 0);
+      WSYNC();
+      completed_now++;
+    }
+  }
+  if (completed_now) run_compact(I);
+  // prefill transitions (engine.hpp:794-809)
+  for (int32_t i = 0; i < I.n_ptiter; ++i) {
+    const int32_t id = I.ptiter_id[i];
+    if (!(I.flags[id] & F_PREFILL_FIN)) continue;
+    LANE0(I.flags[id] &= ~F_PREFILL_FIN);
+    if (I.state[id] != ST_RUNNING) continue;
+    LANE0(I.state[id] = ST_WAITING_GT; I.last_enq[id] = I.clock);
+    group_insert_gt(I, id, I.padded[id], I.slo[id], I.occupied[id], I.clock);
+    logev(I, ECONO_EV_PREFILL_DONE, id, 0, 0);
+    WSYNC();
+    if (I.error) return;
+  }
+  // under-prediction (engine.hpp:812-817): candidates fixed up front, handled in order
+  int32_t npre = 0;
+  for (int32_t base = 0; base < I.R; base += W) {
+    const int32_t i = base + LANE;
+    const int32_t id = i < I.R ? I.run[i] : -1;
+    const bool c = id >= 0 && I.generated[id] >= I.allowance[id] && I.generated[id] < I.true_rl[id];
+    const unsigned m = BALLOT(c);
+    if (c) I.tmp_a[npre + POPC(m & LANEMASK_LT)] = id;
+    npre += POPC(m);
+  }
+  WSYNC();
+  for (int32_t k = 0; k < npre; ++k) {
+    const int32_t id = I.tmp_a[k];
+    if (I.state[id] != ST_RUNNING) continue;
+    handle_underprediction(I, id);
+    if (I.error) return;
+  }
+  // hosted-slot deadlines over a copy of the slot list (engine.hpp:819-828)
+  int32_t ncs = 0;
+  for (int32_t base = 0; base < I.n_slots; base += W) {
+    const int32_t si = base + LANE;
+    bool c = false;
+    int32_t h = -1;
+    if (si < I.n_slots) {
+      h = I.slots[si];
+      const int32_t host = I.slot_host[h];
+      c = I.state[host] == ST_RUNNING && (I.generated[host] - I.gen_epoch[host]) >= I.slot_off[h];
+    }
+    const unsigned m = BALLOT(c);
+    if (c) {
+      const int32_t o = ncs + POPC(m & LANEMASK_LT);
+      I.tmp_b[o] = h;
+      I.tmp_c[o] = I.slot_host[h];
+      I.tmp_a[I.scr_cap + o] = I.slot_off[h];
+    }
+    ncs += POPC(m);
+  }
+  WSYNC();
+  for (int32_t k = 0; k < ncs; ++k) {
+    const int32_t hosted = I.tmp_b[k], host = I.tmp_c[k];
+    if (I.state[host] != ST_RUNNING) continue;
+    if ((Tok)I.generated[host] - I.gen_epoch[host] < I.tmp_a[I.scr_cap + k]) continue;
+    if (I.state[hosted] == ST_DONE || !(I.flags[hosted] & F_HOSTED)) continue;
+    handle_hosted_overrun(I, hosted);
+    if (I.error) return;
+  }
+  if (npre || ncs) run_compact(I);
+  if (LANE == 0) {
+    s.completed = completed_now;
+    if (I.record_samples) {
+      if (I.sm_n < I.sm_cap) I.sm[I.sm_n] = s;
+      I.sm_n++;
+    }
+    I.executed++;
+    I.agg_fs += fs;
+    I.agg_written += s.kvc_written_frac;
+    I.agg_allocated += s.kvc_allocated_frac;
+    if ((double)fs >= 0.95 * (double)I.tfs) I.agg_tfs_hits++;
+    if (s.pts_admitted > 0) I.agg_pt_iters++;
+    I.hist[completed_now < I.hist_cap ? completed_now : I.hist_cap - 1]++;
+    I.n_ptiter = 0;
+    I.n_adm = 0;
+    I.exam_count = 0;
+    I.pts_admitted_iter = 0;
+    I.pt_admittable = 0;
+  }
+  WSYNC();
+}
+
+EDEVNI void handle_idle(Inst& I) {  // engine.hpp:930-961
+  if (I.arrival_cursor < I.n) {
+    const double next = I.arrival[I.arrival_cursor];
+    if (LANE == 0) {
+      long long k = 1;
+      if (next > I.clock) {
+        const long long c = (long long)ceil((next - I.clock) / I.t_base);
+        k = c > 1 ? c : 1;
+      }
+      const double dt = (double)k * I.t_base;
+      I.clock += dt;
+      I.iter += k;
+      if (I.record_samples) {
+        if (I.sm_n < I.sm_cap) {
+          EconoSample& s = I.sm[I.sm_n];
+          s.iter = I.iter;
+          s.clock = I.clock;
+          s.dt = dt;
+          s.forward_size = 0;
+          s.kvc_written_frac = (double)I.written_total / (double)I.capacity;
+          s.kvc_allocated_frac =
+              (double)((I.general_cap - I.free_total) + I.reserved_used) / (double)I.capacity;
+          s.completed = 0;
+          s.pts_admitted = 0;
+          s.pt_admittable = 0;
+          s._pad = 0;
+          s.idle_repeat = k;
+        }
+        I.sm_n++;
+      }
+      I.err_val = k;
+    }
+    WSYNC();
+    logev(I, ECONO_EV_IDLE, -1, I.err_val, 0);
+    LANE0(I.err_val = 0);
+    return;
+  }
+  int32_t stuck = -1;  // first request not done (engine.hpp:951-960)
+  for (int32_t base = 0; base < I.n && stuck < 0; base += W) {
+    const int32_t i = base + LANE;
+    const unsigned m = BALLOT(i < I.n && I.state[i] != ST_DONE);
+    if (m) stuck = base + FFS(m);
+  }
+  set_error(I, ERR_STUCK, stuck, 0);
+}
+
+// Worst-case events one step can append (arrivals + every bounded list), so
+// a launch stops and lets the host drain before a step could overflow.
+EDEV int64_t step_event_bound(const Inst& I) {
+  int64_t arrivals = 0;
+  if (I.arrival_cursor < I.n) {
+    const double lim = I.clock + 1e-12;
+    int64_t lo = I.arrival_cursor, hi = I.n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (I.arrival[mid] <= lim) lo = mid + 1; else hi = mid;
+    }
+    arrivals = lo - I.arrival_cursor;
+  }
+  return arrivals + 2 * I.tfs + 4 * (I.arrival_cursor - I.completed - I.pt_count) + 2 * (int64_t)I.n_slots + 64;
+}
+
+EDEVNI void engine_step(Inst& I) {  // Engine::step (engine.hpp:104-116)
+  ingest(I);
+  form_econoserve(I);
+  if (I.error) return;
+  Tok fs = 0;
+  for (int32_t i = LANE; i < I.n_ptiter; i += W) fs += I.ptiter_tok[i];
+  fs = wsum(fs) + I.R;
+  if (fs == 0) handle_idle(I); else execute_iteration(I, fs);
+  LANE0(I.steps++);
+}
+
+}  // namespace econo

@@ -1,0 +1,1358 @@
+// runtime.cu — host runtime and C-ABI (include/econoserve_b200.h) around the
+// on-device EconoServe engine (engine.cuh).
+//
+// Product build: nvcc -gencode arch=compute_100a,code=sm_100a (see
+// __graft_entry__.build). Every instance is one warp (one CTA) of
+// k_engine_steps; the host only sizes memory, launches, drains the optional
+// event/sample logs, and formats errors. There is no CPU execution path: if
+// the device is unavailable econo_create returns ECONO_ECUDA.
+//
+// ECONO_HOSTSIM (test-only, built by tests/hostsim.py with g++): the same
+// engine source compiled for the host with one lane per "warp", used to check
+// the engine logic against the oracle on machines without a GPU.
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "engine.cuh"
+
+#ifndef ECONO_HOSTSIM
+#include <cuda_runtime.h>
+#endif
+
+using namespace econo;
+
+static_assert(sizeof(Inst) % 8 == 0, "Inst must be 8-byte granular");
+
+// ---------------------------------------------------------------------------
+// device entry points
+// ---------------------------------------------------------------------------
+namespace econo {
+
+// init_requests (engine.hpp:165-209) + empty queue / allocator state.
+EDEVNI void engine_init(Inst& I) {
+  const int32_t n = I.n;
+  // arrival order (engine.hpp:167-169)
+  for (int32_t base = 1; base < n; base += W) {
+    const int32_t i = base + LANE;
+    const unsigned m = BALLOT(i < n && I.arrival[i] < I.arrival[i - 1]);
+    if (m) { set_error(I, ERR_ARRIVAL_ORDER, base + FFS(m), 0); return; }
+  }
+  // mean prompt: an exact integer sum equals the reference's sequential
+  // double sum of integers (engine.hpp:171-174) while below 2^53.
+  int64_t ps = 0;
+  for (int32_t i = LANE; i < n; i += W) ps += I.prompt[i];
+  ps = wsum(ps);
+  const Tok mean_prompt = tmax(1, (Tok)llround((double)ps / (double)n));
+  LANE0(I.t_p = iteration_time(I, mean_prompt); I.t_g = iteration_time(I, I.tfs));
+  // predictions consume pred_rng_ in id order (engine.hpp:187-188)
+  if (I.pred_model == ECONO_PRED_ORACLE) {
+    for (int32_t i = LANE; i < n; i += W) I.predicted[i] = (int32_t)quantize_up(I.true_rl[i], I.pred_quantum);
+  } else if (LANE == 0) {
+    for (int32_t i = 0; i < n; ++i) I.predicted[i] = (int32_t)predict_rl(I, I.true_rl[i], I.pmt, I.pmt_i);
+  }
+  WSYNC();
+  int32_t bad = INF32;
+  int code = ERR_NONE;
+  for (int32_t i = LANE; i < n; i += W) {
+    I.padded[i] = (int32_t)apply_padding(I.predicted[i], I.pred_pad);
+    I.slo[i] = I.arrival[i] + I.slo_scale * (I.t_p + I.t_g * (double)I.true_rl[i]);
+    I.state[i] = ST_WAITING_PT;
+    I.dispatch_t[i] = -1.0;
+    I.first_tok[i] = -1.0;
+    I.compl_clock[i] = -1.0;
+    I.reg_head[i] = -1;
+    I.reg_tail[i] = -1;
+    I.pt_next[i] = -1;
+    I.gt_next[i] = -1;
+    const Tok worst = block_round((Tok)I.prompt[i] + tmax(I.true_rl[i], I.padded[i]), I.block);
+    if (bad == INF32 && (worst > I.general_cap || (Tok)I.prompt[i] > I.reserve_cap)) {
+      bad = i;
+      code = worst > I.general_cap ? ERR_INFEASIBLE_KVC : ERR_INFEASIBLE_RESERVE;
+    }
+  }
+  const int32_t first_bad = wmin(bad);
+  if (first_bad != INF32) {
+    if (bad == first_bad) {
+      const Tok worst = block_round((Tok)I.prompt[bad] + tmax(I.true_rl[bad], I.padded[bad]), I.block);
+      I.error = code;
+      I.err_id = bad;
+      I.err_val = code == ERR_INFEASIBLE_KVC ? worst : I.reserve_cap;
+    }
+    WSYNC();
+    return;
+  }
+  // allocator / queue tables
+  for (int32_t i = LANE; i < I.reg_cap; i += W) I.reg_free[i] = I.reg_cap - 1 - i;
+  for (int32_t i = LANE; i < I.grp_cap; i += W) I.grp_free[i] = I.grp_cap - 1 - i;
+  for (int32_t i = LANE; i < I.rl_cap; i += W) I.rl_map[i] = -1;
+  if (I.ordered) {
+    const int64_t nc = (int64_t)I.nbuckets * (I.pmax + 1);
+    for (int64_t i = LANE; i < nc; i += W) { I.cls_head[i] = -1; I.cls_tail[i] = -1; }
+  } else {
+    const int64_t tn = I.tree_off[I.tree_levels - 1] + 1;
+    for (int64_t i = LANE; i < tn; i += W) I.tree[i] = INF32;
+  }
+  LANE0(I.reg_free_top = I.reg_cap; I.grp_free_top = I.grp_cap; I.next_group_id = 1);
+}
+
+// Engine::run()'s loop body, up to max_steps times (engine.hpp:118-122).
+EDEVNI void engine_steps(Inst& I, int64_t max_steps) {
+  LANE0(I.status = STATUS_RUN);
+  for (int64_t s = 0; s < max_steps; ++s) {
+    if (I.error || I.completed >= I.n) break;
+    if ((I.record_events && I.ev_n + step_event_bound(I) > I.ev_cap) ||
+        (I.record_samples && I.sm_n + 1 > I.sm_cap)) {
+      LANE0(I.status = STATUS_DRAIN);
+      break;
+    }
+    engine_step(I);
+  }
+}
+
+// finalize() per-request records (engine.hpp:963-984), one lane per request.
+EDEV void engine_record(const Inst& I, int32_t i, EconoRecord& rc) {
+  rc.id = i;
+  rc.preempt_count = I.preempt_count[i];
+  rc.arrival = I.arrival[i];
+  const double extra = I.penalty[i] + I.sched_share[i];
+  rc.completion_time = I.compl_clock[i] + extra;
+  rc.first_token_time = I.first_tok[i];
+  rc.waiting_time = I.waiting[i];
+  rc.execution_time = I.exec_t[i];
+  rc.preemption_time = I.preempt_t[i] + I.penalty[i];
+  rc.scheduling_time_share = I.sched_share[i];
+  rc.reserve_draws = I.reserve_draws[i];
+  rc.met_slo = rc.completion_time <= I.slo[i];
+  rc.prompt_len = I.prompt[i];
+  rc.true_rl = I.true_rl[i];
+  rc.slo_deadline = I.slo[i];
+  rc.alloc_failure = (I.flags[i] & F_ALLOC_FAIL) ? 1 : 0;
+  rc._pad = 0;
+}
+
+// Per-instance metric partial sums (metrics.hpp:110-173) for the cross-GPU
+// reduction: [0]=n [1]=sum jct [2]=sum tbt [3]=tbt_n [4]=sum jct/true_rl
+// [5]=met [6]=tokens [7]=preemptions [8]=reserve_draws [9]=alloc failures
+// [10]=max completion [11..14]=sum waiting/execution/preemption/scheduling
+// [15]=executed iters [16]=sum fs [17]=sum written frac [18]=sum allocated
+// frac [19]=tfs hits [20]=pt iters [21]=hosted slots [22]=hosted overruns
+// [23]=completed [24]=pt dispatched [25]=gt scheduled [26]=steps [27]=iter.
+EDEV void engine_partials(const Inst& I, double* out) {
+  double acc[15];
+  for (int k = 0; k < 15; ++k) acc[k] = 0.0;
+  for (int32_t i = LANE; i < I.n; i += W) {
+    EconoRecord rc;
+    engine_record(I, i, rc);
+    const double jct = rc.completion_time - rc.arrival;
+    acc[0] += 1.0;
+    acc[1] += jct;
+    if (rc.true_rl >= 2 && rc.first_token_time >= 0.0) {
+      acc[2] += (rc.completion_time - rc.first_token_time) / (double)(rc.true_rl - 1);
+      acc[3] += 1.0;
+    }
+    acc[4] += jct / (double)rc.true_rl;
+    acc[5] += rc.met_slo ? 1.0 : 0.0;
+    acc[6] += (double)rc.true_rl;
+    acc[7] += rc.preempt_count;
+    acc[8] += rc.reserve_draws;
+    acc[9] += rc.alloc_failure;
+    acc[10] = rc.completion_time > acc[10] ? rc.completion_time : acc[10];
+    acc[11] += rc.waiting_time;
+    acc[12] += rc.execution_time;
+    acc[13] += rc.preemption_time;
+    acc[14] += rc.scheduling_time_share;
+  }
+  for (int k = 0; k < 15; ++k) {
+    if (k == 10) {
+      double v = acc[k];
+      for (int o = W / 2; o > 0; o >>= 1) { const double x = shfl_xor(v, o); v = x > v ? x : v; }
+      acc[k] = v;
+    } else {
+      acc[k] = wsum(acc[k]);
+    }
+  }
+  if (LANE == 0) {
+    for (int k = 0; k < 15; ++k) out[k] = acc[k];
+    out[15] = (double)I.executed;
+    out[16] = (double)I.agg_fs;
+    out[17] = I.agg_written;
+    out[18] = I.agg_allocated;
+    out[19] = (double)I.agg_tfs_hits;
+    out[20] = (double)I.agg_pt_iters;
+    out[21] = (double)I.hosted_total;
+    out[22] = (double)I.hosted_overruns;
+    out[23] = (double)I.completed;
+    out[24] = (double)I.pt_dispatched;
+    out[25] = (double)I.gt_scheduled;
+    out[26] = (double)I.steps;
+    out[27] = (double)I.iter;
+    for (int k = 28; k < ECONO_PARTIAL_WORDS; ++k) out[k] = 0.0;
+  }
+}
+
+}  // namespace econo
+
+#ifndef ECONO_HOSTSIM
+// Inst staged in shared memory for the launch; one warp per instance.
+__device__ __forceinline__ void inst_load(Inst& s, const Inst* g) {
+  const uint64_t* src = reinterpret_cast<const uint64_t*>(g);
+  uint64_t* dst = reinterpret_cast<uint64_t*>(&s);
+  for (int i = threadIdx.x; i < (int)(sizeof(Inst) / 8); i += 32) dst[i] = src[i];
+  __syncwarp();
+}
+__device__ __forceinline__ void inst_store(Inst* g, const Inst& s) {
+  __syncwarp();
+  const uint64_t* src = reinterpret_cast<const uint64_t*>(&s);
+  uint64_t* dst = reinterpret_cast<uint64_t*>(g);
+  for (int i = threadIdx.x; i < (int)(sizeof(Inst) / 8); i += 32) dst[i] = src[i];
+}
+
+__global__ void __launch_bounds__(32) k_engine_init(Inst* insts, const EconoTraceRecord* const* traces,
+                                                    const uint64_t* seeds) {
+  __shared__ Inst I;
+  inst_load(I, &insts[blockIdx.x]);
+  const EconoTraceRecord* tr = traces[blockIdx.x];
+  double* arr = const_cast<double*>(I.arrival);
+  int32_t* pr = const_cast<int32_t*>(I.prompt);
+  int32_t* rl = const_cast<int32_t*>(I.true_rl);
+  for (int32_t i = threadIdx.x; i < I.n; i += 32) {
+    arr[i] = tr[i].arrival_time;
+    pr[i] = (int32_t)tr[i].prompt_len;
+    rl[i] = (int32_t)tr[i].true_rl;
+  }
+  if (threadIdx.x == 0) {
+    mt_seed(I.mt, I.mt_i, seeds[2 * blockIdx.x]);
+    mt_seed(I.pmt, I.pmt_i, seeds[2 * blockIdx.x + 1]);
+  }
+  __syncwarp();
+  engine_init(I);
+  inst_store(&insts[blockIdx.x], I);
+}
+
+__global__ void __launch_bounds__(32) k_engine_steps(Inst* insts, int64_t max_steps) {
+  __shared__ Inst I;
+  inst_load(I, &insts[blockIdx.x]);
+  engine_steps(I, max_steps);
+  inst_store(&insts[blockIdx.x], I);
+}
+
+__global__ void k_engine_records(const Inst* inst, EconoRecord* out) {
+  const Inst& I = *inst;
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < I.n; i += gridDim.x * blockDim.x) {
+    EconoRecord rc;
+    // one thread per request: same arithmetic as engine_record
+    rc.id = i;
+    rc.preempt_count = I.preempt_count[i];
+    rc.arrival = I.arrival[i];
+    const double extra = I.penalty[i] + I.sched_share[i];
+    rc.completion_time = I.compl_clock[i] + extra;
+    rc.first_token_time = I.first_tok[i];
+    rc.waiting_time = I.waiting[i];
+    rc.execution_time = I.exec_t[i];
+    rc.preemption_time = I.preempt_t[i] + I.penalty[i];
+    rc.scheduling_time_share = I.sched_share[i];
+    rc.reserve_draws = I.reserve_draws[i];
+    rc.met_slo = rc.completion_time <= I.slo[i];
+    rc.prompt_len = I.prompt[i];
+    rc.true_rl = I.true_rl[i];
+    rc.slo_deadline = I.slo[i];
+    rc.alloc_failure = (I.flags[i] & F_ALLOC_FAIL) ? 1 : 0;
+    rc._pad = 0;
+    out[i] = rc;
+  }
+}
+
+__global__ void __launch_bounds__(32) k_engine_partials(const Inst* insts, double* out) {
+  engine_partials(insts[blockIdx.x], out + (size_t)blockIdx.x * ECONO_PARTIAL_WORDS);
+}
+#endif
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+
+void set_err(char* err, size_t errlen, const char* fmt, ...) {
+  if (!err || !errlen) return;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(err, errlen, fmt, ap);
+  va_end(ap);
+}
+
+#ifdef ECONO_HOSTSIM
+int dev_alloc(void** p, size_t sz) { *p = calloc(1, sz ? sz : 8); return *p ? 0 : 1; }
+void dev_free(void* p) { free(p); }
+int dev_h2d(void* d, const void* h, size_t sz) { memcpy(d, h, sz); return 0; }
+int dev_d2h(void* h, const void* d, size_t sz) { memcpy(h, d, sz); return 0; }
+#else
+int dev_alloc(void** p, size_t sz) {
+  if (cudaMalloc(p, sz ? sz : 8) != cudaSuccess) return 1;
+  return cudaMemset(*p, 0, sz ? sz : 8) != cudaSuccess;
+}
+void dev_free(void* p) { if (p) cudaFree(p); }
+int dev_h2d(void* d, const void* h, size_t sz) { return cudaMemcpy(d, h, sz, cudaMemcpyHostToDevice) != cudaSuccess; }
+int dev_d2h(void* h, const void* d, size_t sz) { return cudaMemcpy(h, d, sz, cudaMemcpyDeviceToHost) != cudaSuccess; }
+#endif
+
+struct Arena {  // bump allocator over one device allocation, 256-byte aligned
+  size_t off = 0;
+  char* base = nullptr;
+  template <class T>
+  T* take(int64_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += sizeof(T) * (size_t)(count > 0 ? count : 1);
+    return p;
+  }
+};
+
+int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// Lays out every SoA array of one instance; with base == nullptr it only sizes.
+void layout(Inst& I, char* base, size_t* bytes) {
+  Arena a;
+  a.base = base;
+  const int64_t n = I.n;
+  I.arrival = a.take<double>(n);
+  I.prompt = a.take<int32_t>(n);
+  I.true_rl = a.take<int32_t>(n);
+  int32_t** i32s[] = {&I.predicted, &I.padded, &I.generated, &I.occupied, &I.allowance, &I.gen_epoch,
+                      &I.prefill_done, &I.preempt_count, &I.reserve_draws, &I.held, &I.reg_head,
+                      &I.reg_tail, &I.reg_cnt, &I.reserved, &I.written, &I.slot_host, &I.slot_off,
+                      &I.slot_len, &I.slot_abs, &I.pt_next, &I.gt_next, &I.dem};
+  for (auto p : i32s) *p = a.take<int32_t>(n);
+  I.state = a.take<uint8_t>(n);
+  I.flags = a.take<uint8_t>(n);
+  double** f64s[] = {&I.slo, &I.waiting, &I.preempt_t, &I.exec_t, &I.dispatch_t, &I.first_tok,
+                     &I.compl_clock, &I.last_enq, &I.penalty, &I.sched_share};
+  for (auto p : f64s) *p = a.take<double>(n);
+  const int64_t rc = I.reg_cap;
+  I.rg_start = a.take<int32_t>(rc);
+  I.rg_len = a.take<int32_t>(rc);
+  I.rg_owner = a.take<int32_t>(rc);
+  I.rg_next = a.take<int32_t>(rc);
+  I.reg_free = a.take<int32_t>(rc);
+  I.addr = a.take<int32_t>(rc + W);
+  if (I.ordered) {
+    const int64_t nc = (int64_t)I.nbuckets * (I.pmax + 1);
+    I.cls_head = a.take<int32_t>(nc);
+    I.cls_tail = a.take<int32_t>(nc);
+    I.cls_cnt = a.take<int32_t>(nc);
+    I.bm1 = a.take<uint64_t>((int64_t)I.nbuckets * I.bm_words);
+    I.bm2 = a.take<uint64_t>((int64_t)I.nbuckets * I.bm_l2);
+  } else {
+    I.tree = a.take<int32_t>(I.tree_off[I.tree_levels - 1] + 1);
+  }
+  const int64_t gc = I.grp_cap;
+  I.gr_id = a.take<uint64_t>(gc);
+  I.gr_seq = a.take<uint64_t>(gc);
+  int32_t** g32[] = {&I.gr_rl, &I.gr_head, &I.gr_tail, &I.gr_cnt, &I.gr_db, &I.gr_kb, &I.gr_maxocc, &I.grp_free};
+  for (auto p : g32) *p = a.take<int32_t>(gc);
+  I.gq = a.take<int32_t>(gc + W);
+  I.rl_map = a.take<int32_t>(I.rl_cap);
+  I.gr_formed = a.take<double>(gc);
+  I.gr_mindl = a.take<double>(gc);
+  I.gr_dem = a.take<int64_t>(gc);
+  I.run = a.take<int32_t>(I.run_cap + W);
+  I.slots = a.take<int32_t>(I.slot_cap + W);
+  I.ptiter_id = a.take<int32_t>(I.ptiter_cap);
+  I.ptiter_tok = a.take<int32_t>(I.ptiter_cap);
+  I.adm = a.take<int32_t>(I.adm_cap);
+  I.sel_ids = a.take<int32_t>(n + 1);
+  I.selg_start = a.take<int32_t>(n + 2);
+  I.selg_rl = a.take<int32_t>(n + 2);
+  const int64_t pc = 2 * (int64_t)I.scr_cap + W;
+  int32_t** pl[] = {&I.wa_w, &I.wa_b, &I.wa_l, &I.wa_u, &I.wb_w, &I.wb_b, &I.wb_l, &I.wb_u,
+                    &I.cd_ri, &I.cd_abs, &I.cd_use, &I.cd_len, &I.assigned,
+                    &I.os_host, &I.os_hosted, &I.os_off, &I.os_len, &I.os_abs, &I.tmp_a, &I.tmp_b, &I.tmp_c};
+  for (auto p : pl) *p = a.take<int32_t>(pc);
+  I.mt = a.take<uint64_t>(312);
+  I.pmt = a.take<uint64_t>(312);
+  I.hist = a.take<int64_t>(I.hist_cap);
+  *bytes = a.off + 256;
+}
+
+// Rebases every pointer field of a copied Inst from one arena base to another.
+void rebase(Inst& I, const char* from, char* to, size_t bytes) {
+  char* fields = reinterpret_cast<char*>(&I.arrival);
+  char* end = reinterpret_cast<char*>(&I.hist) + sizeof(I.hist);
+  for (char* p = fields; p < end; p += sizeof(void*)) {
+    uintptr_t v;
+    memcpy(&v, p, sizeof(v));
+    if (v >= (uintptr_t)from && v < (uintptr_t)from + bytes) {
+      v = v - (uintptr_t)from + (uintptr_t)to;
+      memcpy(p, &v, sizeof(v));
+    }
+  }
+}
+
+const char* policy_name(int k) {
+  static const char* names[] = {"orca", "vllm", "sarathi", "multires", "sync-coupled",
+                                "econoserve-d", "econoserve-sd", "econoserve-sdo", "econoserve-full"};
+  return k >= 0 && k <= 8 ? names[k] : "?";
+}
+
+// Option validation in the reference constructor's order (engine.hpp:81-100).
+int validate(const EconoOptions* o, int64_t n, char* err, size_t errlen) {
+  const bool econo = o->policy >= ECONO_POLICY_ECONO_D && o->policy <= ECONO_POLICY_ECONO_FULL;
+  if (o->kvc_capacity < 1) return set_err(err, errlen, "kvc capacity must be >= 1"), ECONO_ECONFIG;
+  if (o->kvc_block_size < 1) return set_err(err, errlen, "kvc block_size must be >= 1"), ECONO_ECONFIG;
+  const double rf = econo ? o->reserved_fraction : 0.0;
+  if (rf < 0.0 || rf >= 1.0) return set_err(err, errlen, "reserved_fraction must be in [0, 1)"), ECONO_ECONFIG;
+  if (o->n_deadline_bounds < 0 || o->n_deadline_bounds > ECONO_MAX_BOUNDS || o->n_kvc_bounds < 0 ||
+      o->n_kvc_bounds > ECONO_MAX_BOUNDS || o->n_length_bounds < 0 || o->n_length_bounds > ECONO_MAX_BOUNDS)
+    return set_err(err, errlen, "ordering: at most %d bucket boundaries", ECONO_MAX_BOUNDS), ECONO_ECONFIG;
+  for (int i = 1; i < o->n_deadline_bounds; ++i)
+    if (o->deadline_bounds[i] < o->deadline_bounds[i - 1]) goto unordered;
+  for (int i = 1; i < o->n_kvc_bounds; ++i)
+    if (o->kvc_bounds[i] < o->kvc_bounds[i - 1]) goto unordered;
+  for (int i = 1; i < o->n_length_bounds; ++i)
+    if (o->length_bounds[i] < o->length_bounds[i - 1]) goto unordered;
+  if (o->tfs < 1) return set_err(err, errlen, "tfs must be >= 1"), ECONO_ECONFIG;
+  if (o->chunk_size < 1) return set_err(err, errlen, "chunk_size must be >= 1"), ECONO_ECONFIG;
+  if (o->batch_size_cap < 1) return set_err(err, errlen, "batch_size_cap must be >= 1"), ECONO_ECONFIG;
+  if (o->padding_ratio < 0.0) return set_err(err, errlen, "padding_ratio must be >= 0"), ECONO_ECONFIG;
+  if (o->reserved_fraction < 0.0 || o->reserved_fraction >= 1.0)
+    return set_err(err, errlen, "reserved_fraction must be in [0, 1)"), ECONO_ECONFIG;
+  if (o->buffer_ratio < 0.0) return set_err(err, errlen, "buffer_ratio must be >= 0"), ECONO_ECONFIG;
+  if (!(o->t_base > 0.0)) return set_err(err, errlen, "cost model: t_base must be > 0"), ECONO_ECONFIG;
+  if (!(o->t_token > 0.0)) return set_err(err, errlen, "cost model: t_token must be > 0"), ECONO_ECONFIG;
+  if (o->cost_tfs < 1) return set_err(err, errlen, "cost model: tfs must be >= 1"), ECONO_ECONFIG;
+  if (o->preempt_offload_penalty < 0.0 || o->preempt_free_penalty < 0.0 || o->reserve_penalty < 0.0 ||
+      o->sched_cost_per_exam < 0.0 || o->swap_stall < 0.0)
+    return set_err(err, errlen, "cost model: penalties must be >= 0"), ECONO_ECONFIG;
+  if (o->pred_sigma < 0.0) return set_err(err, errlen, "predictor sigma must be >= 0"), ECONO_ECONFIG;
+  if (o->pred_accuracy < 0.0 || o->pred_accuracy > 1.0)
+    return set_err(err, errlen, "predictor accuracy must be in [0,1]"), ECONO_ECONFIG;
+  if (o->pred_tolerance < 0.0) return set_err(err, errlen, "predictor tolerance must be >= 0"), ECONO_ECONFIG;
+  if (o->pred_padding_ratio < 0.0) return set_err(err, errlen, "padding_ratio must be >= 0"), ECONO_ECONFIG;
+  if (o->pred_quantum < 1) return set_err(err, errlen, "predictor quantum must be >= 1"), ECONO_ECONFIG;
+  if (n <= 0) return set_err(err, errlen, "trace is empty"), ECONO_ECONFIG;
+  if (!econo)
+    return set_err(err, errlen,
+                   "policy '%s' is outside the B200 scheduling path (econoserve-d/-sd/-sdo/-full only)",
+                   policy_name(o->policy)),
+           ECONO_ECONFIG;
+  if (o->kvc_capacity >= (int64_t)1 << 30)
+    return set_err(err, errlen, "kvc capacity must be < 2^30 tokens on the device path"), ECONO_ECONFIG;
+  return ECONO_OK;
+unordered:
+  return set_err(err, errlen, "ordering bucket boundaries must be increasing"), ECONO_ECONFIG;
+}
+
+// Fills configuration fields and capacities of an Inst from options + trace.
+int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t n, char* err, size_t errlen) {
+  memset(&I, 0, sizeof(I));
+  if (n >= (int64_t)1 << 31) return set_err(err, errlen, "trace longer than 2^31 requests"), ECONO_ECONFIG;
+  int64_t pmax = 1;
+  for (int64_t i = 0; i < n; ++i) {
+    if (t[i].prompt_len < 1 || t[i].prompt_len >= ((int64_t)1 << 30) || t[i].true_rl < 1 ||
+        t[i].true_rl >= ((int64_t)1 << 30))
+      return set_err(err, errlen, "request %lld: prompt_len and response_len must be in [1, 2^30)", (long long)i),
+             ECONO_ECONFIG;
+    pmax = imax(pmax, t[i].prompt_len);
+  }
+  I.n = (int32_t)n;
+  I.policy = o->policy;
+  I.ordered = o->policy == ECONO_POLICY_ECONO_SDO || o->policy == ECONO_POLICY_ECONO_FULL;
+  I.grouping = o->policy != ECONO_POLICY_ECONO_D;
+  I.full = o->policy == ECONO_POLICY_ECONO_FULL;
+  I.pred_model = o->pred_model;
+  I.nbd = o->n_deadline_bounds;
+  I.nbk = o->n_kvc_bounds;
+  for (int i = 0; i < ECONO_MAX_BOUNDS; ++i) {
+    I.dbounds[i] = o->deadline_bounds[i];
+    I.kbounds[i] = o->kvc_bounds[i];
+  }
+  I.record_events = o->record_events ? 1 : 0;
+  I.record_samples = o->record_samples ? 1 : 0;
+  I.tfs = o->tfs;  // cost_.tfs = pol_.tfs (engine.hpp:98)
+  I.capacity = o->kvc_capacity;
+  I.block = o->kvc_block_size;
+  I.reserve_cap = (int64_t)llround(o->reserved_fraction * (double)o->kvc_capacity);
+  I.general_cap = I.capacity - I.reserve_cap;
+  I.pred_quantum = o->pred_quantum;
+  I.t_base = o->t_base;
+  I.t_token = o->t_token;
+  I.over_rate = o->t_token_over < 0.0 ? o->t_token : o->t_token_over;
+  I.reserve_penalty = o->reserve_penalty;
+  I.pen_free = o->preempt_free_penalty;
+  I.pen_offload = o->preempt_offload_penalty;
+  I.sched_cost = o->sched_cost_per_exam;
+  I.pred_sigma = o->pred_sigma;
+  I.pred_accuracy = o->pred_accuracy;
+  I.pred_tol = o->pred_tolerance;
+  I.pred_pad = o->pred_padding_ratio;
+  I.slo_scale = o->slo_scale;
+  I.buffer_ratio = o->buffer_ratio;
+  I.free_total = I.general_cap;
+  // capacities
+  I.pmax = (int32_t)pmax;
+  I.nbuckets = I.nbd + 1;
+  I.bm_words = (I.pmax >> 6) + 1;
+  I.bm_l2 = (I.bm_words >> 6) + 1;
+  {
+    int64_t len = n, off = 0;
+    int lv = 0;
+    for (;;) {
+      I.tree_off[lv] = (int32_t)off;
+      I.tree_len[lv] = (int32_t)len;
+      off += len;
+      ++lv;
+      if (len == 1) break;
+      len = (len + 31) / 32;
+    }
+    I.tree_levels = lv;
+  }
+  const int64_t cap = I.capacity;
+  I.reg_cap = (int32_t)(I.general_cap + 2);
+  I.grp_cap = (int32_t)(n + 1);
+  I.slot_cap = (int32_t)(imin(n, cap) + 1);
+  I.run_cap = (int32_t)(imin(n, cap) + 1);
+  I.ptiter_cap = (int32_t)(imin(n, I.tfs) + 2);
+  I.adm_cap = (int32_t)(imin(n, cap + I.tfs) + 2);
+  I.scr_cap = (int32_t)(imax(n, I.general_cap) + 64);
+  I.hist_cap = (int32_t)(imin(n, cap) + 2);
+  I.rl_cap = (int32_t)(I.general_cap + 1);
+  return ECONO_OK;
+}
+
+std::string format_error(const Inst& I, int* code) {
+  char buf[512];
+  *code = ECONO_ESIM;
+  switch (I.error) {
+    case ERR_ALLOC_FAIL:
+      snprintf(buf, sizeof(buf), "exact allocation failed for scheduled request %d", I.err_id);
+      break;
+    case ERR_RESERVED_DRAW:
+      snprintf(buf, sizeof(buf), "reserved pool draw failed for selected PT %d", I.err_id);
+      break;
+    case ERR_SLOT_OUTSIDE:
+      snprintf(buf, sizeof(buf), "hosting slot outside the host's space");
+      break;
+    case ERR_STUCK:
+      snprintf(buf, sizeof(buf),
+               "simulation stuck: request %d can never be scheduled (demand exceeds what the "
+               "configuration can free)", I.err_id);
+      break;
+    case ERR_RELEASE_UNKNOWN:
+      snprintf(buf, sizeof(buf), "release: unknown id");
+      break;
+    case ERR_TABLE_OVERFLOW:
+      snprintf(buf, sizeof(buf), "device table overflow (site %lld, request %d)", (long long)I.err_val, I.err_id);
+      break;
+    case ERR_INFEASIBLE_KVC:
+      snprintf(buf, sizeof(buf), "request %d: KVC demand %lld exceeds usable capacity %lld", I.err_id,
+               (long long)I.err_val, (long long)I.general_cap);
+      break;
+    case ERR_INFEASIBLE_RESERVE:
+      snprintf(buf, sizeof(buf), "request %d: prompt does not fit the reserved pool (%lld tokens)", I.err_id,
+               (long long)I.reserve_cap);
+      break;
+    case ERR_ARRIVAL_ORDER:
+      *code = ECONO_ECONFIG;
+      snprintf(buf, sizeof(buf), "trace arrival times must be nondecreasing");
+      break;
+    default:
+      snprintf(buf, sizeof(buf), "unknown engine error %d", I.error);
+  }
+  return buf;
+}
+
+}  // namespace
+
+// One instance's host-side bookkeeping.
+struct HostInst {
+  Inst desc;           // mirror of the device descriptor (device pointers)
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  EconoEvent* d_ev = nullptr;
+  EconoSample* d_sm = nullptr;
+  std::vector<EconoEvent> events;
+  std::vector<EconoSample> samples;
+  std::vector<EconoTraceRecord> trace;
+  uint64_t seed = 1, pred_seed = 1;
+  int32_t policy = 0;
+};
+
+struct econo_batch {
+  int device = 0;
+  std::vector<HostInst> inst;
+  Inst* d_insts = nullptr;
+#ifndef ECONO_HOSTSIM
+  cudaStream_t stream = nullptr;
+#endif
+  std::vector<econo_engine*> views;
+};
+
+struct econo_engine {
+  econo_batch* b;
+  int32_t i;
+  bool owns;
+};
+
+namespace {
+
+int cuda_check(char* err, size_t errlen, const char* what) {
+#ifndef ECONO_HOSTSIM
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_err(err, errlen, "CUDA error in %s: %s", what, cudaGetErrorString(e));
+    return ECONO_ECUDA;
+  }
+#else
+  (void)err; (void)errlen; (void)what;
+#endif
+  return ECONO_OK;
+}
+
+int pull_descs(econo_batch* b) {
+  std::vector<Inst> tmp(b->inst.size());
+  if (dev_d2h(tmp.data(), b->d_insts, sizeof(Inst) * tmp.size())) return 1;
+  for (size_t i = 0; i < tmp.size(); ++i) b->inst[i].desc = tmp[i];
+  return 0;
+}
+int push_descs(econo_batch* b) {
+  std::vector<Inst> tmp(b->inst.size());
+  for (size_t i = 0; i < tmp.size(); ++i) tmp[i] = b->inst[i].desc;
+  return dev_h2d(b->d_insts, tmp.data(), sizeof(Inst) * tmp.size());
+}
+
+int ensure_logs(HostInst& h, int64_t ev_cap, int64_t sm_cap) {
+  Inst& I = h.desc;
+  if (I.record_events && ev_cap > I.ev_cap) {
+    dev_free(h.d_ev);
+    void* p;
+    if (dev_alloc(&p, sizeof(EconoEvent) * (size_t)ev_cap)) return 1;
+    h.d_ev = (EconoEvent*)p;
+    I.ev = h.d_ev;
+    I.ev_cap = ev_cap;
+  }
+  if (I.record_samples && sm_cap > I.sm_cap) {
+    dev_free(h.d_sm);
+    void* p;
+    if (dev_alloc(&p, sizeof(EconoSample) * (size_t)sm_cap)) return 1;
+    h.d_sm = (EconoSample*)p;
+    I.sm = h.d_sm;
+    I.sm_cap = sm_cap;
+  }
+  return 0;
+}
+
+// Copies logged events/samples to the host vectors and empties the device logs.
+int drain(HostInst& h) {
+  Inst& I = h.desc;
+  if (I.record_events && I.ev_n > 0) {
+    const int64_t k = imin(I.ev_n, I.ev_cap);
+    const size_t old = h.events.size();
+    h.events.resize(old + (size_t)k);
+    if (dev_d2h(h.events.data() + old, h.d_ev, sizeof(EconoEvent) * (size_t)k)) return 1;
+    I.ev_n = 0;
+  }
+  if (I.record_samples && I.sm_n > 0) {
+    const int64_t k = imin(I.sm_n, I.sm_cap);
+    const size_t old = h.samples.size();
+    h.samples.resize(old + (size_t)k);
+    if (dev_d2h(h.samples.data() + old, h.d_sm, sizeof(EconoSample) * (size_t)k)) return 1;
+    I.sm_n = 0;
+  }
+  return 0;
+}
+
+void launch_steps(econo_batch* b, int64_t max_steps, void* stream) {
+#ifdef ECONO_HOSTSIM
+  (void)stream;
+  for (auto& h : b->inst) engine_steps(h.desc, max_steps);
+  push_descs(b);
+#else
+  cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
+  k_engine_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps);
+#endif
+}
+
+int sync_batch(econo_batch* b, char* err, size_t errlen) {
+#ifndef ECONO_HOSTSIM
+  if (cudaStreamSynchronize(b->stream) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    set_err(err, errlen, "CUDA error: %s", cudaGetErrorString(cudaGetLastError()));
+    return ECONO_ECUDA;
+  }
+#endif
+  if (pull_descs(b)) return set_err(err, errlen, "device copy failed"), ECONO_ECUDA;
+  return ECONO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void econo_default_options(EconoOptions* o) {
+  memset(o, 0, sizeof(*o));
+  o->policy = ECONO_POLICY_ECONO_FULL;
+  o->batch_size_cap = 8;
+  o->tfs = 2048;
+  o->chunk_size = 512;
+  o->padding_ratio = 0.10;
+  o->reserved_fraction = 0.03;
+  o->buffer_ratio = 0.15;
+  o->t_base = 0.005;
+  o->t_token = 1e-4;
+  o->t_token_over = -1.0;
+  o->cost_tfs = 2048;
+  o->preempt_offload_penalty = 0.30;
+  o->preempt_free_penalty = 0.06;
+  o->reserve_penalty = 0.004;
+  o->sched_cost_per_exam = 2e-5;
+  o->swap_stall = 0.088;
+  o->pred_model = ECONO_PRED_ORACLE;
+  o->pred_accuracy = 1.0;
+  o->pred_tolerance = 0.1;
+  o->pred_quantum = 1;
+  o->pred_seed = 1;
+  o->n_deadline_bounds = 3;
+  o->deadline_bounds[0] = 0.2;
+  o->deadline_bounds[1] = 0.5;
+  o->deadline_bounds[2] = 2.0;
+  o->n_kvc_bounds = 4;
+  o->n_length_bounds = 4;
+  for (int i = 0; i < 4; ++i) o->kvc_bounds[i] = o->length_bounds[i] = 128 * (i + 1);
+  o->kvc_capacity = 32768;
+  o->kvc_block_size = 32;
+  o->slo_scale = 2.0;
+  o->seed = 1;
+  o->record_events = 1;
+  o->record_samples = 1;
+}
+
+void econo_batch_destroy(econo_batch* b) {
+  if (!b) return;
+  for (auto& h : b->inst) {
+    dev_free(h.arena);
+    dev_free(h.d_ev);
+    dev_free(h.d_sm);
+  }
+  dev_free(b->d_insts);
+  for (auto* v : b->views) delete v;
+#ifndef ECONO_HOSTSIM
+  if (b->stream) cudaStreamDestroy(b->stream);
+#endif
+  delete b;
+}
+
+int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns, int32_t n_inst,
+                       const EconoOptions* opts, int device, econo_batch** out, char* err, size_t errlen) {
+  *out = nullptr;
+  if (n_inst < 1) return set_err(err, errlen, "n_inst must be >= 1"), ECONO_ECONFIG;
+  for (int32_t i = 0; i < n_inst; ++i) {
+    const int rc = validate(&opts[i], ns[i], err, errlen);
+    if (rc) return rc;
+  }
+#ifndef ECONO_HOSTSIM
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0)
+    return set_err(err, errlen, "no CUDA device %d available (the EconoServe B200 path has no CPU fallback)", device),
+           ECONO_ECUDA;
+  if (cudaSetDevice(device) != cudaSuccess)
+    return set_err(err, errlen, "cudaSetDevice(%d) failed", device), ECONO_ECUDA;
+#endif
+  econo_batch* b = new econo_batch();
+  b->device = device;
+  b->inst.resize((size_t)n_inst);
+#ifndef ECONO_HOSTSIM
+  cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking);
+#endif
+  std::vector<const EconoTraceRecord*> d_traces((size_t)n_inst);
+  std::vector<uint64_t> seeds(2 * (size_t)n_inst);
+  for (int32_t i = 0; i < n_inst; ++i) {
+    HostInst& h = b->inst[(size_t)i];
+    const int rc = configure(h.desc, &opts[i], traces[i], ns[i], err, errlen);
+    if (rc) { econo_batch_destroy(b); return rc; }
+    h.trace.assign(traces[i], traces[i] + ns[i]);
+    h.seed = opts[i].seed;
+    h.pred_seed = opts[i].pred_seed;
+    h.policy = opts[i].policy;
+    size_t bytes = 0;
+    layout(h.desc, nullptr, &bytes);
+    void* arena;
+    if (dev_alloc(&arena, bytes)) {
+      econo_batch_destroy(b);
+      return set_err(err, errlen, "device allocation of %zu bytes failed", bytes), ECONO_ECUDA;
+    }
+    h.arena = (char*)arena;
+    h.arena_bytes = bytes;
+    layout(h.desc, h.arena, &bytes);
+    const int64_t n = ns[i];
+    if (ensure_logs(h, h.desc.record_events ? 4 * n + 4096 : 0, h.desc.record_samples ? 2 * n + 4096 : 0)) {
+      econo_batch_destroy(b);
+      return set_err(err, errlen, "device allocation of the event log failed"), ECONO_ECUDA;
+    }
+    seeds[2 * i] = opts[i].seed;
+    seeds[2 * i + 1] = opts[i].pred_seed;
+  }
+  void* di;
+  if (dev_alloc(&di, sizeof(Inst) * (size_t)n_inst)) {
+    econo_batch_destroy(b);
+    return set_err(err, errlen, "device allocation failed"), ECONO_ECUDA;
+  }
+  b->d_insts = (Inst*)di;
+  push_descs(b);
+#ifdef ECONO_HOSTSIM
+  for (int32_t i = 0; i < n_inst; ++i) {
+    Inst& I = b->inst[(size_t)i].desc;
+    double* arr = const_cast<double*>(I.arrival);
+    int32_t* pr = const_cast<int32_t*>(I.prompt);
+    int32_t* rl = const_cast<int32_t*>(I.true_rl);
+    for (int64_t k = 0; k < I.n; ++k) {
+      arr[k] = traces[i][k].arrival_time;
+      pr[k] = (int32_t)traces[i][k].prompt_len;
+      rl[k] = (int32_t)traces[i][k].true_rl;
+    }
+    mt_seed(I.mt, I.mt_i, seeds[2 * i]);
+    mt_seed(I.pmt, I.pmt_i, seeds[2 * i + 1]);
+    engine_init(I);
+  }
+  push_descs(b);
+#else
+  {
+    // stage traces on the device (AoS, converted to SoA by the init kernel)
+    std::vector<void*> bufs((size_t)n_inst, nullptr);
+    for (int32_t i = 0; i < n_inst; ++i) {
+      if (dev_alloc(&bufs[i], sizeof(EconoTraceRecord) * (size_t)ns[i]) ||
+          dev_h2d(bufs[i], traces[i], sizeof(EconoTraceRecord) * (size_t)ns[i])) {
+        for (auto p : bufs) dev_free(p);
+        econo_batch_destroy(b);
+        return set_err(err, errlen, "device trace upload failed"), ECONO_ECUDA;
+      }
+      d_traces[i] = (const EconoTraceRecord*)bufs[i];
+    }
+    void *dt, *ds;
+    dev_alloc(&dt, sizeof(void*) * (size_t)n_inst);
+    dev_alloc(&ds, sizeof(uint64_t) * 2 * (size_t)n_inst);
+    dev_h2d(dt, d_traces.data(), sizeof(void*) * (size_t)n_inst);
+    dev_h2d(ds, seeds.data(), sizeof(uint64_t) * 2 * (size_t)n_inst);
+    k_engine_init<<<(unsigned)n_inst, 32, 0, b->stream>>>(b->d_insts, (const EconoTraceRecord* const*)dt,
+                                                           (const uint64_t*)ds);
+    const int rc = sync_batch(b, err, errlen);
+    dev_free(dt);
+    dev_free(ds);
+    for (auto p : bufs) dev_free(p);
+    if (rc) { econo_batch_destroy(b); return rc; }
+  }
+#endif
+  if (pull_descs(b)) { econo_batch_destroy(b); return set_err(err, errlen, "device copy failed"), ECONO_ECUDA; }
+  for (auto& h : b->inst) {
+    if (h.desc.error) {
+      int code;
+      std::string m = format_error(h.desc, &code);
+      set_err(err, errlen, "%s", m.c_str());
+      econo_batch_destroy(b);
+      return code;
+    }
+  }
+  *out = b;
+  return ECONO_OK;
+}
+
+int econo_batch_launch(econo_batch* b, int64_t max_steps, void* stream) {
+  launch_steps(b, max_steps, stream);
+  return ECONO_OK;
+}
+
+int econo_batch_sync(econo_batch* b, char* err, size_t errlen) {
+  int rc = sync_batch(b, err, errlen);
+  if (rc) return rc;
+  return cuda_check(err, errlen, "econo_batch_sync");
+}
+
+int econo_batch_scalars(econo_batch* b, EconoScalars* out) {
+  for (size_t i = 0; i < b->inst.size(); ++i) {
+    const Inst& I = b->inst[i].desc;
+    EconoScalars& s = out[i];
+    memset(&s, 0, sizeof(s));
+    s.clock = I.clock;
+    s.iter = I.iter;
+    s.completed = I.completed;
+    s.steps = I.steps;
+    s.executed_iters = I.executed;
+    s.hosted_slots_created = I.hosted_total;
+    s.hosted_overruns = I.hosted_overruns;
+    s.calibrated_prefill_time = I.t_p;
+    s.calibrated_decode_time = I.t_g;
+    s.pt_dispatched = I.pt_dispatched;
+    s.gt_scheduled = I.gt_scheduled;
+    s.pt_queue_len = I.pt_count;
+    s.gt_queue_groups = I.G;
+    s.running = I.R;
+    s.arrived = I.arrival_cursor;
+    s.done = I.completed >= I.n;
+    s.error = I.error ? ECONO_ESIM : 0;
+  }
+  return ECONO_OK;
+}
+
+int econo_batch_engine(econo_batch* b, int32_t i, econo_engine** out) {
+  if (i < 0 || i >= (int32_t)b->inst.size()) return ECONO_ECONFIG;
+  econo_engine* e = new econo_engine{b, i, false};
+  b->views.push_back(e);
+  *out = e;
+  return ECONO_OK;
+}
+
+int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen) {
+  const size_t bytes = sizeof(double) * ECONO_PARTIAL_WORDS * b->inst.size();
+#ifdef ECONO_HOSTSIM
+  for (size_t i = 0; i < b->inst.size(); ++i) engine_partials(b->inst[i].desc, out + i * ECONO_PARTIAL_WORDS);
+  (void)bytes; (void)err; (void)errlen;
+  return ECONO_OK;
+#else
+  void* d;
+  if (dev_alloc(&d, bytes)) return set_err(err, errlen, "device allocation failed"), ECONO_ECUDA;
+  k_engine_partials<<<(unsigned)b->inst.size(), 32, 0, b->stream>>>(b->d_insts, (double*)d);
+  int rc = sync_batch(b, err, errlen);
+  if (!rc && dev_d2h(out, d, bytes)) rc = ECONO_ECUDA;
+  dev_free(d);
+  return rc;
+#endif
+}
+
+// ---- single engine -------------------------------------------------------
+
+int econo_create(const EconoTraceRecord* trace, int64_t n, const EconoOptions* opt, int device,
+                 econo_engine** out, char* err, size_t errlen) {
+  econo_batch* b = nullptr;
+  const int rc = econo_batch_create(&trace, &n, 1, opt, device, &b, err, errlen);
+  if (rc) return rc;
+  *out = new econo_engine{b, 0, true};
+  return ECONO_OK;
+}
+
+void econo_destroy(econo_engine* e) {
+  if (!e) return;
+  if (e->owns) {
+    econo_batch_destroy(e->b);
+    delete e;
+  }
+}
+
+int econo_step(econo_engine* e, int64_t max_steps, int32_t* more, char* err, size_t errlen) {
+  econo_batch* b = e->b;
+  HostInst& h = b->inst[(size_t)e->i];
+  if (b->inst.size() != 1) return set_err(err, errlen, "econo_step drives single-instance engines"), ECONO_ECONFIG;
+  int64_t left = max_steps;
+  for (;;) {
+    Inst& I = h.desc;
+    if (I.error) {
+      int code;
+      std::string m = format_error(I, &code);
+      set_err(err, errlen, "%s", m.c_str());
+      return code;
+    }
+    if (I.completed >= I.n || left <= 0) break;
+    const int64_t before = I.steps;
+    launch_steps(b, left, nullptr);
+    int rc = sync_batch(b, err, errlen);
+    if (rc) return rc;
+    rc = cuda_check(err, errlen, "k_engine_steps");
+    if (rc) return rc;
+    left -= h.desc.steps - before;
+    if (h.desc.status == STATUS_DRAIN) {
+      const bool empty_logs = h.desc.ev_n == 0 && h.desc.sm_n == 0;
+      if (drain(h)) return set_err(err, errlen, "device copy failed"), ECONO_ECUDA;
+      if (empty_logs) {  // the next step needs a bigger log
+        if (ensure_logs(h, 2 * h.desc.ev_cap + 4096, 2 * h.desc.sm_cap + 4096))
+          return set_err(err, errlen, "device allocation of the event log failed"), ECONO_ECUDA;
+      }
+      push_descs(b);
+    }
+  }
+  if (drain(h)) return set_err(err, errlen, "device copy failed"), ECONO_ECUDA;
+  push_descs(b);
+  *more = h.desc.completed < h.desc.n ? 1 : 0;
+  return ECONO_OK;
+}
+
+int econo_run(econo_engine* e, char* err, size_t errlen) {
+  int32_t more = 1;
+  while (more) {
+    const int rc = econo_step(e, (int64_t)1 << 40, &more, err, errlen);
+    if (rc) return rc;
+  }
+  return ECONO_OK;
+}
+
+int64_t econo_events(econo_engine* e, EconoEvent* out, int64_t cap) {
+  HostInst& h = e->b->inst[(size_t)e->i];
+  const int64_t n = (int64_t)h.events.size();
+  if (out) memcpy(out, h.events.data(), sizeof(EconoEvent) * (size_t)imin(n, cap));
+  return n;
+}
+
+int64_t econo_samples(econo_engine* e, EconoSample* out, int64_t cap) {
+  HostInst& h = e->b->inst[(size_t)e->i];
+  const int64_t n = (int64_t)h.samples.size();
+  if (out) memcpy(out, h.samples.data(), sizeof(EconoSample) * (size_t)imin(n, cap));
+  return n;
+}
+
+int econo_scalars(econo_engine* e, EconoScalars* out) {
+  std::vector<EconoScalars> all(e->b->inst.size());
+  econo_batch_scalars(e->b, all.data());
+  *out = all[(size_t)e->i];
+  return ECONO_OK;
+}
+
+int econo_records(econo_engine* e, EconoRecord* out, int64_t cap, char* err, size_t errlen) {
+  HostInst& h = e->b->inst[(size_t)e->i];
+  const Inst& I = h.desc;
+  if (I.completed < I.n)
+    return set_err(err, errlen, "report requested before the run finished"), ECONO_ESIM;
+  std::vector<EconoRecord> recs((size_t)I.n);
+#ifdef ECONO_HOSTSIM
+  for (int32_t i = 0; i < I.n; ++i) engine_record(I, i, recs[(size_t)i]);
+#else
+  void* d;
+  if (dev_alloc(&d, sizeof(EconoRecord) * (size_t)I.n)) return set_err(err, errlen, "device allocation failed"), ECONO_ECUDA;
+  k_engine_records<<<148, 256, 0, e->b->stream>>>(e->b->d_insts + e->i, (EconoRecord*)d);
+  int rc = sync_batch(e->b, err, errlen);
+  if (!rc && dev_d2h(recs.data(), d, sizeof(EconoRecord) * (size_t)I.n)) rc = ECONO_ECUDA;
+  dev_free(d);
+  if (rc) return rc;
+#endif
+  memcpy(out, recs.data(), sizeof(EconoRecord) * (size_t)imin(I.n, cap));
+  return ECONO_OK;
+}
+
+// aggregate (metrics.hpp:96-175) + the report tail of finalize (engine.hpp:986-993).
+int econo_report(econo_engine* e, EconoReport* out, char* err, size_t errlen) {
+  HostInst& h = e->b->inst[(size_t)e->i];
+  const Inst& I = h.desc;
+  std::vector<EconoRecord> recs((size_t)I.n);
+  int rc = econo_records(e, recs.data(), I.n, err, errlen);
+  if (rc) return rc;
+  EconoReport r;
+  memset(&r, 0, sizeof(r));
+  std::vector<double> jcts(recs.size());
+  double tbt_sum = 0.0, norm_sum = 0.0;
+  long tbt_n = 0, met = 0, failures = 0;
+  int64_t tokens_total = 0;
+  for (size_t i = 0; i < recs.size(); ++i) {
+    const EconoRecord& rc2 = recs[i];
+    const double jct = rc2.completion_time - rc2.arrival;
+    jcts[i] = jct;
+    if (rc2.true_rl >= 2 && rc2.first_token_time >= 0.0) {
+      tbt_sum += (rc2.completion_time - rc2.first_token_time) / (double)(rc2.true_rl - 1);
+      ++tbt_n;
+    }
+    norm_sum += jct / (double)rc2.true_rl;
+    if (rc2.met_slo) ++met;
+    tokens_total += rc2.true_rl;
+    r.preemptions += rc2.preempt_count;
+    r.reserve_draws += rc2.reserve_draws;
+    if (rc2.alloc_failure) ++failures;
+    r.makespan = r.makespan < rc2.completion_time ? rc2.completion_time : r.makespan;
+    r.mean_waiting += rc2.waiting_time;
+    r.mean_execution += rc2.execution_time;
+    r.mean_preemption += rc2.preemption_time;
+    r.mean_scheduling += rc2.scheduling_time_share;
+  }
+  const double n = (double)recs.size();
+  for (double j : jcts) r.mean_jct += j;
+  r.mean_jct /= n;
+  std::sort(jcts.begin(), jcts.end());
+  auto pct = [&](double q) {
+    const double rank = q * (double)(jcts.size() - 1);
+    const size_t lo = (size_t)rank;
+    const size_t hi = std::min(lo + 1, jcts.size() - 1);
+    const double frac = rank - (double)lo;
+    return jcts[lo] * (1.0 - frac) + jcts[hi] * frac;
+  };
+  r.p5_jct = pct(0.05);
+  r.p95_jct = pct(0.95);
+  r.mean_tbt = tbt_n > 0 ? tbt_sum / (double)tbt_n : 0.0;
+  r.ssr = (double)met / n;
+  r.normalized_latency = norm_sum / n;
+  r.mean_waiting /= n;
+  r.mean_execution /= n;
+  r.mean_preemption /= n;
+  r.mean_scheduling /= n;
+  if (r.makespan > 0.0) {
+    r.throughput_rps = n / r.makespan;
+    r.throughput_tps = (double)tokens_total / r.makespan;
+    r.goodput_rps = (double)met / r.makespan;
+  }
+  r.allocation_failure_pct = 100.0 * (double)failures / n;
+  // sample aggregates were accumulated on the device in sample order
+  const long executed = (long)I.executed;
+  r.iterations = executed;
+  if (executed > 0) {
+    r.mean_forward_size = (double)I.agg_fs / (double)executed;
+    r.mean_kvc_written = I.agg_written / (double)executed;
+    r.mean_kvc_allocated = I.agg_allocated / (double)executed;
+    r.tfs_hit_frac = (double)I.agg_tfs_hits / (double)executed;
+    r.pt_admit_frac = (double)I.agg_pt_iters / (double)executed;
+    std::vector<int64_t> hist((size_t)I.hist_cap);
+    if (dev_d2h(hist.data(), I.hist, sizeof(int64_t) * hist.size()))
+      return set_err(err, errlen, "device copy failed"), ECONO_ECUDA;
+    int k = 0;
+    for (int c = 0; c < I.hist_cap && k < ECONO_MAX_HIST; ++c)
+      if (hist[(size_t)c]) {
+        r.hist_count[k] = c;
+        r.hist_frac[k] = (double)hist[(size_t)c] / (double)executed;
+        ++k;
+      }
+    r.n_hist = k;
+  }
+  // trace hash: write_trace_csv + FNV-1a (workload.hpp:127-134, metrics.hpp:320-328)
+  uint64_t hh = 1469598103934665603ULL;
+  auto feed = [&](const char* s, int len) {
+    for (int j = 0; j < len; ++j) {
+      hh ^= (unsigned char)s[j];
+      hh *= 1099511628211ULL;
+    }
+  };
+  const char* hdr = "arrival_time,prompt_len,response_len\n";
+  feed(hdr, (int)strlen(hdr));
+  char buf[128];
+  for (const auto& t : h.trace) {
+    const int len = snprintf(buf, sizeof(buf), "%.17g,%lld,%lld\n", t.arrival_time, (long long)t.prompt_len,
+                             (long long)t.true_rl);
+    feed(buf, len);
+  }
+  r.trace_hash = hh;
+  r.hosted_slots = I.hosted_total;
+  r.hosted_overruns = I.hosted_overruns;
+  *out = r;
+  return ECONO_OK;
+}
+
+// Canonical snapshot, assembled on the host from
+// a copy of the instance's device arena.
+int64_t econo_snapshot(econo_engine* e, int64_t* out, int64_t cap) {
+  HostInst& h = e->b->inst[(size_t)e->i];
+  std::vector<char> buf(h.arena_bytes);
+  if (dev_d2h(buf.data(), h.arena, h.arena_bytes)) return -1;
+  Inst I = h.desc;
+  rebase(I, h.arena, buf.data(), h.arena_bytes);
+  std::vector<int64_t> w;
+  w.reserve(1024 + 24 * (size_t)I.n);
+  auto bits = [](double d) {
+    int64_t v;
+    memcpy(&v, &d, 8);
+    return v;
+  };
+  w.push_back(0x45434f4e);
+  w.push_back(I.iter);
+  w.push_back(bits(I.clock));
+  w.push_back(I.completed);
+  w.push_back(I.arrival_cursor);
+  w.push_back(I.free_total);
+  w.push_back(I.reserved_used);
+  w.push_back(I.written_total);
+  w.push_back(I.hosted_total);
+  w.push_back(I.hosted_overruns);
+  w.push_back(I.exam_count);
+  w.push_back(I.n);
+  // PT queue in order
+  std::vector<int64_t> ptq;
+  if (I.ordered) {
+    for (int b = 0; b < I.nbuckets; ++b)
+      for (int p = I.pmax; p >= 0; --p)
+        for (int32_t id = I.cls_head[b * (I.pmax + 1) + p]; id >= 0; id = I.pt_next[id]) ptq.push_back(id);
+  } else {
+    for (int64_t id = 0; id < I.arrival_cursor; ++id)
+      if (I.state[id] == ST_WAITING_PT) ptq.push_back(id);
+  }
+  w.push_back((int64_t)ptq.size());
+  w.insert(w.end(), ptq.begin(), ptq.end());
+  // GT groups in key order
+  w.push_back(I.G);
+  for (int32_t k = 0; k < I.G; ++k) {
+    const int32_t g = I.gq[k];
+    w.push_back((int64_t)I.gr_id[g]);
+    w.push_back(I.gr_rl[g]);
+    w.push_back(bits(I.gr_formed[g]));
+    w.push_back(bits(I.gr_mindl[g]));
+    w.push_back(I.gr_maxocc[g]);
+    w.push_back(I.ordered ? I.gr_db[g] : 0);
+    w.push_back(I.ordered ? I.gr_kb[g] : 0);
+    w.push_back(I.ordered ? I.gr_rl[g] : 0);
+    w.push_back((int64_t)I.gr_seq[g]);
+    w.push_back(I.gr_cnt[g]);
+    int32_t m = I.gr_head[g];
+    for (int32_t j = 0; j < I.gr_cnt[g]; ++j) {
+      w.push_back(m);
+      m = I.gt_next[m];
+    }
+  }
+  // hosting slots in insertion order
+  w.push_back(I.n_slots);
+  for (int32_t k = 0; k < I.n_slots; ++k) {
+    const int32_t hs = I.slots[k];
+    w.push_back(I.slot_host[hs]);
+    w.push_back(hs);
+    w.push_back(I.slot_off[hs]);
+    w.push_back(I.slot_len[hs]);
+    w.push_back(I.slot_off[hs]);
+    w.push_back(I.slot_abs[hs]);
+  }
+  // holdings by id
+  int64_t nh = 0;
+  for (int32_t id = 0; id < I.n; ++id) nh += I.reg_cnt[id] > 0;
+  w.push_back(nh);
+  for (int32_t id = 0; id < I.n; ++id) {
+    if (I.reg_cnt[id] <= 0) continue;
+    w.push_back(id);
+    w.push_back(I.held[id]);
+    w.push_back(I.reg_cnt[id]);
+    for (int32_t r = I.reg_head[id]; r >= 0; r = I.rg_next[r]) {
+      w.push_back(I.rg_start[r]);
+      w.push_back(I.rg_len[r]);
+    }
+  }
+  // free gaps: the complement of the address-ordered regions
+  std::vector<int64_t> gaps;
+  int64_t cur = 0;
+  for (int32_t k = 0; k <= I.n_regions; ++k) {
+    const int64_t s = k < I.n_regions ? I.rg_start[I.addr[k]] : I.general_cap;
+    if (s > cur) { gaps.push_back(cur); gaps.push_back(s - cur); }
+    if (k < I.n_regions) cur = (int64_t)I.rg_start[I.addr[k]] + I.rg_len[I.addr[k]];
+  }
+  w.push_back((int64_t)gaps.size() / 2);
+  w.insert(w.end(), gaps.begin(), gaps.end());
+  int64_t nr = 0;
+  for (int32_t id = 0; id < I.n; ++id) nr += (I.flags[id] & F_HAS_RESERVED) ? 1 : 0;
+  w.push_back(nr);
+  for (int32_t id = 0; id < I.n; ++id)
+    if (I.flags[id] & F_HAS_RESERVED) { w.push_back(id); w.push_back(I.reserved[id]); }
+  int64_t nw = 0;
+  for (int32_t id = 0; id < I.n; ++id) nw += I.written[id] != 0;
+  w.push_back(nw);
+  for (int32_t id = 0; id < I.n; ++id)
+    if (I.written[id] != 0) { w.push_back(id); w.push_back(I.written[id]); }
+  w.push_back(I.R);
+  for (int32_t k = 0; k < I.R; ++k) w.push_back(I.run[k]);
+  for (int32_t i = 0; i < I.n; ++i) {
+    w.push_back(I.state[i]);
+    w.push_back(I.generated[i]);
+    w.push_back(I.predicted[i]);
+    w.push_back(I.padded[i]);
+    w.push_back(I.allowance[i]);
+    w.push_back(I.gen_epoch[i]);
+    w.push_back(I.occupied[i]);
+    w.push_back((I.flags[i] & F_HOSTED) ? 1 : 0);
+    w.push_back((I.flags[i] & F_WAS_PREEMPTED) ? 1 : 0);
+    w.push_back(I.preempt_count[i]);
+    w.push_back(I.reserve_draws[i]);
+    w.push_back((I.flags[i] & F_ALLOC_FAIL) ? 1 : 0);
+    w.push_back(I.prefill_done[i]);
+    w.push_back(bits(I.waiting[i]));
+    w.push_back(bits(I.preempt_t[i]));
+    w.push_back(bits(I.exec_t[i]));
+    w.push_back(bits(I.dispatch_t[i]));
+    w.push_back(bits(I.first_tok[i]));
+    w.push_back(bits(I.compl_clock[i]));
+    w.push_back(bits(I.last_enq[i]));
+    w.push_back(bits(I.sched_share[i]));
+    w.push_back(bits(I.penalty[i]));
+    w.push_back(bits(I.slo[i]));
+  }
+  const int64_t nwords = (int64_t)w.size();
+  if (out) memcpy(out, w.data(), sizeof(int64_t) * (size_t)imin(nwords, cap));
+  return nwords;
+}
+
+// ---- host-side trace generation (input preparation) ----------------------
+// generate_synthetic (workload.hpp:42-125) with libstdc++'s mt19937_64,
+// generate_canonical, polar normal and exponential (random.tcc:1811-1844,
+// 3349-3380; random.h:2358, 4904), glibc libm. Bit-identical to the reference.
+namespace {
+struct Mt64 {
+  uint64_t x[312];
+  int32_t i;
+  explicit Mt64(uint64_t s) { mt_seed(x, i, s); }
+  uint64_t next() { return mt_next(x, i); }
+  double canon() { return canonical(x, i); }
+};
+double cdf(double v) { return 0.5 * std::erfc(-v / std::sqrt(2.0)); }
+double trunc_mean(double mu, double sg, double a, double b) {
+  const double al = (std::log(a) - mu) / sg, be = (std::log(b) - mu) / sg;
+  const double mass = cdf(be) - cdf(al);
+  if (mass <= 0.0) return a;
+  const double num = cdf(be - sg) - cdf(al - sg);
+  return std::exp(mu + 0.5 * sg * sg) * num / mass;
+}
+double fit_mu(const EconoLengthDist& d) {
+  const double a = (double)d.min_value, b = (double)d.max_value;
+  double lo = std::log(a) - 10.0, hi = std::log(b) + 10.0;
+  for (int k = 0; k < 200; ++k) {
+    const double mid = 0.5 * (lo + hi);
+    if (trunc_mean(mid, d.sigma, a, b) < d.mean) lo = mid; else hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+struct Polar {  // normal_distribution with its cached second variate
+  bool have = false;
+  double saved = 0.0;
+  double draw(Mt64& g) {
+    if (have) { have = false; return saved; }
+    double x, y, r2;
+    do {
+      x = 2.0 * g.canon() - 1.0;
+      y = 2.0 * g.canon() - 1.0;
+      r2 = x * x + y * y;
+    } while (r2 > 1.0 || r2 == 0.0);
+    const double mult = std::sqrt(-2 * std::log(r2) / r2);
+    saved = x * mult;
+    have = true;
+    return y * mult;
+  }
+};
+int64_t sample_len(const EconoLengthDist& d, double mu, Mt64& g) {
+  if (d.min_value == d.max_value) return d.min_value;
+  Polar nd;
+  for (int attempt = 0; attempt < 10000; ++attempt) {
+    const int64_t v = (int64_t)std::llround(std::exp(d.sigma * (nd.draw(g) * 1.0 + 0.0) + mu));
+    if (v >= d.min_value && v <= d.max_value) return v;
+  }
+  return std::clamp<int64_t>((int64_t)std::llround(std::exp(mu)), d.min_value, d.max_value);
+}
+int check_dist(const EconoLengthDist& d, char* err, size_t errlen) {
+  if (d.min_value < 1 || d.max_value < d.min_value)
+    return set_err(err, errlen, "length distribution bounds invalid: min=%lld max=%lld", (long long)d.min_value,
+                   (long long)d.max_value), ECONO_ECONFIG;
+  if (d.sigma <= 0.0) return set_err(err, errlen, "length distribution sigma must be > 0"), ECONO_ECONFIG;
+  if (d.mean < (double)d.min_value || d.mean > (double)d.max_value)
+    return set_err(err, errlen, "length distribution mean outside [min, max]"), ECONO_ECONFIG;
+  return ECONO_OK;
+}
+}  // namespace
+
+int econo_generate_trace(int64_t n, double rate, const EconoLengthDist* p, const EconoLengthDist* r, uint64_t seed,
+                         EconoTraceRecord* out, char* err, size_t errlen) {
+  if (n < 1) return set_err(err, errlen, "n_requests must be >= 1"), ECONO_ECONFIG;
+  if (!(rate > 0.0)) return set_err(err, errlen, "arrival_rate must be > 0"), ECONO_ECONFIG;
+  int rc = check_dist(*p, err, errlen);
+  if (!rc) rc = check_dist(*r, err, errlen);
+  if (rc) return rc;
+  const double mp = fit_mu(*p), mr = fit_mu(*r);
+  Mt64 g(seed);
+  double clock = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    clock += -std::log(1.0 - g.canon()) / rate;
+    out[i].arrival_time = clock;
+    out[i].prompt_len = sample_len(*p, mp, g);
+    out[i].true_rl = sample_len(*r, mr, g);
+  }
+  return ECONO_OK;
+}
+
+}  // extern "C"

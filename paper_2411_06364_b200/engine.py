@@ -1,0 +1,255 @@
+"""Python host mirror of econosim::Engine over the C-ABI (include/econoserve_b200.h).
+
+`Engine(trace, options)` / `step()` / `run()` / `report()` / `events()` /
+`samples()` / `requests()`-style snapshots follow the reference's public
+surface (engine.hpp:79-145); `run(trace, options)` is the one-call entry point
+(engine.hpp:1039-1042). Errors raise `ConfigError` / `SimulationError` with the
+reference's messages (common.hpp:17-24).
+
+The library is the sm_100a build in paper_2411_06364_b200/_lib/. There is no CPU
+fallback: without a CUDA device, creating an Engine raises DeviceError.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libeconoserve_b200.so")
+
+SYMBOLS = [
+    "econo_default_options", "econo_create", "econo_step", "econo_run", "econo_records",
+    "econo_report", "econo_events", "econo_samples", "econo_scalars", "econo_snapshot",
+    "econo_destroy", "econo_batch_create", "econo_batch_launch", "econo_batch_sync",
+    "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
+    "econo_generate_trace",
+]
+
+
+class ConfigError(ValueError):
+    """econosim::ConfigError (common.hpp:17-19)."""
+
+
+class SimulationError(RuntimeError):
+    """econosim::SimulationError (common.hpp:22-24)."""
+
+
+class DeviceError(RuntimeError):
+    """No usable CUDA device / CUDA failure (the product has no CPU path)."""
+
+
+def _raise(rc, err):
+    msg = err.value.decode(errors="replace")
+    if rc == abi.ECONFIG:
+        raise ConfigError(msg)
+    if rc == abi.ESIM:
+        raise SimulationError(msg)
+    raise DeviceError(msg)
+
+
+_libs = {}
+
+
+def load(path=None):
+    """Loads (once) and types the C-ABI library at `path` (default: the sm_100a build)."""
+    path = path or LIB_PATH
+    if path in _libs:
+        return _libs[path]
+    if not os.path.exists(path):
+        raise DeviceError(f"{path} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(path)
+    vp, i64, i32, cp, sz = C.c_void_p, C.c_int64, C.c_int32, C.c_char_p, C.c_size_t
+    L.econo_default_options.argtypes = [C.POINTER(abi.Options)]
+    L.econo_create.argtypes = [vp, i64, C.POINTER(abi.Options), C.c_int, C.POINTER(vp), cp, sz]
+    L.econo_step.argtypes = [vp, i64, C.POINTER(i32), cp, sz]
+    L.econo_run.argtypes = [vp, cp, sz]
+    L.econo_records.argtypes = [vp, vp, i64, cp, sz]
+    L.econo_report.argtypes = [vp, C.POINTER(abi.Report), cp, sz]
+    L.econo_events.argtypes = [vp, vp, i64]
+    L.econo_events.restype = i64
+    L.econo_samples.argtypes = [vp, vp, i64]
+    L.econo_samples.restype = i64
+    L.econo_scalars.argtypes = [vp, C.POINTER(abi.Scalars)]
+    L.econo_snapshot.argtypes = [vp, vp, i64]
+    L.econo_snapshot.restype = i64
+    L.econo_destroy.argtypes = [vp]
+    L.econo_batch_create.argtypes = [C.POINTER(vp), C.POINTER(i64), i32, C.POINTER(abi.Options),
+                                     C.c_int, C.POINTER(vp), cp, sz]
+    L.econo_batch_launch.argtypes = [vp, i64, vp]
+    L.econo_batch_sync.argtypes = [vp, cp, sz]
+    L.econo_batch_scalars.argtypes = [vp, C.POINTER(abi.Scalars)]
+    L.econo_batch_engine.argtypes = [vp, i32, C.POINTER(vp)]
+    L.econo_batch_partials.argtypes = [vp, vp, cp, sz]
+    L.econo_batch_destroy.argtypes = [vp]
+    L.econo_generate_trace.argtypes = [i64, C.c_double, C.POINTER(abi.LengthDist),
+                                       C.POINTER(abi.LengthDist), C.c_uint64, vp, cp, sz]
+    _libs[path] = L
+    return L
+
+
+def generate_trace(n, rate, prompt, rl, seed, lib=None):
+    """generate_synthetic (workload.hpp:104-125): host-side input preparation."""
+    L = load(lib)
+    out = np.zeros(n, dtype=abi.TRACE_DTYPE)
+    err = C.create_string_buffer(512)
+    rc = L.econo_generate_trace(n, rate, C.byref(abi.LengthDist(*prompt)),
+                                C.byref(abi.LengthDist(*rl)), seed, out.ctypes.data, err, 512)
+    if rc:
+        _raise(rc, err)
+    return out
+
+
+class Engine:
+    """econosim::Engine (engine.hpp:79-145) running on the B200."""
+
+    def __init__(self, trace, options=None, device=0, lib=None):
+        self._L = load(lib)
+        self.trace = abi.trace_array(trace)
+        self.options = options if options is not None else abi.default_options()
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_create(self.trace.ctypes.data, len(self.trace), C.byref(self.options),
+                                  device, C.byref(h), err, 1024)
+        if rc:
+            _raise(rc, err)
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.econo_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def step(self, n=1):
+        """Advances up to n Engine::step() calls; returns step()'s last value."""
+        more = C.c_int32()
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_step(self.h, n, C.byref(more), err, 1024)
+        if rc:
+            _raise(rc, err)
+        return bool(more.value)
+
+    def run(self):
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_run(self.h, err, 1024)
+        if rc:
+            _raise(rc, err)
+        return self.report()
+
+    def records(self):
+        out = np.zeros(len(self.trace), dtype=abi.RECORD_DTYPE)
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_records(self.h, out.ctypes.data, len(out), err, 1024)
+        if rc:
+            _raise(rc, err)
+        return out
+
+    def report(self):
+        """(records, EconoReport) — finalize() + aggregate() (engine.hpp:963-994)."""
+        recs = self.records()
+        rep = abi.Report()
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_report(self.h, C.byref(rep), err, 1024)
+        if rc:
+            _raise(rc, err)
+        return recs, rep
+
+    finalize = report
+
+    def events(self):
+        n = self._L.econo_events(self.h, None, 0)
+        out = np.zeros(n, dtype=abi.EVENT_DTYPE)
+        self._L.econo_events(self.h, out.ctypes.data, n)
+        return out
+
+    def samples(self):
+        n = self._L.econo_samples(self.h, None, 0)
+        out = np.zeros(n, dtype=abi.SAMPLE_DTYPE)
+        self._L.econo_samples(self.h, out.ctypes.data, n)
+        return out
+
+    def scalars(self):
+        s = abi.Scalars()
+        self._L.econo_scalars(self.h, C.byref(s))
+        return s
+
+    def snapshot(self):
+        n = self._L.econo_snapshot(self.h, None, 0)
+        out = np.zeros(n, dtype=np.int64)
+        self._L.econo_snapshot(self.h, out.ctypes.data, n)
+        return out
+
+    # engine.hpp:136-145 accessors
+    def clock(self):
+        return self.scalars().clock
+
+    def hosted_slots_created(self):
+        return self.scalars().hosted_slots_created
+
+    def hosted_overruns(self):
+        return self.scalars().hosted_overruns
+
+    def calibrated_prefill_time(self):
+        return self.scalars().calibrated_prefill_time
+
+    def calibrated_decode_time(self):
+        return self.scalars().calibrated_decode_time
+
+
+def run(trace, options=None, device=0, lib=None):
+    """econosim::run(trace, opt) (engine.hpp:1039-1042)."""
+    return Engine(trace, options, device=device, lib=lib).run()
+
+
+class Batch:
+    """Many independent instances advanced together (one warp each) — the
+    device form of run_sweep's engine pool (sweep.hpp:112-149)."""
+
+    def __init__(self, traces, options, device=0, lib=None):
+        self._L = load(lib)
+        self.traces = [abi.trace_array(t) for t in traces]
+        if not isinstance(options, (list, tuple)):
+            options = [options] * len(self.traces)
+        self.options = (abi.Options * len(self.traces))(*options)
+        ptrs = (C.c_void_p * len(self.traces))(*[t.ctypes.data for t in self.traces])
+        ns = (C.c_int64 * len(self.traces))(*[len(t) for t in self.traces])
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_batch_create(ptrs, ns, len(self.traces), self.options, device,
+                                        C.byref(h), err, 1024)
+        if rc:
+            _raise(rc, err)
+        self.h = h
+        self.n = len(self.traces)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.econo_batch_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def launch(self, max_steps, stream=None):
+        self._L.econo_batch_launch(self.h, max_steps, stream)
+
+    def sync(self):
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_batch_sync(self.h, err, 1024)
+        if rc:
+            _raise(rc, err)
+
+    def scalars(self):
+        out = (abi.Scalars * self.n)()
+        self._L.econo_batch_scalars(self.h, out)
+        return list(out)
+
+    def partials(self):
+        out = np.zeros((self.n, abi.PARTIAL_WORDS), dtype=np.float64)
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_batch_partials(self.h, out.ctypes.data, err, 1024)
+        if rc:
+            _raise(rc, err)
+        return out
