@@ -1,0 +1,48 @@
+"""Parity case catalogue: (name, trace factory, options) built from the
+reference's own test fixtures (tests/test_engine.cpp, acceptance_main.cpp) and
+the BASELINE.json config shapes at sizes the oracle finishes in seconds."""
+from paper_2411_06364_b200 import abi, workloads as W
+
+from parity import base_options, sat_trace
+
+
+def catalogue(gen):
+    """gen(n, rate, prompt_dist, rl_dist, seed) -> trace."""
+    cases = []
+    tr = sat_trace(gen, 300, 40.0, 8, 64, 8, 96, 3)  # test_engine.cpp:110-125
+    for k in ["econoserve-full", "econoserve-sd", "econoserve-d", "econoserve-sdo"]:
+        cases.append((f"determinism-{k}", tr, base_options(
+            k, pred_model="lognormal", pred_sigma=0.3, pred_padding_ratio=0.1)))
+    tr = sat_trace(gen, 200, 40.0, 8, 40, 16, 120, 31)  # test_engine.cpp:181-206
+    for k, rf in [("econoserve-sd", 0.30), ("econoserve-sd", 0.02), ("econoserve-full", 0.02),
+                  ("econoserve-d", 0.02)]:
+        cases.append((f"underprediction-{k}-rf{rf}", tr, base_options(
+            k, pred_model="lognormal", pred_sigma=0.6, reserved_fraction=rf)))
+    tr = sat_trace(gen, 500, 250.0, 8, 32, 8, 128, 43)  # test_engine.cpp:233-241
+    cases.append(("hosted-oracle-full", tr, base_options("econoserve-full")))
+    for k in ["econoserve-full", "econoserve-sdo"]:
+        cases.append((f"hosted-bucket-{k}", tr, base_options(
+            k, pred_model="bucket", pred_accuracy=0.732, pred_tolerance=0.15,
+            pred_padding_ratio=0.15, buffer_ratio=0.15, sched_cost_per_exam=2e-5)))
+    tr = sat_trace(gen, 150, 25.0, 8, 60, 8, 64, 19)  # test_engine.cpp:147-162
+    cases.append(("jct-identity", tr, base_options(
+        "econoserve-full", sched_cost_per_exam=2e-5, pred_model="lognormal", pred_sigma=0.3,
+        pred_padding_ratio=0.05)))
+    tr = sat_trace(gen, 400, 60.0, 8, 32, 8, 48, 41)  # test_engine.cpp:208-231
+    cases.append(("same-rl-groups", tr, base_options("econoserve-sd")))
+    c = W.CONFIGS["cfg1_alpaca_10k"]
+    a = gen(3000, 400.0, c["shape"]["prompt"], c["shape"]["rl"], 5)  # SURVEY §8a saturated Alpaca
+    for pm, extra in [("bucket", dict(pred_accuracy=0.775, pred_tolerance=0.10)),
+                      ("lognormal", dict(pred_sigma=0.3))]:
+        for pol in ["econoserve-full", "econoserve-sd"]:
+            cases.append((f"alpaca400-{pm}-{pol}", a, abi.default_options(
+                **dict(c["opts"], policy=pol, pred_model=pm, **extra))))
+    s = W.CONFIGS["cfg2_sharegpt_100k"]
+    sg = gen(1500, 60.0, s["shape"]["prompt"], s["shape"]["rl"], 2)
+    cases.append(("sharegpt-cfg2-shape", sg, abi.default_options(**s["opts"])))
+    b = W.CONFIGS["cfg3_bookcorpus_1m"]
+    bk = gen(300, 1e9, b["shape"]["prompt"], b["shape"]["rl"], 1)
+    cases.append(("bookcorpus-cfg3-shape-burst", bk, abi.default_options(**b["opts"])))
+    cases.append(("bookcorpus-cfg3-shape-burst-sd", bk, abi.default_options(
+        **dict(b["opts"], policy="econoserve-sd"))))
+    return cases
