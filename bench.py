@@ -1,0 +1,345 @@
+"""EconoServe per-iteration scheduling step on B200 — benchmark (driver contract).
+
+Workload (BASELINE.json configs[2], the "1M queued" case the metric is quoted
+on): BookCorpus-shaped synthetic trace, 1M requests arriving as one burst,
+Llama-2-13B KVC (14,648 tokens, 16-token blocks, 14% reserve), tfs 4096,
+econoserve-full (SLO-priority selection + GT grouping + KVC pipelining),
+oracle predictor. Each GPU runs `--instances` independent serving instances
+(one warp each; instance i uses trace seed 1000 + global index), so per-GPU
+work is fixed as N grows ("scaling": "weak").
+
+A step = one device pass advancing every instance by `--iters` scheduler
+iterations (Engine::step(), engine.hpp:104-116) with 1M requests queued.
+value = PT admissions (pt_dispatch, engine.hpp:380) per second over all GPUs;
+us_per_iter = per-instance wall time of one scheduler iteration.
+
+`--impl reference` times the unmodified reference simulator (oracle/_ref,
+compiled from /root/reference by oracle/Makefile) on the host cores on the
+same config: one engine per thread, each step a bounded window of iterations.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2411_06364_b200 import abi, workloads as W  # noqa: E402
+
+METRIC = "scheduled requests/sec & us per scheduler iteration at 1M queued reqs; % HBM BW"
+UNIT = "req/s"
+WORKLOAD = "cfg3_bookcorpus_1m"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def options(record=False):
+    o = abi.default_options(**W.CONFIGS[WORKLOAD]["opts"])
+    o.record_events = 1 if record else 0
+    o.record_samples = 1 if record else 0
+    return o
+
+
+def make_traces(gen, n, seeds, threads=32):
+    c = W.CONFIGS[WORKLOAD]
+    with ThreadPoolExecutor(threads) as ex:
+        return list(ex.map(lambda s: gen(n, c["rate"], c["shape"]["prompt"], c["shape"]["rl"], s),
+                           seeds))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------
+# CPU baseline: the reference itself (oracle/_ref) on the host cores
+# --------------------------------------------------------------------------
+def reference_windows(n, threads, window, reps, warmup):
+    """Builds `threads` reference engines on the workload (trace seeds
+    1000+i), ingests the 1M burst (oracle/ref_driver.cpp ref_fast_ingest —
+    same post-ingest state as ingest_arrivals), then times `reps` windows of
+    `window` step() calls on one std::thread per engine. Returns
+    (per-window (seconds, admissions) list, setup seconds)."""
+    import ctypes as C
+
+    from oracle import ref
+    t0 = time.time()
+    traces = make_traces(ref.generate_trace, n, [1000 + i for i in range(threads)], threads)
+    o = options(record=True)  # the reference's default EngineOptions logs events
+    with ThreadPoolExecutor(threads) as ex:
+        engines = list(ex.map(lambda t: ref.RefEngine(t, o), traces))
+    for e in engines:
+        e.idle_to_first_arrival()
+        e.fast_ingest()
+        e.step(1)  # form + execute of the ingest step
+    setup = time.time() - t0
+    hv = (C.c_void_p * threads)(*[e.h.value for e in engines])
+    pts = np.zeros(threads, dtype=np.int64)
+    out = []
+    for r in range(warmup + reps):
+        secs = ref.lib().ref_time_steps_parallel(hv, threads, window, pts.ctypes.data)
+        if r >= warmup:
+            out.append((secs, int(pts.sum())))
+    return out, setup, engines
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = args.ref_threads or min(os.cpu_count() or 1, 32)
+    wins, setup, _ = reference_windows(args.n, threads, args.ref_iters, args.steps, args.warmup)
+    secs = sum(w[0] for w in wins)
+    adm = sum(w[1] for w in wins)
+    value = adm / secs if secs > 0 else 0.0
+    us_iter = 1e6 * secs / (args.ref_iters * len(wins))
+    sample = (f"{threads} reference engines (one std::thread each) x {args.n} requests "
+              f"({WORKLOAD}), {args.ref_iters} step() calls per engine per step after the burst ingest")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / len(wins), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "requests_per_instance": args.n, "instances": threads,
+                   "iters_per_step": args.ref_iters, "policy": "econoserve-full"},
+        "us_per_iter": us_iter,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": setup,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def algorithmic_bytes(sc_before, sc_after, iters, n_inst):
+    """Minimal HBM bytes one step's scheduler iterations must touch with this
+    design: per executed iteration 48 B per running request
+    (generated/occupied/written r+w, exec_t r+w, true_rl, allowance, state)
+    + 64 B of queue/bitmap probes; per PT admission 40 B (class head/count,
+    next link, prompt, reserve draw, dispatch fields); per GT schedule 96 B
+    (allocation scan share, region record, address insert, request fields)."""
+    run = np.mean([s.running for s in sc_after])
+    pt = sum(a.pt_dispatched - b.pt_dispatched for a, b in zip(sc_after, sc_before))
+    gt = sum(a.gt_scheduled - b.gt_scheduled for a, b in zip(sc_after, sc_before))
+    return n_inst * iters * (48.0 * run + 64.0) + 40.0 * pt + 96.0 * gt
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_06364_b200.engine import Batch, generate_trace
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    I = args.instances
+    seeds = [1000 + rank * I + i for i in range(I)]
+    t0 = time.time()
+    traces = make_traces(generate_trace, args.n, seeds)
+    t_gen = time.time() - t0
+
+    # ---- end to end through the public API: host traces -> device -> host results
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    b = Batch(traces, options(), device=local)
+    b.launch(2)  # idle tick + burst ingest (engine.hpp:216-235, 930-949)
+    b.sync()
+    t_create_ingest = time.perf_counter() - t0
+    sc_a = b.scalars()
+    b.launch(args.iters)
+    b.sync()
+    sc_b = b.scalars()
+    parts = b.partials()
+    t_e2e = time.perf_counter() - t0
+    e2e_adm = sum(x.pt_dispatched for x in sc_b)
+    h2d = sum(t.nbytes for t in traces)
+    d2h = parts.nbytes + I * 2 * 1600
+    del sc_a
+
+    # ---- device-timed windows (inputs resident in HBM)
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    for _ in range(args.warmup):
+        b.launch(args.iters, stream.cuda_stream)
+    stream.synchronize()
+    b.sync()
+    clocks = ClockSampler(local)
+    clocks.start()
+    times = []
+    sc0 = b.scalars()
+    for _ in range(args.steps):
+        flush.fill_(1)  # L2 flush between timed steps (not timed)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        b.launch(args.iters, stream.cuda_stream)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    b.sync()
+    sc1 = b.scalars()
+    errors = [s.error for s in sc1 if s.error]
+    adm = sum(a.pt_dispatched - z.pt_dispatched for a, z in zip(sc1, sc0))
+    gts = sum(a.gt_scheduled - z.gt_scheduled for a, z in zip(sc1, sc0))
+    tot = float(sum(times))
+    abytes = algorithmic_bytes(sc0, sc1, args.iters * args.steps, I)
+    t = torch.tensor([tot, float(adm), float(gts), float(e2e_adm), t_e2e], dtype=torch.float64,
+                     device=dev)
+    if world > 1:
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        tot_max, adm_all, gts_all, e2e_adm_all, e2e_t = (mx[0].item(), sm[1].item(), sm[2].item(),
+                                                         sm[3].item(), mx[4].item())
+        # metric partial sums of every instance: one NCCL reduction
+        pt = torch.from_numpy(b.partials()).to(dev)
+        dist.all_reduce(pt, op=dist.ReduceOp.SUM)
+    else:
+        tot_max, adm_all, gts_all, e2e_adm_all, e2e_t = tot, float(adm), float(gts), float(e2e_adm), t_e2e
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    value = adm_all / tot_max
+    iters_total = args.iters * args.steps
+    us_iter = 1e6 * tot_max / iters_total
+    peak, peak_kind = measured_peaks()
+    achieved = abytes / tot / 1e9  # GB/s, this rank's launches
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "requests_per_instance": args.n,
+                   "instances_per_gpu": I, "iters_per_step": args.iters,
+                   "policy": "econoserve-full", "l2": "flushed between timed steps (256 MiB write)"},
+        "us_per_iter": us_iter,
+        "iters_per_s_per_gpu": iters_total * I / tot_max,
+        "gt_scheduled_per_s": gts_all / tot_max,
+        "ingest_and_create_s": t_create_ingest,
+        "tracegen_s": t_gen,
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "k_engine_steps",
+                     "note": "latency-bound dependency chain; see DESIGN.md §5"},
+        "clocks": clk,
+        "e2e": {"value": e2e_adm_all / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "scope": "one job per step: Batch(host traces) + burst ingest + one "
+                         f"{args.iters}-iteration window + partials to host"},
+        "errors": len(errors),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            thr = min(os.cpu_count() or 1, 16)
+            wins, setup, _ = reference_windows(args.n, thr, args.ref_iters, 1, 0)
+            secs, pts = wins[0]
+            line["cpu_baseline"] = {
+                "value": pts / secs if secs > 0 else 0.0, "unit": UNIT, "cores": thr,
+                "kind": "reference", "us_per_iter": 1e6 * secs / args.ref_iters,
+                "sample": f"{thr} reference engines x {args.n} requests ({WORKLOAD}), "
+                          f"{args.ref_iters} step() calls each after the burst ingest, one std::thread per engine"}
+        except Exception as ex:  # the reference build is missing on this box
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                    "sample": f"unavailable: {ex}"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--instances", type=int, default=64)
+    ap.add_argument("--iters", type=int, default=1000)
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--ref-iters", type=int, default=100)
+    ap.add_argument("--ref-threads", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
