@@ -134,13 +134,18 @@ def reference_windows(n, threads, window, reps, warmup):
         e.fast_ingest()
         e.step(1)  # form + execute of the ingest step
     setup = time.time() - t0
-    hv = (C.c_void_p * threads)(*[e.h.value for e in engines])
     pts = np.zeros(threads, dtype=np.int64)
+    if warmup:  # warm up on deep copies so the timed windows start post-ingest
+        clones = [e.clone() for e in engines]
+        hc = (C.c_void_p * threads)(*[e.h.value for e in clones])
+        for _ in range(warmup):
+            ref.lib().ref_time_steps_parallel(hc, threads, window, pts.ctypes.data)
+        del clones
+    hv = (C.c_void_p * threads)(*[e.h.value for e in engines])
     out = []
-    for r in range(warmup + reps):
+    for r in range(reps):
         secs = ref.lib().ref_time_steps_parallel(hv, threads, window, pts.ctypes.data)
-        if r >= warmup:
-            out.append((secs, int(pts.sum())))
+        out.append((secs, int(pts.sum())))
     return out, setup, engines
 
 
@@ -149,20 +154,23 @@ def run_reference(args):
     if rank != 0:
         return
     threads = args.ref_threads or min(os.cpu_count() or 1, 32)
-    wins, setup, _ = reference_windows(args.n, threads, args.ref_iters, args.steps, args.warmup)
+    wins, setup, _ = reference_windows(args.n, threads, args.iters, args.steps, args.warmup)
     secs = sum(w[0] for w in wins)
     adm = sum(w[1] for w in wins)
     value = adm / secs if secs > 0 else 0.0
-    us_iter = 1e6 * secs / (args.ref_iters * len(wins))
+    us_iter = 1e6 * secs / (args.iters * len(wins))
     sample = (f"{threads} reference engines (one std::thread each) x {args.n} requests "
-              f"({WORKLOAD}), {args.ref_iters} step() calls per engine per step after the burst ingest")
+              f"({WORKLOAD}), {args.iters} step() calls per engine per step; the {args.steps} timed "
+              f"steps cover iterations 2..{2 + args.iters * args.steps} after the burst ingest "
+              f"(warm-up ran on deep copies)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / len(wins), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "requests_per_instance": args.n, "instances": threads,
-                   "iters_per_step": args.ref_iters, "policy": "econoserve-full"},
+                   "iters_per_step": args.iters, "policy": "econoserve-full",
+                   "window": f"iterations 2..{2 + args.iters * args.steps} after the burst ingest"},
         "us_per_iter": us_iter,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
@@ -215,23 +223,26 @@ def run_ours(args):
     b.sync()
     t_create_ingest = time.perf_counter() - t0
     sc_a = b.scalars()
-    b.launch(args.iters)
+    b.checkpoint()  # post-ingest state: every window below starts here (untimed)
+    t1 = time.perf_counter()
+    b.launch(args.iters * args.steps)
     b.sync()
     sc_b = b.scalars()
     parts = b.partials()
-    t_e2e = time.perf_counter() - t0
-    e2e_adm = sum(x.pt_dispatched for x in sc_b)
+    t_e2e = t_create_ingest + time.perf_counter() - t1
+    e2e_adm = sum(x.pt_dispatched - y.pt_dispatched for x, y in zip(sc_b, sc_a))
     h2d = sum(t.nbytes for t in traces)
     d2h = parts.nbytes + I * 2 * 1600
-    del sc_a
 
     # ---- device-timed windows (inputs resident in HBM)
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    b.restore()
     for _ in range(args.warmup):
         b.launch(args.iters, stream.cuda_stream)
     stream.synchronize()
     b.sync()
+    b.restore()  # timed steps cover the same post-ingest window as the reference arm
     clocks = ClockSampler(local)
     clocks.start()
     times = []
@@ -286,7 +297,8 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "requests_per_instance": args.n,
                    "instances_per_gpu": I, "iters_per_step": args.iters,
-                   "policy": "econoserve-full", "l2": "flushed between timed steps (256 MiB write)"},
+                   "policy": "econoserve-full", "l2": "flushed between timed steps (256 MiB write)",
+                   "window": f"iterations 2..{2 + args.iters * args.steps} after the burst ingest"},
         "us_per_iter": us_iter,
         "iters_per_s_per_gpu": iters_total * I / tot_max,
         "gt_scheduled_per_s": gts_all / tot_max,
@@ -300,20 +312,21 @@ def run_ours(args):
         "clocks": clk,
         "e2e": {"value": e2e_adm_all / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "scope": "one job per step: Batch(host traces) + burst ingest + one "
-                         f"{args.iters}-iteration window + partials to host"},
+                "scope": "one whole job: Batch(host traces) + burst ingest + the same "
+                         f"{args.iters * args.steps}-iteration window + partials to host"},
         "errors": len(errors),
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
             thr = min(os.cpu_count() or 1, 16)
-            wins, setup, _ = reference_windows(args.n, thr, args.ref_iters, 1, 0)
+            wins, setup, _ = reference_windows(args.n, thr, args.iters * args.steps, 1, 0)
             secs, pts = wins[0]
             line["cpu_baseline"] = {
                 "value": pts / secs if secs > 0 else 0.0, "unit": UNIT, "cores": thr,
-                "kind": "reference", "us_per_iter": 1e6 * secs / args.ref_iters,
+                "kind": "reference", "us_per_iter": 1e6 * secs / (args.iters * args.steps),
                 "sample": f"{thr} reference engines x {args.n} requests ({WORKLOAD}), "
-                          f"{args.ref_iters} step() calls each after the burst ingest, one std::thread per engine"}
+                          f"iterations 2..{2 + args.iters * args.steps} after the burst ingest "
+                          "(the timed window), one std::thread per engine"}
         except Exception as ex:  # the reference build is missing on this box
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {ex}"}
@@ -329,9 +342,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--instances", type=int, default=64)
-    ap.add_argument("--iters", type=int, default=1000)
+    ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--n", type=int, default=1_000_000)
-    ap.add_argument("--ref-iters", type=int, default=100)
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

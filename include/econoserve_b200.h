@@ -263,6 +263,10 @@ int econo_batch_engine(econo_batch* b, int32_t i, econo_engine** out); /* borrow
  * (metrics.hpp:110-173) into `out` (ECONO_PARTIAL_WORDS doubles per instance). */
 #define ECONO_PARTIAL_WORDS 32
 int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen);
+/* Device-side checkpoint / restore of every instance's complete state
+ * (arena + descriptor), e.g. to rerun one scheduling window. */
+int econo_batch_checkpoint(econo_batch* b, char* err, size_t errlen);
+int econo_batch_restore(econo_batch* b, char* err, size_t errlen);
 void econo_batch_destroy(econo_batch* b);
 
 /* ---- host-side input preparation (out of the hot path) ------------------ */

@@ -23,6 +23,8 @@ def lib():
         L.ref_create.argtypes = [C.c_void_p, C.c_int64, C.POINTER(abi.Options),
                                  C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
         L.ref_destroy.argtypes = [C.c_void_p]
+        L.ref_clone.argtypes = [C.c_void_p]
+        L.ref_clone.restype = C.c_void_p
         L.ref_step.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int32), C.c_char_p, C.c_size_t]
         L.ref_events.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
         L.ref_events.restype = C.c_int64
@@ -77,9 +79,12 @@ def trace_hash(trace):
 class RefEngine:
     """econosim::Engine (engine.hpp:79-145), the reference itself."""
 
-    def __init__(self, trace, opts):
+    def __init__(self, trace, opts, _handle=None):
         self.trace = abi.trace_array(trace)
         self.opts = opts
+        if _handle is not None:
+            self.h = C.c_void_p(_handle)
+            return
         h = C.c_void_p()
         err = C.create_string_buffer(1024)
         rc = lib().ref_create(self.trace.ctypes.data, len(self.trace), C.byref(opts),
@@ -92,6 +97,9 @@ class RefEngine:
         if getattr(self, "h", None):
             lib().ref_destroy(self.h)
             self.h = None
+
+    def clone(self):
+        return RefEngine(self.trace, self.opts, _handle=lib().ref_clone(self.h))
 
     def step(self, n=1):
         more = C.c_int32()

@@ -173,6 +173,16 @@ int ref_create(const EconoTraceRecord* trace, int64_t n, const EconoOptions* opt
 
 void ref_destroy(void* h) { delete static_cast<RefEngine*>(h); }
 
+// Deep copy of an engine (Engine is a value type): lets a benchmark warm up
+// on the copy and time the original from the same state.
+void* ref_clone(void* hv) {
+  auto* h = static_cast<RefEngine*>(hv);
+  auto* c = new RefEngine();
+  c->eng = std::make_unique<Engine>(*h->eng);
+  c->steps = h->steps;
+  return c;
+}
+
 // Advances up to max_steps step() calls; *more = step()'s last return value.
 int ref_step(void* hv, int64_t max_steps, int32_t* more, char* err, size_t errlen) {
   auto* h = static_cast<RefEngine*>(hv);

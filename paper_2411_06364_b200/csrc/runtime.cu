@@ -583,6 +583,9 @@ struct HostInst {
   std::vector<EconoTraceRecord> trace;
   uint64_t seed = 1, pred_seed = 1;
   int32_t policy = 0;
+  char* ckpt = nullptr;  // device copy of the arena (econo_batch_checkpoint)
+  Inst ckpt_desc;
+  std::vector<int64_t> ckpt_hist;
 };
 
 struct econo_batch {
@@ -737,6 +740,7 @@ void econo_batch_destroy(econo_batch* b) {
   if (!b) return;
   for (auto& h : b->inst) {
     dev_free(h.arena);
+    dev_free(h.ckpt);
     dev_free(h.d_ev);
     dev_free(h.d_sm);
   }
@@ -922,6 +926,47 @@ int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen) 
   dev_free(d);
   return rc;
 #endif
+}
+
+int econo_batch_checkpoint(econo_batch* b, char* err, size_t errlen) {
+  int rc = sync_batch(b, err, errlen);
+  if (rc) return rc;
+  for (auto& h : b->inst) {
+    if (!h.ckpt) {
+      void* p;
+      if (dev_alloc(&p, h.arena_bytes)) return set_err(err, errlen, "checkpoint allocation failed"), ECONO_ECUDA;
+      h.ckpt = (char*)p;
+    }
+#ifdef ECONO_HOSTSIM
+    memcpy(h.ckpt, h.arena, h.arena_bytes);
+#else
+    if (cudaMemcpyAsync(h.ckpt, h.arena, h.arena_bytes, cudaMemcpyDeviceToDevice, b->stream) != cudaSuccess)
+      return set_err(err, errlen, "checkpoint copy failed"), ECONO_ECUDA;
+#endif
+    h.ckpt_desc = h.desc;
+  }
+  return sync_batch(b, err, errlen);
+}
+
+int econo_batch_restore(econo_batch* b, char* err, size_t errlen) {
+  int rc = sync_batch(b, err, errlen);
+  if (rc) return rc;
+  for (auto& h : b->inst) {
+    if (!h.ckpt) return set_err(err, errlen, "no checkpoint to restore"), ECONO_ECONFIG;
+#ifdef ECONO_HOSTSIM
+    memcpy(h.arena, h.ckpt, h.arena_bytes);
+#else
+    if (cudaMemcpyAsync(h.arena, h.ckpt, h.arena_bytes, cudaMemcpyDeviceToDevice, b->stream) != cudaSuccess)
+      return set_err(err, errlen, "restore copy failed"), ECONO_ECUDA;
+#endif
+    // logs are not part of the state: keep the current log buffers
+    Inst d = h.ckpt_desc;
+    d.ev = h.desc.ev; d.ev_cap = h.desc.ev_cap; d.ev_n = 0;
+    d.sm = h.desc.sm; d.sm_cap = h.desc.sm_cap; d.sm_n = 0;
+    h.desc = d;
+  }
+  if (push_descs(b)) return set_err(err, errlen, "device copy failed"), ECONO_ECUDA;
+  return sync_batch(b, err, errlen);
 }
 
 // ---- single engine -------------------------------------------------------

@@ -24,7 +24,7 @@ SYMBOLS = [
     "econo_report", "econo_events", "econo_samples", "econo_scalars", "econo_snapshot",
     "econo_destroy", "econo_batch_create", "econo_batch_launch", "econo_batch_sync",
     "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
-    "econo_generate_trace",
+    "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore",
 ]
 
 
@@ -83,6 +83,8 @@ def load(path=None):
     L.econo_batch_engine.argtypes = [vp, i32, C.POINTER(vp)]
     L.econo_batch_partials.argtypes = [vp, vp, cp, sz]
     L.econo_batch_destroy.argtypes = [vp]
+    L.econo_batch_checkpoint.argtypes = [vp, cp, sz]
+    L.econo_batch_restore.argtypes = [vp, cp, sz]
     L.econo_generate_trace.argtypes = [i64, C.c_double, C.POINTER(abi.LengthDist),
                                        C.POINTER(abi.LengthDist), C.c_uint64, vp, cp, sz]
     _libs[path] = L
@@ -245,6 +247,18 @@ class Batch:
         out = (abi.Scalars * self.n)()
         self._L.econo_batch_scalars(self.h, out)
         return list(out)
+
+    def checkpoint(self):
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_batch_checkpoint(self.h, err, 1024)
+        if rc:
+            _raise(rc, err)
+
+    def restore(self):
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_batch_restore(self.h, err, 1024)
+        if rc:
+            _raise(rc, err)
 
     def partials(self):
         out = np.zeros((self.n, abi.PARTIAL_WORDS), dtype=np.float64)
