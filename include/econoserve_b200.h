@@ -221,6 +221,8 @@ typedef struct EconoScalars {
   int64_t arrived;
   int32_t done;
   int32_t error;          /* ECONO_OK or ECONO_ESIM once the engine faulted */
+  int64_t quiet_steps;    /* steps replayed by event-horizon skipping */
+  int64_t quiet_spans;
 } EconoScalars;
 
 /* Default options, identical to a default-constructed econosim::EngineOptions

@@ -130,7 +130,7 @@ class Scalars(C.Structure):
                 ("pt_dispatched", C.c_int64), ("gt_scheduled", C.c_int64),
                 ("pt_queue_len", C.c_int64), ("gt_queue_groups", C.c_int64),
                 ("running", C.c_int64), ("arrived", C.c_int64), ("done", C.c_int32),
-                ("error", C.c_int32)]
+                ("error", C.c_int32), ("quiet_steps", C.c_int64), ("quiet_spans", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -100,7 +100,7 @@ enum { STATUS_RUN = 0, STATUS_DRAIN = 1 };
 struct Inst {
   // ---- configuration (immutable after create) ----
   int32_t n, policy, ordered, grouping, full, pred_model;
-  int32_t nbd, nbk, record_events, record_samples;
+  int32_t nbd, nbk, record_events, record_samples, skip, _pad1;
   int32_t pmax, nbuckets, bm_words, bm_l2;    // PT class table (ordered mode)
   int32_t tree_levels, rl_cap;
   int32_t tree_off[8], tree_len[8];            // 32-ary min tree (FIFO mode)
@@ -119,6 +119,8 @@ struct Inst {
   int32_t reg_free_top, grp_free_top, n_sel, n_selg, n_hosts_members;
   int32_t error, err_id, status, mt_i, pmt_i, _pad0;
   int64_t err_val, ev_n, ev_cap, sm_n, sm_cap, ev_total;
+  int64_t pt_min_lb;   // lower bound on the smallest queued prompt (only grows between arrivals)
+  int64_t quiet_steps, quiet_spans, bcast;
   double agg_written, agg_allocated;
   int64_t agg_fs, agg_tfs_hits, agg_pt_iters;
   // ---- per-request SoA (n entries) ----
@@ -856,6 +858,12 @@ EDEVNI void ingest(Inst& I) {
       }
     }
   }
+  {
+    int64_t pm = INT64_MAX;
+    for (int64_t id = first + LANE; id < last; id += W) pm = I.prompt[id] < pm ? I.prompt[id] : pm;
+    pm = wmin(pm);
+    LANE0(if (pm < I.pt_min_lb) I.pt_min_lb = pm);
+  }
   if (I.ordered) {
     // class append in id order: peers of a class inside each warp chunk link
     // to each other; the lowest links to the class tail, the highest becomes it.
@@ -1268,18 +1276,21 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
   if (I.pt_count > 0) {
     // pt_admittable (engine.hpp:301-307): some queued prompt fits both budgets
     bool adm = false;
-    if (C0 >= 1) {
+    if (C0 >= 1 && C0 >= I.pt_min_lb) {
       if (I.ordered) {
         for (int b = 0; b < I.nbuckets && !adm; ++b) adm = bm_prev(I, b, C0) >= 1;
       } else {
         adm = I.tree[I.tree_off[I.tree_levels - 1]] <= C0;
       }
+      if (!adm) LANE0(I.pt_min_lb = C0 + 1);
     }
     if (adm) LANE0(I.pt_admittable = 1);
     if (tfs_rem > 0 && rfree > 0) {
       LANE0(I.exam_count += I.pt_count);
       Tok C = C0;  // both budgets drop by p: take iff p <= min(budgets)
-      if (I.ordered) {
+      if (!adm) {
+        // nothing fits (the admittable probe above used the same bound)
+      } else if (I.ordered) {
         for (int b = 0; b < I.nbuckets && C > 0; ++b) {
           Tok x = C;
           for (;;) {
@@ -1601,6 +1612,115 @@ EDEV int64_t step_event_bound(const Inst& I) {
     arrivals = lo - I.arrival_cursor;
   }
   return arrivals + 2 * I.tfs + 4 * (I.arrival_cursor - I.completed - I.pt_count) + 2 * (int64_t)I.n_slots + 64;
+}
+
+// ------------------------------------------------------------------------
+// Exact event-horizon skipping (SURVEY.md §7 hard part 7; the reference has
+// no such thing). A step is "quiet" when ingest_arrivals admits nothing,
+// select_gt_groups and select_pts select nothing (their inputs — free KVC,
+// the GT queue head, tfs-|running|, the reserve and the PT queue — only
+// change at events) and execute_iteration sees no completion, under-
+// prediction or slot deadline. Quiet steps only advance clock/iter, the
+// running requests' progress counters and the in-order sample aggregates, so
+// a span of them is replayed with the same sequential FP adds (never k*dt).
+// ------------------------------------------------------------------------
+EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
+  if (I.R == 0 || I.n_ptiter != 0 || I.n_adm != 0 || budget <= 0) return 0;
+  if (I.arrival_cursor < I.n && I.arrival[I.arrival_cursor] <= I.clock + 1e-12) return 0;
+  if (I.free_total > 0 && I.G > 0) {  // queues.hpp:220-263 would take >= 1 member
+    const int32_t g = I.gq[0];
+    if (I.gr_dem[g] <= I.free_total || I.dem[I.gr_head[g]] <= I.free_total) return 0;
+  }
+  const Tok C0 = tmin(I.tfs - (Tok)I.R, I.reserve_cap - I.reserved_used);
+  if (C0 >= 1 && I.pt_count > 0 && C0 >= I.pt_min_lb) {  // queues.hpp:279-299 would take a PT
+    bool fit = false;
+    if (I.ordered) {
+      for (int b = 0; b < I.nbuckets && !fit; ++b) fit = bm_prev(I, b, C0) >= 1;
+    } else {
+      fit = I.tree[I.tree_off[I.tree_levels - 1]] <= C0;
+    }
+    if (fit) return 0;
+    LANE0(I.pt_min_lb = C0 + 1);
+  }
+  // first decode-side event: completion / under-prediction / slot deadline
+  int64_t kev = INT64_MAX;
+  for (int32_t i = LANE; i < I.R; i += W) {
+    const int32_t id = I.run[i];
+    const int64_t lim = I.true_rl[id] < I.allowance[id] ? I.true_rl[id] : I.allowance[id];
+    const int64_t e = lim - I.generated[id];
+    kev = e < kev ? e : kev;
+  }
+  for (int32_t si = LANE; si < I.n_slots; si += W) {
+    const int32_t h = I.slots[si];
+    const int32_t host = I.slot_host[h];
+    if (I.state[host] == ST_RUNNING) {
+      const int64_t e = (int64_t)I.slot_off[h] - (I.generated[host] - I.gen_epoch[host]);
+      kev = e < kev ? e : kev;
+    }
+  }
+  kev = wmin(kev);
+  int64_t k = kev - 1;  // the event iteration itself runs as a normal step
+  if (k > budget) k = budget;
+  if (I.record_samples && k > I.sm_cap - I.sm_n) k = I.sm_cap - I.sm_n;
+  return k > 0 ? k : 0;
+}
+
+EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
+  const Tok fs = I.R;
+  const double dt = iteration_time(I, fs) + 0.0;
+  const double clk1 = I.clock + dt;
+  if (LANE == 0) {
+    double clock = I.clock, aw = I.agg_written, aa = I.agg_allocated;
+    int64_t wt = I.written_total;
+    const double af = (double)((I.general_cap - I.free_total) + I.reserved_used) / (double)I.capacity;
+    const bool has_arr = I.arrival_cursor < I.n;
+    const double ta = has_arr ? I.arrival[I.arrival_cursor] : 0.0;
+    int64_t j = 0;
+    for (; j < k; ++j) {
+      if (j > 0 && has_arr && ta <= clock + 1e-12) break;  // ingest would admit it
+      clock += dt;
+      wt += fs;
+      const double wf = (double)wt / (double)I.capacity;
+      aw += wf;
+      aa += af;
+      if (I.record_samples) {
+        EconoSample& s = I.sm[I.sm_n + j];
+        s.iter = I.iter + j + 1;
+        s.clock = clock;
+        s.dt = dt;
+        s.forward_size = fs;
+        s.kvc_written_frac = wf;
+        s.kvc_allocated_frac = af;
+        s.completed = 0;
+        s.pts_admitted = 0;
+        s.pt_admittable = 0;
+        s._pad = 0;
+        s.idle_repeat = 0;
+      }
+    }
+    I.clock = clock;
+    I.written_total = wt;
+    I.agg_written = aw;
+    I.agg_allocated = aa;
+    I.bcast = j;
+  }
+  WSYNC();
+  k = I.bcast;
+  for (int32_t i = LANE; i < I.R; i += W) {
+    const int32_t id = I.run[i];
+    double e = I.exec_t[id];
+    for (int64_t j = 0; j < k; ++j) e += dt;
+    I.exec_t[id] = e;
+    if (I.generated[id] == 0 && I.first_tok[id] < 0.0) I.first_tok[id] = clk1;
+    I.generated[id] += (int32_t)k;
+    I.occupied[id] += (int32_t)k;
+    I.written[id] += (int32_t)k;
+  }
+  LANE0(I.iter += k; I.steps += k; I.executed += k; I.agg_fs += fs * k;
+        if ((double)fs >= 0.95 * (double)I.tfs) I.agg_tfs_hits += k;
+        I.hist[0] += k; if (I.record_samples) I.sm_n += k;
+        I.quiet_steps += k; I.quiet_spans++);
+  return k;
 }
 
 EDEVNI void engine_step(Inst& I) {  // Engine::step (engine.hpp:104-116)

@@ -106,14 +106,22 @@ EDEVNI void engine_init(Inst& I) {
 // Engine::run()'s loop body, up to max_steps times (engine.hpp:118-122).
 EDEVNI void engine_steps(Inst& I, int64_t max_steps) {
   LANE0(I.status = STATUS_RUN);
-  for (int64_t s = 0; s < max_steps; ++s) {
+  for (int64_t s = 0; s < max_steps;) {
     if (I.error || I.completed >= I.n) break;
     if ((I.record_events && I.ev_n + step_event_bound(I) > I.ev_cap) ||
         (I.record_samples && I.sm_n + 1 > I.sm_cap)) {
       LANE0(I.status = STATUS_DRAIN);
       break;
     }
+    if (I.skip) {
+      const int64_t k = quiet_span(I, max_steps - s);
+      if (k > 0) {
+        s += quiet_steps(I, k);
+        continue;
+      }
+    }
     engine_step(I);
+    ++s;
   }
 }
 
@@ -496,6 +504,8 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   I.slo_scale = o->slo_scale;
   I.buffer_ratio = o->buffer_ratio;
   I.free_total = I.general_cap;
+  I.pt_min_lb = INT64_MAX;
+  I.skip = getenv("ECONO_NO_SKIP") ? 0 : 1;
   // capacities
   I.pmax = (int32_t)pmax;
   I.nbuckets = I.nbd + 1;
@@ -899,6 +909,8 @@ int econo_batch_scalars(econo_batch* b, EconoScalars* out) {
     s.arrived = I.arrival_cursor;
     s.done = I.completed >= I.n;
     s.error = I.error ? ECONO_ESIM : 0;
+    s.quiet_steps = I.quiet_steps;
+    s.quiet_spans = I.quiet_spans;
   }
   return ECONO_OK;
 }

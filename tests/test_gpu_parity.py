@@ -18,7 +18,21 @@ CASES = catalogue(port.generate_trace)
 
 @pytest.mark.parametrize("name,trace,opts", CASES, ids=[c[0] for c in CASES])
 def test_lockstep_vs_oracle(name, trace, opts):
+    """Snapshot after every single step."""
     lockstep(port.OracleEngine(trace, opts), Engine(trace, opts))
+
+
+@pytest.mark.parametrize("name,trace,opts", CASES, ids=[c[0] for c in CASES])
+def test_spans_vs_oracle(name, trace, opts):
+    """Snapshots every 97 steps: exercises multi-step launches and the
+    event-horizon skipping inside them."""
+    lockstep(port.OracleEngine(trace, opts), Engine(trace, opts), every=97)
+
+
+@pytest.mark.parametrize("name,trace,opts", CASES, ids=[c[0] for c in CASES])
+def test_full_run_vs_oracle(name, trace, opts):
+    """One launch for the whole run, then events / samples / records / report."""
+    lockstep(port.OracleEngine(trace, opts), Engine(trace, opts), every=1 << 40)
 
 
 @pytest.mark.parametrize("policy", ["econoserve-full", "econoserve-sd"])
