@@ -51,8 +51,32 @@ def lib():
         L.ref_time_steps_parallel.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.c_int64,
                                               C.c_void_p]
         L.ref_time_steps_parallel.restype = C.c_double
+        L.ref_mt_draws.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]
+        L.ref_shuffle_indices.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]
+        L.ref_predict.argtypes = [C.POINTER(abi.Options), C.c_uint64, C.c_void_p, C.c_int64,
+                                  C.c_void_p]
+        L.ref_predict.restype = C.c_int64
         _lib = L
     return _lib
+
+
+def mt_draws(seed, n):
+    out = np.zeros(n, dtype=np.uint64)
+    lib().ref_mt_draws(seed, n, out.ctypes.data)
+    return out
+
+
+def shuffle_indices(seed, n):
+    out = np.zeros(n, dtype=np.int64)
+    lib().ref_shuffle_indices(seed, n, out.ctypes.data)
+    return out
+
+
+def predict(opts, seed, true_rl):
+    t = np.ascontiguousarray(true_rl, dtype=np.int64)
+    out = np.zeros(len(t), dtype=np.int64)
+    lib().ref_predict(C.byref(opts), seed, t.ctypes.data, len(t), out.ctypes.data)
+    return out
 
 
 class EngineError(RuntimeError):

@@ -586,4 +586,25 @@ double ref_time_steps_parallel(void** hv, int32_t n_eng, int64_t steps, int64_t*
   return m;
 }
 
+// libstdc++ known-answer vectors for the restated RNG plumbing.
+void ref_mt_draws(uint64_t seed, int64_t n, uint64_t* out) {
+  Rng g(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = g();
+}
+void ref_shuffle_indices(uint64_t seed, int64_t n, int64_t* idx) {
+  Rng g(seed);
+  std::vector<int64_t> v(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) v[static_cast<size_t>(i)] = i;
+  std::shuffle(v.begin(), v.end(), g);
+  for (int64_t i = 0; i < n; ++i) idx[i] = v[static_cast<size_t>(i)];
+}
+// predict_rl + apply_padding over a sequence (workload.hpp:228-268).
+int64_t ref_predict(const EconoOptions* o, uint64_t seed, const int64_t* true_rl, int64_t n, int64_t* out) {
+  EngineOptions e = to_options(o);
+  Rng g(seed);
+  for (int64_t i = 0; i < n; ++i)
+    out[i] = apply_padding(predict_rl(true_rl[i], e.predictor, g), e.predictor.padding_ratio);
+  return n;
+}
+
 }  // extern "C"
