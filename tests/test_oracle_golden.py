@@ -129,3 +129,21 @@ def test_fast_ingest_equals_ingest_arrivals():
         b.step(2)
         assert np.array_equal(a.snapshot(), b.snapshot())
         assert np.array_equal(a.events(), b.events())
+
+
+@needs_ref
+def test_event_detail_strings_match_reference():
+    """The integer event encoding renders back to the reference's exact
+    kind/detail strings (engine.hpp:221-948)."""
+    from parity import base_options, sat_trace
+    tr = sat_trace(ref.generate_trace, 200, 40.0, 8, 40, 16, 120, 31)
+    o = base_options("econoserve-full", pred_model="lognormal", pred_sigma=0.6, reserved_fraction=0.02)
+    e = ref.RefEngine(tr, o)
+    e.run()
+    ev = e.events()
+    seen = set()
+    for i in range(len(ev)):
+        k, d = e.event_detail(i)
+        assert abi.event_str(ev[i]) == (k, d)
+        seen.add(k)
+    assert {"preempt", "reserve_topup", "hosted", "complete", "gt_schedule"} <= seen
