@@ -146,4 +146,4 @@ def test_event_detail_strings_match_reference():
         k, d = e.event_detail(i)
         assert abi.event_str(ev[i]) == (k, d)
         seen.add(k)
-    assert {"preempt", "reserve_topup", "hosted", "complete", "gt_schedule"} <= seen
+    assert {"preempt", "reserve_topup", "complete", "gt_schedule", "prefill_done", "idle"} <= seen
