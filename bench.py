@@ -216,6 +216,8 @@ def run_ours(args):
     t_gen = time.time() - t0
 
     # ---- end to end through the public API: host traces -> device -> host results
+    clocks = ClockSampler(local)  # sampled from here to the end of the timed steps
+    clocks.start()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     b = Batch(traces, options(), device=local)
@@ -243,8 +245,6 @@ def run_ours(args):
     stream.synchronize()
     b.sync()
     b.restore()  # timed steps cover the same post-ingest window as the reference arm
-    clocks = ClockSampler(local)
-    clocks.start()
     times = []
     sc0 = b.scalars()
     for _ in range(args.steps):
@@ -302,6 +302,8 @@ def run_ours(args):
         "us_per_iter": us_iter,
         "iters_per_s_per_gpu": iters_total * I / tot_max,
         "gt_scheduled_per_s": gts_all / tot_max,
+        "quiet_step_frac": (sum(a.quiet_steps - z.quiet_steps for a, z in zip(sc1, sc0)) /
+                            max(1, sum(a.steps - z.steps for a, z in zip(sc1, sc0)))),
         "ingest_and_create_s": t_create_ingest,
         "tracegen_s": t_gen,
         "gpu_launches": args.steps,

@@ -381,6 +381,17 @@ EDEV void bm_clear(Inst& I, int b, int p) {  // lane 0
   w &= ~(1ULL << (p & 63));
   if (w == 0) I.bm2[(int64_t)b * I.bm_l2 + (p >> 12)] &= ~(1ULL << ((p >> 6) & 63));
 }
+// bm_set from several lanes at once (words are shared between classes).
+EDEV void bm_set_shared(Inst& I, int b, int p) {
+#ifdef __CUDACC__
+  atomicOr(reinterpret_cast<unsigned long long*>(&I.bm1[(int64_t)b * I.bm_words + (p >> 6)]),
+           1ULL << (p & 63));
+  atomicOr(reinterpret_cast<unsigned long long*>(&I.bm2[(int64_t)b * I.bm_l2 + (p >> 12)]),
+           1ULL << ((p >> 6) & 63));
+#else
+  bm_set(I, b, p);
+#endif
+}
 // Largest nonempty prompt class p <= x in bucket b, or -1.
 EDEV int bm_prev(const Inst& I, int b, int64_t xx) {
   if (xx < 0) return -1;
@@ -893,11 +904,7 @@ EDEVNI void ingest(Inst& I) {
         if (highest) I.cls_tail[cls] = (int32_t)id;
       }
       WSYNC();
-      for (int l = 0; l < W; ++l) {  // bitmap words are shared between classes
-        const int pb = shfl(p, l), bb = shfl(b, l);
-        const bool okl = shfl((int)ok, l);
-        if (okl && LANE == 0) bm_set(I, bb, pb);
-      }
+      if (ok) bm_set_shared(I, b, p);  // bitmap words are shared between classes
       WSYNC();
     }
   } else {

@@ -10,12 +10,14 @@
 // ECONO_HOSTSIM (test-only, built by tests/hostsim.py with g++): the same
 // engine source compiled for the host with one lane per "warp", used to check
 // the engine logic against the oracle on machines without a GPU.
+#include <limits.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <string>
 #include <thread>
@@ -36,71 +38,85 @@ static_assert(sizeof(Inst) % 8 == 0, "Inst must be 8-byte granular");
 // ---------------------------------------------------------------------------
 namespace econo {
 
-// init_requests (engine.hpp:165-209) + empty queue / allocator state.
-EDEVNI void engine_init(Inst& I) {
-  const int32_t n = I.n;
-  // arrival order (engine.hpp:167-169)
-  for (int32_t base = 1; base < n; base += W) {
-    const int32_t i = base + LANE;
-    const unsigned m = BALLOT(i < n && I.arrival[i] < I.arrival[i - 1]);
-    if (m) { set_error(I, ERR_ARRIVAL_ORDER, base + FFS(m), 0); return; }
-  }
-  // mean prompt: an exact integer sum equals the reference's sequential
-  // double sum of integers (engine.hpp:171-174) while below 2^53.
-  int64_t ps = 0;
-  for (int32_t i = LANE; i < n; i += W) ps += I.prompt[i];
-  ps = wsum(ps);
-  const Tok mean_prompt = tmax(1, (Tok)llround((double)ps / (double)n));
-  LANE0(I.t_p = iteration_time(I, mean_prompt); I.t_g = iteration_time(I, I.tfs));
-  // predictions consume pred_rng_ in id order (engine.hpp:187-188)
-  if (I.pred_model == ECONO_PRED_ORACLE) {
-    for (int32_t i = LANE; i < n; i += W) I.predicted[i] = (int32_t)quantize_up(I.true_rl[i], I.pred_quantum);
-  } else if (LANE == 0) {
-    for (int32_t i = 0; i < n; ++i) I.predicted[i] = (int32_t)predict_rl(I, I.true_rl[i], I.pmt, I.pmt_i);
-  }
+// init_requests (engine.hpp:165-209), split so the O(n) parts run grid-wide
+// over every instance's requests and only the sequential pieces (the
+// pred_rng_ stream for non-oracle predictors, scalar calibration) run per
+// instance. Phase 1: trace AoS -> SoA, arrival-order check, prompt sum.
+EDEV void init_soa_one(Inst& I, const EconoTraceRecord* tr, int64_t i, bool* order_bad, int64_t* prompt) {
+  double* arr = const_cast<double*>(I.arrival);
+  int32_t* pr = const_cast<int32_t*>(I.prompt);
+  int32_t* rl = const_cast<int32_t*>(I.true_rl);
+  arr[i] = tr[i].arrival_time;
+  pr[i] = (int32_t)tr[i].prompt_len;
+  rl[i] = (int32_t)tr[i].true_rl;
+  *order_bad = i > 0 && tr[i].arrival_time < tr[i - 1].arrival_time;
+  *prompt = tr[i].prompt_len;
+}
+// Phase 2 (per instance): calibration t_p / t_g (engine.hpp:171-176); the
+// prompt sum is an exact integer, equal to the reference's sequential
+// double sum of integers below 2^53.
+EDEV void init_calibrate(Inst& I, int64_t prompt_sum) {
+  const Tok mean_prompt = tmax(1, (Tok)llround((double)prompt_sum / (double)I.n));
+  I.t_p = iteration_time(I, mean_prompt);
+  I.t_g = iteration_time(I, I.tfs);
+}
+// Predictions consume pred_rng_ in id order (engine.hpp:187-188): sequential
+// unless the predictor is the oracle.
+EDEVNI void init_predict_sequential(Inst& I) {
+  if (I.pred_model == ECONO_PRED_ORACLE) return;
+  if (LANE == 0)
+    for (int32_t i = 0; i < I.n; ++i) I.predicted[i] = (int32_t)predict_rl(I, I.true_rl[i], I.pmt, I.pmt_i);
   WSYNC();
-  int32_t bad = INF32;
-  int code = ERR_NONE;
-  for (int32_t i = LANE; i < n; i += W) {
-    I.padded[i] = (int32_t)apply_padding(I.predicted[i], I.pred_pad);
-    I.slo[i] = I.arrival[i] + I.slo_scale * (I.t_p + I.t_g * (double)I.true_rl[i]);
-    I.state[i] = ST_WAITING_PT;
-    I.dispatch_t[i] = -1.0;
-    I.first_tok[i] = -1.0;
-    I.compl_clock[i] = -1.0;
-    I.reg_head[i] = -1;
-    I.reg_tail[i] = -1;
-    I.pt_next[i] = -1;
-    I.gt_next[i] = -1;
-    const Tok worst = block_round((Tok)I.prompt[i] + tmax(I.true_rl[i], I.padded[i]), I.block);
-    if (bad == INF32 && (worst > I.general_cap || (Tok)I.prompt[i] > I.reserve_cap)) {
-      bad = i;
-      code = worst > I.general_cap ? ERR_INFEASIBLE_KVC : ERR_INFEASIBLE_RESERVE;
-    }
+}
+// Phase 3: per-request fields + feasibility (engine.hpp:186-206).
+EDEV bool init_req_one(Inst& I, int64_t i) {
+  if (I.pred_model == ECONO_PRED_ORACLE) I.predicted[i] = (int32_t)quantize_up(I.true_rl[i], I.pred_quantum);
+  I.padded[i] = (int32_t)apply_padding(I.predicted[i], I.pred_pad);
+  I.slo[i] = I.arrival[i] + I.slo_scale * (I.t_p + I.t_g * (double)I.true_rl[i]);
+  I.state[i] = ST_WAITING_PT;
+  I.dispatch_t[i] = -1.0;
+  I.first_tok[i] = -1.0;
+  I.compl_clock[i] = -1.0;
+  I.reg_head[i] = -1;
+  I.reg_tail[i] = -1;
+  I.pt_next[i] = -1;
+  I.gt_next[i] = -1;
+  const Tok worst = block_round((Tok)I.prompt[i] + tmax(I.true_rl[i], I.padded[i]), I.block);
+  return worst > I.general_cap || (Tok)I.prompt[i] > I.reserve_cap;
+}
+// Table initialisation for index i of every table.
+EDEV void init_tables_one(Inst& I, int64_t i) {
+  if (i < I.reg_cap) I.reg_free[i] = I.reg_cap - 1 - (int32_t)i;
+  if (i < I.grp_cap) I.grp_free[i] = I.grp_cap - 1 - (int32_t)i;
+  if (i < I.rl_cap) I.rl_map[i] = -1;
+  if (I.ordered) {
+    if (i < (int64_t)I.nbuckets * (I.pmax + 1)) { I.cls_head[i] = -1; I.cls_tail[i] = -1; }
+  } else if (i <= I.tree_off[I.tree_levels - 1]) {
+    I.tree[i] = INF32;
   }
-  const int32_t first_bad = wmin(bad);
-  if (first_bad != INF32) {
-    if (bad == first_bad) {
-      const Tok worst = block_round((Tok)I.prompt[bad] + tmax(I.true_rl[bad], I.padded[bad]), I.block);
-      I.error = code;
-      I.err_id = bad;
-      I.err_val = code == ERR_INFEASIBLE_KVC ? worst : I.reserve_cap;
-    }
-    WSYNC();
+}
+EDEV int64_t init_table_extent(const Inst& I) {
+  int64_t m = I.n;
+  m = m > I.reg_cap ? m : I.reg_cap;
+  m = m > I.grp_cap ? m : I.grp_cap;
+  m = m > I.rl_cap ? m : I.rl_cap;
+  const int64_t t = I.ordered ? (int64_t)I.nbuckets * (I.pmax + 1) : (int64_t)I.tree_off[I.tree_levels - 1] + 1;
+  return m > t ? m : t;
+}
+// Phase 4 (per instance): report the first infeasible request like the
+// reference (it throws at the first failing id), then open the tables.
+EDEV void init_finish(Inst& I, int64_t first_bad) {
+  if (first_bad < I.n) {
+    const int32_t bad = (int32_t)first_bad;
+    const Tok worst = block_round((Tok)I.prompt[bad] + tmax(I.true_rl[bad], I.padded[bad]), I.block);
+    I.error = worst > I.general_cap ? ERR_INFEASIBLE_KVC : ERR_INFEASIBLE_RESERVE;
+    I.err_id = bad;
+    I.err_val = worst > I.general_cap ? worst : I.reserve_cap;
     return;
   }
-  // allocator / queue tables
-  for (int32_t i = LANE; i < I.reg_cap; i += W) I.reg_free[i] = I.reg_cap - 1 - i;
-  for (int32_t i = LANE; i < I.grp_cap; i += W) I.grp_free[i] = I.grp_cap - 1 - i;
-  for (int32_t i = LANE; i < I.rl_cap; i += W) I.rl_map[i] = -1;
-  if (I.ordered) {
-    const int64_t nc = (int64_t)I.nbuckets * (I.pmax + 1);
-    for (int64_t i = LANE; i < nc; i += W) { I.cls_head[i] = -1; I.cls_tail[i] = -1; }
-  } else {
-    const int64_t tn = I.tree_off[I.tree_levels - 1] + 1;
-    for (int64_t i = LANE; i < tn; i += W) I.tree[i] = INF32;
-  }
-  LANE0(I.reg_free_top = I.reg_cap; I.grp_free_top = I.grp_cap; I.next_group_id = 1);
+  I.reg_free_top = I.reg_cap;
+  I.grp_free_top = I.grp_cap;
+  I.next_group_id = 1;
 }
 
 // Engine::run()'s loop body, up to max_steps times (engine.hpp:118-122).
@@ -223,26 +239,71 @@ __device__ __forceinline__ void inst_store(Inst* g, const Inst& s) {
   for (int i = threadIdx.x; i < (int)(sizeof(Inst) / 8); i += 32) dst[i] = src[i];
 }
 
-__global__ void __launch_bounds__(32) k_engine_init(Inst* insts, const EconoTraceRecord* const* traces,
-                                                    const uint64_t* seeds) {
+// Per-instance init scratch: [0] first out-of-order arrival, [1] prompt sum,
+// [2] first infeasible request.
+__global__ void __launch_bounds__(256) k_init_soa(Inst* insts, const EconoTraceRecord* const* traces,
+                                                  unsigned long long* scr) {
+  Inst& I = insts[blockIdx.y];
+  const EconoTraceRecord* tr = traces[blockIdx.y];
+  unsigned long long* sc = scr + 4 * blockIdx.y;
+  int64_t psum = 0;
+  long long bad = LLONG_MAX;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I.n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool ob;
+    int64_t p;
+    init_soa_one(I, tr, i, &ob, &p);
+    psum += p;
+    if (ob && i < bad) bad = i;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    psum += __shfl_xor_sync(0xffffffffu, psum, o);
+    const long long b2 = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = b2 < bad ? b2 : bad;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (psum) atomicAdd(&sc[1], (unsigned long long)psum);
+    if (bad != LLONG_MAX) atomicMin(&sc[0], (unsigned long long)bad);
+  }
+}
+
+__global__ void __launch_bounds__(32) k_init_scalar(Inst* insts, const uint64_t* seeds, const unsigned long long* scr) {
   __shared__ Inst I;
   inst_load(I, &insts[blockIdx.x]);
-  const EconoTraceRecord* tr = traces[blockIdx.x];
-  double* arr = const_cast<double*>(I.arrival);
-  int32_t* pr = const_cast<int32_t*>(I.prompt);
-  int32_t* rl = const_cast<int32_t*>(I.true_rl);
-  for (int32_t i = threadIdx.x; i < I.n; i += 32) {
-    arr[i] = tr[i].arrival_time;
-    pr[i] = (int32_t)tr[i].prompt_len;
-    rl[i] = (int32_t)tr[i].true_rl;
+  const unsigned long long* sc = scr + 4 * blockIdx.x;
+  if (sc[0] < (unsigned long long)I.n) {
+    LANE0(I.error = ERR_ARRIVAL_ORDER; I.err_id = (int32_t)sc[0]);
+  } else {
+    if (threadIdx.x == 0) {
+      mt_seed(I.mt, I.mt_i, seeds[2 * blockIdx.x]);
+      mt_seed(I.pmt, I.pmt_i, seeds[2 * blockIdx.x + 1]);
+      init_calibrate(I, (int64_t)sc[1]);
+    }
+    __syncwarp();
+    init_predict_sequential(I);
   }
-  if (threadIdx.x == 0) {
-    mt_seed(I.mt, I.mt_i, seeds[2 * blockIdx.x]);
-    mt_seed(I.pmt, I.pmt_i, seeds[2 * blockIdx.x + 1]);
-  }
-  __syncwarp();
-  engine_init(I);
   inst_store(&insts[blockIdx.x], I);
+}
+
+__global__ void __launch_bounds__(256) k_init_req(Inst* insts, unsigned long long* scr) {
+  Inst& I = insts[blockIdx.y];
+  if (I.error) return;
+  unsigned long long* sc = scr + 4 * blockIdx.y;
+  const int64_t ext = init_table_extent(I);
+  long long bad = LLONG_MAX;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ext; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < I.n && init_req_one(I, i) && i < bad) bad = i;
+    init_tables_one(I, i);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long b2 = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = b2 < bad ? b2 : bad;
+  }
+  if ((threadIdx.x & 31) == 0 && bad != LLONG_MAX) atomicMin(&sc[2], (unsigned long long)bad);
+}
+
+__global__ void __launch_bounds__(32) k_init_finish(Inst* insts, const unsigned long long* scr) {
+  Inst& I = insts[blockIdx.x];
+  if (threadIdx.x == 0 && !I.error) init_finish(I, (int64_t)scr[4 * blockIdx.x + 2]);
 }
 
 __global__ void __launch_bounds__(32) k_engine_steps(Inst* insts, int64_t max_steps) {
@@ -786,6 +847,7 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
 #endif
   std::vector<const EconoTraceRecord*> d_traces((size_t)n_inst);
   std::vector<uint64_t> seeds(2 * (size_t)n_inst);
+  const auto t_alloc0 = std::chrono::steady_clock::now();
   for (int32_t i = 0; i < n_inst; ++i) {
     HostInst& h = b->inst[(size_t)i];
     const int rc = configure(h.desc, &opts[i], traces[i], ns[i], err, errlen);
@@ -812,6 +874,9 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     seeds[2 * i] = opts[i].seed;
     seeds[2 * i + 1] = opts[i].pred_seed;
   }
+  if (getenv("ECONO_VERBOSE"))
+    fprintf(stderr, "[econo] create: arenas %.1f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_alloc0).count());
   void* di;
   if (dev_alloc(&di, sizeof(Inst) * (size_t)n_inst)) {
     econo_batch_destroy(b);
@@ -832,33 +897,93 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     }
     mt_seed(I.mt, I.mt_i, seeds[2 * i]);
     mt_seed(I.pmt, I.pmt_i, seeds[2 * i + 1]);
-    engine_init(I);
+    int64_t bad_order = I.n, psum = 0;
+    for (int64_t k = 0; k < I.n; ++k) {
+      bool ob;
+      int64_t p;
+      init_soa_one(I, traces[i], k, &ob, &p);
+      psum += p;
+      if (ob && k < bad_order) bad_order = k;
+    }
+    if (bad_order < I.n) {
+      I.error = ERR_ARRIVAL_ORDER;
+      I.err_id = (int32_t)bad_order;
+      continue;
+    }
+    init_calibrate(I, psum);
+    init_predict_sequential(I);
+    int64_t bad = I.n;
+    const int64_t ext = init_table_extent(I);
+    for (int64_t k = 0; k < ext; ++k) {
+      if (k < I.n && init_req_one(I, k) && k < bad) bad = k;
+      init_tables_one(I, k);
+    }
+    init_finish(I, bad);
   }
   push_descs(b);
 #else
   {
-    // stage traces on the device (AoS, converted to SoA by the init kernel)
-    std::vector<void*> bufs((size_t)n_inst, nullptr);
+    // Stage every trace in one device buffer (AoS; the init kernels convert
+    // it to SoA). Host pages are pinned in place for the copy when possible.
+    const bool verbose = getenv("ECONO_VERBOSE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b2) { return std::chrono::duration<double, std::milli>(b2 - a).count(); };
+    const auto t0 = now();
+    size_t total = 0;
+    std::vector<size_t> off((size_t)n_inst);
     for (int32_t i = 0; i < n_inst; ++i) {
-      if (dev_alloc(&bufs[i], sizeof(EconoTraceRecord) * (size_t)ns[i]) ||
-          dev_h2d(bufs[i], traces[i], sizeof(EconoTraceRecord) * (size_t)ns[i])) {
-        for (auto p : bufs) dev_free(p);
-        econo_batch_destroy(b);
-        return set_err(err, errlen, "device trace upload failed"), ECONO_ECUDA;
-      }
-      d_traces[i] = (const EconoTraceRecord*)bufs[i];
+      off[(size_t)i] = total;
+      total += sizeof(EconoTraceRecord) * (size_t)ns[i];
     }
-    void *dt, *ds;
+    void* dtr = nullptr;
+    if (dev_alloc(&dtr, total)) {
+      econo_batch_destroy(b);
+      return set_err(err, errlen, "device trace allocation failed"), ECONO_ECUDA;
+    }
+    std::vector<bool> pinned((size_t)n_inst, false);
+    for (int32_t i = 0; i < n_inst; ++i) {
+      const size_t bytes = sizeof(EconoTraceRecord) * (size_t)ns[i];
+      pinned[(size_t)i] = cudaHostRegister(const_cast<EconoTraceRecord*>(traces[i]), bytes,
+                                           cudaHostRegisterReadOnly) == cudaSuccess;
+      if (!pinned[(size_t)i]) cudaGetLastError();
+      cudaMemcpyAsync((char*)dtr + off[(size_t)i], traces[i], bytes, cudaMemcpyHostToDevice, b->stream);
+      d_traces[(size_t)i] = (const EconoTraceRecord*)((char*)dtr + off[(size_t)i]);
+    }
+    cudaStreamSynchronize(b->stream);
+    for (int32_t i = 0; i < n_inst; ++i)
+      if (pinned[(size_t)i]) cudaHostUnregister(const_cast<EconoTraceRecord*>(traces[i]));
+    const auto t1 = now();
+    void *dt, *ds, *dsc;
     dev_alloc(&dt, sizeof(void*) * (size_t)n_inst);
     dev_alloc(&ds, sizeof(uint64_t) * 2 * (size_t)n_inst);
+    dev_alloc(&dsc, sizeof(unsigned long long) * 4 * (size_t)n_inst);
     dev_h2d(dt, d_traces.data(), sizeof(void*) * (size_t)n_inst);
     dev_h2d(ds, seeds.data(), sizeof(uint64_t) * 2 * (size_t)n_inst);
-    k_engine_init<<<(unsigned)n_inst, 32, 0, b->stream>>>(b->d_insts, (const EconoTraceRecord* const*)dt,
-                                                           (const uint64_t*)ds);
+    std::vector<unsigned long long> sc0(4 * (size_t)n_inst, 0);
+    for (int32_t i = 0; i < n_inst; ++i) sc0[4 * (size_t)i] = sc0[4 * (size_t)i + 2] = ~0ULL;
+    dev_h2d(dsc, sc0.data(), sizeof(unsigned long long) * sc0.size());
+    int64_t nmax = 0, emax = 0;
+    for (auto& h : b->inst) {
+      nmax = imax(nmax, h.desc.n);
+      emax = imax(emax, h.desc.n + h.desc.general_cap + (int64_t)h.desc.nbuckets * (h.desc.pmax + 1) + 64);
+    }
+    const unsigned gx = (unsigned)imin(imax(1, (nmax + 255) / 256), 1184 / imax(1, n_inst / 8 + 1) + 1);
+    const unsigned gx2 = (unsigned)imin(imax(1, (emax + 255) / 256), 1184 / imax(1, n_inst / 8 + 1) + 1);
+    k_init_soa<<<dim3(gx, (unsigned)n_inst), 256, 0, b->stream>>>(b->d_insts, (const EconoTraceRecord* const*)dt,
+                                                                  (unsigned long long*)dsc);
+    k_init_scalar<<<(unsigned)n_inst, 32, 0, b->stream>>>(b->d_insts, (const uint64_t*)ds,
+                                                          (const unsigned long long*)dsc);
+    k_init_req<<<dim3(gx2, (unsigned)n_inst), 256, 0, b->stream>>>(b->d_insts, (unsigned long long*)dsc);
+    k_init_finish<<<(unsigned)n_inst, 32, 0, b->stream>>>(b->d_insts, (const unsigned long long*)dsc);
     const int rc = sync_batch(b, err, errlen);
+    const auto t2 = now();
+    if (verbose)
+      fprintf(stderr, "[econo] create: trace upload %.1f ms (%zu MB), init kernels %.1f ms\n", ms(t0, t1),
+              total >> 20, ms(t1, t2));
     dev_free(dt);
     dev_free(ds);
-    for (auto p : bufs) dev_free(p);
+    dev_free(dsc);
+    dev_free(dtr);
     if (rc) { econo_batch_destroy(b); return rc; }
   }
 #endif
