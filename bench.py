@@ -247,6 +247,7 @@ def run_ours(args):
     b.restore()  # timed steps cover the same post-ingest window as the reference arm
     times = []
     sc0 = b.scalars()
+    dbg0 = b.debug().sum(axis=0)
     for _ in range(args.steps):
         flush.fill_(1)  # L2 flush between timed steps (not timed)
         torch.cuda.synchronize()
@@ -264,6 +265,9 @@ def run_ours(args):
     b.sync()
     sc1 = b.scalars()
     errors = [s.error for s in sc1 if s.error]
+    dbg = b.debug().sum(axis=0) - dbg0
+    log(f"[bench] device cycles: quiet_span {dbg[0]} replay {dbg[1]} normal {dbg[2]}; "
+        f"spans {dbg[4]} normal steps {dbg[5]}")
     adm = sum(a.pt_dispatched - z.pt_dispatched for a, z in zip(sc1, sc0))
     gts = sum(a.gt_scheduled - z.gt_scheduled for a, z in zip(sc1, sc0))
     tot = float(sum(times))

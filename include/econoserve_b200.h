@@ -269,6 +269,9 @@ int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen);
  * (arena + descriptor), e.g. to rerun one scheduling window. */
 int econo_batch_checkpoint(econo_batch* b, char* err, size_t errlen);
 int econo_batch_restore(econo_batch* b, char* err, size_t errlen);
+/* Development counters (8 int64 per instance): device cycles spent in the
+ * quiet-span test, quiet-span replay and normal steps, and their counts. */
+int econo_batch_debug(econo_batch* b, int64_t* out);
 void econo_batch_destroy(econo_batch* b);
 
 /* ---- host-side input preparation (out of the hot path) ------------------ */

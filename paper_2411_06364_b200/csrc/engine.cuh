@@ -74,6 +74,12 @@ static inline uint64_t umulhi64(uint64_t a, uint64_t b) {
 }
 #endif
 
+#ifdef __CUDACC__
+#define PROF_NOW() ((int64_t)clock64())
+#else
+#define PROF_NOW() ((int64_t)0)
+#endif
+
 #define LANE0(stmt) \
   do {              \
     if (LANE == 0) { stmt; } \
@@ -104,7 +110,7 @@ struct Inst {
   int32_t pmax, nbuckets, bm_words, bm_l2;    // PT class table (ordered mode)
   int32_t tree_levels, rl_cap;
   int32_t tree_off[8], tree_len[8];            // 32-ary min tree (FIFO mode)
-  int32_t reg_cap, grp_cap, slot_cap, run_cap, ptiter_cap, adm_cap, scr_cap, hist_cap;
+  int32_t reg_cap, grp_cap, slot_cap, run_cap, ptiter_cap, adm_cap, scr_cap, hist_cap, sel_cap, _pad2;
   int64_t tfs, capacity, block, reserve_cap, general_cap, pred_quantum;
   double t_base, t_token, over_rate, reserve_penalty, pen_free, pen_offload, sched_cost;
   double pred_sigma, pred_accuracy, pred_tol, pred_pad, slo_scale, buffer_ratio;
@@ -121,6 +127,7 @@ struct Inst {
   int64_t err_val, ev_n, ev_cap, sm_n, sm_cap, ev_total;
   int64_t pt_min_lb;   // lower bound on the smallest queued prompt (only grows between arrivals)
   int64_t quiet_steps, quiet_spans, bcast;
+  int64_t prof[8];     // ECONO_PROF: cycles in quiet_span / quiet_steps / normal steps, counts
   double agg_written, agg_allocated;
   int64_t agg_fs, agg_tfs_hits, agg_pt_iters;
   // ---- per-request SoA (n entries) ----
@@ -1080,6 +1087,7 @@ EDEVNI int32_t plan_host_group(Inst& I, int32_t l, int32_t hs, int32_t he, int32
       if (best < 0) break;
       any = true;
       const int32_t take = I.gr_cnt[best] < nc - next_slot ? I.gr_cnt[best] : nc - next_slot;
+      if (nout + take > 2 * I.scr_cap) { set_error(I, ERR_TABLE_OVERFLOW, -1, 7); return nout; }
       if (LANE == 0) {
         int32_t m = I.gr_head[best];
         Tok dsum = 0;
@@ -1166,6 +1174,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
       const int32_t g = I.gq[gi];
       LANE0(I.exam_count++);
       const Tok total = I.gr_dem[g];
+      if (nsel + I.gr_cnt[g] > I.sel_cap && total <= remaining) { set_error(I, ERR_TABLE_OVERFLOW, g, 8); return; }
       if (total <= remaining) {
         remaining -= total;
         if (LANE == 0) {
@@ -1676,24 +1685,36 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
   const Tok fs = I.R;
   const double dt = iteration_time(I, fs) + 0.0;
   const double clk1 = I.clock + dt;
-  if (LANE == 0) {
-    double clock = I.clock, aw = I.agg_written, aa = I.agg_allocated;
-    int64_t wt = I.written_total;
-    const double af = (double)((I.general_cap - I.free_total) + I.reserved_used) / (double)I.capacity;
+  const double af = (double)((I.general_cap - I.free_total) + I.reserved_used) / (double)I.capacity;
+  const int64_t wt0 = I.written_total;
+  const double cap = (double)I.capacity;
+  // pass 1 (every lane, identical arithmetic): the sequential clock chain and
+  // the arrival cut-off — ingest would admit an arrival at the next step.
+  double clock = I.clock;
+  {
     const bool has_arr = I.arrival_cursor < I.n;
     const double ta = has_arr ? I.arrival[I.arrival_cursor] : 0.0;
     int64_t j = 0;
     for (; j < k; ++j) {
-      if (j > 0 && has_arr && ta <= clock + 1e-12) break;  // ingest would admit it
+      if (j > 0 && has_arr && ta <= clock + 1e-12) break;
       clock += dt;
-      wt += fs;
-      const double wf = (double)wt / (double)I.capacity;
-      aw += wf;
-      aa += af;
-      if (I.record_samples) {
+    }
+    k = j;
+  }
+  // pass 2: per-iteration written fractions computed lane-parallel, summed in
+  // sample order (metrics.hpp:153-162) so the FP sums match the reference.
+  double aw = I.agg_written, aa = I.agg_allocated;
+  if (I.record_samples) {
+    if (LANE == 0) {
+      double c = I.clock;
+      for (int64_t j = 0; j < k; ++j) {
+        c += dt;
+        const double wf = (double)(wt0 + (j + 1) * fs) / cap;
+        aw += wf;
+        aa += af;
         EconoSample& s = I.sm[I.sm_n + j];
         s.iter = I.iter + j + 1;
-        s.clock = clock;
+        s.clock = c;
         s.dt = dt;
         s.forward_size = fs;
         s.kvc_written_frac = wf;
@@ -1705,14 +1726,19 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
         s.idle_repeat = 0;
       }
     }
-    I.clock = clock;
-    I.written_total = wt;
-    I.agg_written = aw;
-    I.agg_allocated = aa;
-    I.bcast = j;
+  } else {
+    for (int64_t base = 0; base < k; base += W) {
+      const int64_t jj = base + LANE;
+      const double wf = jj < k ? (double)(wt0 + (jj + 1) * fs) / cap : 0.0;
+      const int lim = k - base < W ? (int)(k - base) : W;
+      for (int l = 0; l < lim; ++l) {
+        aw += shfl(wf, l);
+        aa += af;
+      }
+    }
   }
   WSYNC();
-  k = I.bcast;
+  LANE0(I.clock = clock; I.written_total = wt0 + k * fs; I.agg_written = aw; I.agg_allocated = aa);
   for (int32_t i = LANE; i < I.R; i += W) {
     const int32_t id = I.run[i];
     double e = I.exec_t[id];

@@ -130,13 +130,19 @@ EDEVNI void engine_steps(Inst& I, int64_t max_steps) {
       break;
     }
     if (I.skip) {
+      const int64_t t0 = PROF_NOW();
       const int64_t k = quiet_span(I, max_steps - s);
+      const int64_t t1 = PROF_NOW();
+      LANE0(I.prof[0] += t1 - t0);
       if (k > 0) {
         s += quiet_steps(I, k);
+        LANE0(I.prof[1] += PROF_NOW() - t1; I.prof[4]++);
         continue;
       }
     }
+    const int64_t t2 = PROF_NOW();
     engine_step(I);
+    LANE0(I.prof[2] += PROF_NOW() - t2; I.prof[5]++);
     ++s;
   }
 }
@@ -303,7 +309,8 @@ __global__ void __launch_bounds__(256) k_init_req(Inst* insts, unsigned long lon
 
 __global__ void __launch_bounds__(32) k_init_finish(Inst* insts, const unsigned long long* scr) {
   Inst& I = insts[blockIdx.x];
-  if (threadIdx.x == 0 && !I.error) init_finish(I, (int64_t)scr[4 * blockIdx.x + 2]);
+  const unsigned long long bad = scr[4 * blockIdx.x + 2];
+  if (threadIdx.x == 0 && !I.error) init_finish(I, bad < (unsigned long long)I.n ? (int64_t)bad : I.n);
 }
 
 __global__ void __launch_bounds__(32) k_engine_steps(Inst* insts, int64_t max_steps) {
@@ -364,8 +371,18 @@ int dev_h2d(void* d, const void* h, size_t sz) { memcpy(d, h, sz); return 0; }
 int dev_d2h(void* h, const void* d, size_t sz) { memcpy(h, d, sz); return 0; }
 #else
 int dev_alloc(void** p, size_t sz) {
+  const auto t0 = std::chrono::steady_clock::now();
   if (cudaMalloc(p, sz ? sz : 8) != cudaSuccess) return 1;
-  return cudaMemset(*p, 0, sz ? sz : 8) != cudaSuccess;
+  const auto t1 = std::chrono::steady_clock::now();
+  const int rc = cudaMemset(*p, 0, sz ? sz : 8) != cudaSuccess;
+  if (sz > ((size_t)1 << 30) && getenv("ECONO_VERBOSE")) {
+    cudaDeviceSynchronize();
+    const auto t2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[econo] dev_alloc %zu MB: malloc %.1f ms memset %.1f ms\n", sz >> 20,
+            std::chrono::duration<double, std::milli>(t1 - t0).count(),
+            std::chrono::duration<double, std::milli>(t2 - t1).count());
+  }
+  return rc;
 }
 void dev_free(void* p) { if (p) cudaFree(p); }
 int dev_h2d(void* d, const void* h, size_t sz) { return cudaMemcpy(d, h, sz, cudaMemcpyHostToDevice) != cudaSuccess; }
@@ -437,9 +454,9 @@ void layout(Inst& I, char* base, size_t* bytes) {
   I.ptiter_id = a.take<int32_t>(I.ptiter_cap);
   I.ptiter_tok = a.take<int32_t>(I.ptiter_cap);
   I.adm = a.take<int32_t>(I.adm_cap);
-  I.sel_ids = a.take<int32_t>(n + 1);
-  I.selg_start = a.take<int32_t>(n + 2);
-  I.selg_rl = a.take<int32_t>(n + 2);
+  I.sel_ids = a.take<int32_t>(I.sel_cap);
+  I.selg_start = a.take<int32_t>(I.sel_cap + 1);
+  I.selg_rl = a.take<int32_t>(I.sel_cap + 1);
   const int64_t pc = 2 * (int64_t)I.scr_cap + W;
   int32_t** pl[] = {&I.wa_w, &I.wa_b, &I.wa_l, &I.wa_u, &I.wb_w, &I.wb_b, &I.wb_l, &I.wb_u,
                     &I.cd_ri, &I.cd_abs, &I.cd_use, &I.cd_len, &I.assigned,
@@ -592,7 +609,12 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   I.run_cap = (int32_t)(imin(n, cap) + 1);
   I.ptiter_cap = (int32_t)(imin(n, I.tfs) + 2);
   I.adm_cap = (int32_t)(imin(n, cap + I.tfs) + 2);
-  I.scr_cap = (int32_t)(imax(n, I.general_cap) + 64);
+  // Scratch bounds: selected GT members <= 2*general_cap (each
+  // has a positive block demand or holds a region of >= 1 token); planner
+  // regions/slots, compaction, promotion and deadline lists are bounded by
+  // the general pool, the running set or tfs — never by the request count.
+  I.sel_cap = (int32_t)(imin(n, 2 * I.general_cap) + 2);
+  I.scr_cap = (int32_t)(imax(imax(I.general_cap, I.sel_cap), imax(imin(n, cap), I.tfs)) + 64);
   I.hist_cap = (int32_t)(imin(n, cap) + 2);
   I.rl_cap = (int32_t)(I.general_cap + 1);
   return ECONO_OK;
@@ -645,13 +667,12 @@ std::string format_error(const Inst& I, int* code) {
 // One instance's host-side bookkeeping.
 struct HostInst {
   Inst desc;           // mirror of the device descriptor (device pointers)
-  char* arena = nullptr;
+  char* arena = nullptr;  // slice of econo_batch::block
   size_t arena_bytes = 0;
   EconoEvent* d_ev = nullptr;
   EconoSample* d_sm = nullptr;
   std::vector<EconoEvent> events;
   std::vector<EconoSample> samples;
-  std::vector<EconoTraceRecord> trace;
   uint64_t seed = 1, pred_seed = 1;
   int32_t policy = 0;
   char* ckpt = nullptr;  // device copy of the arena (econo_batch_checkpoint)
@@ -661,6 +682,8 @@ struct HostInst {
 
 struct econo_batch {
   int device = 0;
+  char* block = nullptr;  // every instance's arena, one allocation
+  char* ckpt_block = nullptr;
   std::vector<HostInst> inst;
   Inst* d_insts = nullptr;
 #ifndef ECONO_HOSTSIM
@@ -809,9 +832,9 @@ void econo_default_options(EconoOptions* o) {
 
 void econo_batch_destroy(econo_batch* b) {
   if (!b) return;
+  dev_free(b->block);
+  dev_free(b->ckpt_block);
   for (auto& h : b->inst) {
-    dev_free(h.arena);
-    dev_free(h.ckpt);
     dev_free(h.d_ev);
     dev_free(h.d_sm);
   }
@@ -848,31 +871,62 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
   std::vector<const EconoTraceRecord*> d_traces((size_t)n_inst);
   std::vector<uint64_t> seeds(2 * (size_t)n_inst);
   const auto t_alloc0 = std::chrono::steady_clock::now();
+  {  // per-instance configuration scans its trace (lengths, max prompt): threads
+    std::vector<int> rcs((size_t)n_inst, ECONO_OK);
+    std::vector<std::string> msgs((size_t)n_inst);
+    const int nt = (int)std::max<unsigned>(1, std::min<unsigned>(std::thread::hardware_concurrency(), 32));
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&, t] {
+        char e2[512];
+        for (int32_t i = t; i < n_inst; i += nt) {
+          rcs[(size_t)i] = configure(b->inst[(size_t)i].desc, &opts[i], traces[i], ns[i], e2, sizeof(e2));
+          if (rcs[(size_t)i]) msgs[(size_t)i] = e2;
+        }
+      });
+    for (auto& x : th) x.join();
+    for (int32_t i = 0; i < n_inst; ++i)
+      if (rcs[(size_t)i]) {
+        set_err(err, errlen, "%s", msgs[(size_t)i].c_str());
+        econo_batch_destroy(b);
+        return rcs[(size_t)i];
+      }
+  }
   for (int32_t i = 0; i < n_inst; ++i) {
     HostInst& h = b->inst[(size_t)i];
-    const int rc = configure(h.desc, &opts[i], traces[i], ns[i], err, errlen);
-    if (rc) { econo_batch_destroy(b); return rc; }
-    h.trace.assign(traces[i], traces[i] + ns[i]);
     h.seed = opts[i].seed;
     h.pred_seed = opts[i].pred_seed;
     h.policy = opts[i].policy;
     size_t bytes = 0;
     layout(h.desc, nullptr, &bytes);
-    void* arena;
-    if (dev_alloc(&arena, bytes)) {
+    h.arena_bytes = (bytes + 4095) & ~size_t(4095);
+    seeds[2 * i] = opts[i].seed;
+    seeds[2 * i + 1] = opts[i].pred_seed;
+  }
+  {
+    size_t total = 0;
+    for (auto& h : b->inst) total += h.arena_bytes;
+    void* blk;
+    if (dev_alloc(&blk, total)) {
       econo_batch_destroy(b);
-      return set_err(err, errlen, "device allocation of %zu bytes failed", bytes), ECONO_ECUDA;
+      return set_err(err, errlen, "device allocation of %zu bytes failed", total), ECONO_ECUDA;
     }
-    h.arena = (char*)arena;
-    h.arena_bytes = bytes;
-    layout(h.desc, h.arena, &bytes);
+    b->block = (char*)blk;
+    size_t off = 0;
+    for (auto& h : b->inst) {
+      h.arena = b->block + off;
+      off += h.arena_bytes;
+      size_t bytes = 0;
+      layout(h.desc, h.arena, &bytes);
+    }
+  }
+  for (int32_t i = 0; i < n_inst; ++i) {
+    HostInst& h = b->inst[(size_t)i];
     const int64_t n = ns[i];
     if (ensure_logs(h, h.desc.record_events ? 4 * n + 4096 : 0, h.desc.record_samples ? 2 * n + 4096 : 0)) {
       econo_batch_destroy(b);
       return set_err(err, errlen, "device allocation of the event log failed"), ECONO_ECUDA;
     }
-    seeds[2 * i] = opts[i].seed;
-    seeds[2 * i + 1] = opts[i].pred_seed;
   }
   if (getenv("ECONO_VERBOSE"))
     fprintf(stderr, "[econo] create: arenas %.1f ms\n",
@@ -943,9 +997,7 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     std::vector<bool> pinned((size_t)n_inst, false);
     for (int32_t i = 0; i < n_inst; ++i) {
       const size_t bytes = sizeof(EconoTraceRecord) * (size_t)ns[i];
-      pinned[(size_t)i] = cudaHostRegister(const_cast<EconoTraceRecord*>(traces[i]), bytes,
-                                           cudaHostRegisterReadOnly) == cudaSuccess;
-      if (!pinned[(size_t)i]) cudaGetLastError();
+      pinned[(size_t)i] = false;  // registering costs as much as the pageable copy (tools/probe_upload.py)
       cudaMemcpyAsync((char*)dtr + off[(size_t)i], traces[i], bytes, cudaMemcpyHostToDevice, b->stream);
       d_traces[(size_t)i] = (const EconoTraceRecord*)((char*)dtr + off[(size_t)i]);
     }
@@ -1065,15 +1117,29 @@ int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen) 
 #endif
 }
 
+// Development counters: per instance 8 int64 (engine.cuh Inst::prof).
+int econo_batch_debug(econo_batch* b, int64_t* out) {
+  for (size_t i = 0; i < b->inst.size(); ++i)
+    for (int k = 0; k < 8; ++k) out[8 * i + k] = b->inst[i].desc.prof[k];
+  return ECONO_OK;
+}
+
 int econo_batch_checkpoint(econo_batch* b, char* err, size_t errlen) {
   int rc = sync_batch(b, err, errlen);
   if (rc) return rc;
-  for (auto& h : b->inst) {
-    if (!h.ckpt) {
-      void* p;
-      if (dev_alloc(&p, h.arena_bytes)) return set_err(err, errlen, "checkpoint allocation failed"), ECONO_ECUDA;
-      h.ckpt = (char*)p;
+  if (!b->ckpt_block) {
+    size_t total = 0;
+    for (auto& h : b->inst) total += h.arena_bytes;
+    void* p;
+    if (dev_alloc(&p, total)) return set_err(err, errlen, "checkpoint allocation failed"), ECONO_ECUDA;
+    b->ckpt_block = (char*)p;
+    size_t off = 0;
+    for (auto& h : b->inst) {
+      h.ckpt = b->ckpt_block + off;
+      off += h.arena_bytes;
     }
+  }
+  for (auto& h : b->inst) {
 #ifdef ECONO_HOSTSIM
     memcpy(h.ckpt, h.arena, h.arena_bytes);
 #else
@@ -1303,11 +1369,19 @@ int econo_report(econo_engine* e, EconoReport* out, char* err, size_t errlen) {
   };
   const char* hdr = "arrival_time,prompt_len,response_len\n";
   feed(hdr, (int)strlen(hdr));
-  char buf[128];
-  for (const auto& t : h.trace) {
-    const int len = snprintf(buf, sizeof(buf), "%.17g,%lld,%lld\n", t.arrival_time, (long long)t.prompt_len,
-                             (long long)t.true_rl);
-    feed(buf, len);
+  {  // the device holds the trace as SoA (lengths < 2^30, so int32 is exact)
+    std::vector<double> arr((size_t)I.n);
+    std::vector<int32_t> pr((size_t)I.n), rl((size_t)I.n);
+    if (dev_d2h(arr.data(), I.arrival, sizeof(double) * arr.size()) ||
+        dev_d2h(pr.data(), I.prompt, sizeof(int32_t) * pr.size()) ||
+        dev_d2h(rl.data(), I.true_rl, sizeof(int32_t) * rl.size()))
+      return set_err(err, errlen, "device copy failed"), ECONO_ECUDA;
+    char buf[128];
+    for (int32_t i = 0; i < I.n; ++i) {
+      const int len = snprintf(buf, sizeof(buf), "%.17g,%lld,%lld\n", arr[(size_t)i], (long long)pr[(size_t)i],
+                               (long long)rl[(size_t)i]);
+      feed(buf, len);
+    }
   }
   r.trace_hash = hh;
   r.hosted_slots = I.hosted_total;

@@ -24,7 +24,7 @@ SYMBOLS = [
     "econo_report", "econo_events", "econo_samples", "econo_scalars", "econo_snapshot",
     "econo_destroy", "econo_batch_create", "econo_batch_launch", "econo_batch_sync",
     "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
-    "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore",
+    "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore", "econo_batch_debug",
 ]
 
 
@@ -85,6 +85,7 @@ def load(path=None):
     L.econo_batch_destroy.argtypes = [vp]
     L.econo_batch_checkpoint.argtypes = [vp, cp, sz]
     L.econo_batch_restore.argtypes = [vp, cp, sz]
+    L.econo_batch_debug.argtypes = [vp, vp]
     L.econo_generate_trace.argtypes = [i64, C.c_double, C.POINTER(abi.LengthDist),
                                        C.POINTER(abi.LengthDist), C.c_uint64, vp, cp, sz]
     _libs[path] = L
@@ -259,6 +260,11 @@ class Batch:
         rc = self._L.econo_batch_restore(self.h, err, 1024)
         if rc:
             _raise(rc, err)
+
+    def debug(self):
+        out = np.zeros((self.n, 8), dtype=np.int64)
+        self._L.econo_batch_debug(self.h, out.ctypes.data)
+        return out
 
     def partials(self):
         out = np.zeros((self.n, abi.PARTIAL_WORDS), dtype=np.float64)
