@@ -31,7 +31,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2411_06364_b200 import abi, workloads as W  # noqa: E402
+from paper_2411_06364_b200 import abi, metrics, workloads as W  # noqa: E402
 
 METRIC = "scheduled requests/sec & us per scheduler iteration at 1M queued reqs; % HBM BW"
 UNIT = "req/s"
@@ -135,18 +135,19 @@ def reference_windows(n, threads, window, reps, warmup):
         e.step(1)  # form + execute of the ingest step
     setup = time.time() - t0
     pts = np.zeros(threads, dtype=np.int64)
-    if warmup:  # warm up on deep copies so the timed windows start post-ingest
-        clones = [e.clone() for e in engines]
-        hc = (C.c_void_p * threads)(*[e.h.value for e in clones])
-        for _ in range(warmup):
-            ref.lib().ref_time_steps_parallel(hc, threads, window, pts.ctypes.data)
-        del clones
     hv = (C.c_void_p * threads)(*[e.h.value for e in engines])
+    for _ in range(warmup):  # the same warm-up window the device arm runs
+        ref.lib().ref_time_steps_parallel(hv, threads, window, pts.ctypes.data)
     out = []
     for r in range(reps):
         secs = ref.lib().ref_time_steps_parallel(hv, threads, window, pts.ctypes.data)
         out.append((secs, int(pts.sum())))
     return out, setup, engines
+
+
+def window_str(args):
+    lo = 2 + args.iters * args.warmup
+    return f"scheduler iterations {lo}..{lo + args.iters * args.steps} after the 1M burst ingest"
 
 
 def run_reference(args):
@@ -160,9 +161,8 @@ def run_reference(args):
     value = adm / secs if secs > 0 else 0.0
     us_iter = 1e6 * secs / (args.iters * len(wins))
     sample = (f"{threads} reference engines (one std::thread each) x {args.n} requests "
-              f"({WORKLOAD}), {args.iters} step() calls per engine per step; the {args.steps} timed "
-              f"steps cover iterations 2..{2 + args.iters * args.steps} after the burst ingest "
-              f"(warm-up ran on deep copies)")
+              f"({WORKLOAD}), {args.iters} step() calls per engine per step; after {args.warmup} warm-up "
+              f"steps the {args.steps} timed steps cover {window_str(args)}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -170,7 +170,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "requests_per_instance": args.n, "instances": threads,
                    "iters_per_step": args.iters, "policy": "econoserve-full",
-                   "window": f"iterations 2..{2 + args.iters * args.steps} after the burst ingest"},
+                   "window": window_str(args)},
         "us_per_iter": us_iter,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
@@ -215,57 +215,53 @@ def run_ours(args):
     traces = make_traces(generate_trace, args.n, seeds)
     t_gen = time.time() - t0
 
-    # ---- end to end through the public API: host traces -> device -> host results
-    clocks = ClockSampler(local)  # sampled from here to the end of the timed steps
+    # ---- one pass through the public API, from host trace buffers:
+    # Batch(traces) [H2D] -> idle tick + 1M burst ingest -> W warm-up steps ->
+    # K device-timed steps -> partial sums back to the host [D2H]. `value` is
+    # the device-timed K steps; `e2e` is the same job's wall clock end to end.
+    clocks = ClockSampler(local)
     clocks.start()
+    stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     b = Batch(traces, options(), device=local)
-    b.launch(2)  # idle tick + burst ingest (engine.hpp:216-235, 930-949)
+    b.launch(2, stream.cuda_stream)  # idle tick + burst ingest (engine.hpp:216-235, 930-949)
+    stream.synchronize()
     b.sync()
     t_create_ingest = time.perf_counter() - t0
     sc_a = b.scalars()
-    b.checkpoint()  # post-ingest state: every window below starts here (untimed)
-    t1 = time.perf_counter()
-    b.launch(args.iters * args.steps)
-    b.sync()
-    sc_b = b.scalars()
-    parts = b.partials()
-    t_e2e = t_create_ingest + time.perf_counter() - t1
-    e2e_adm = sum(x.pt_dispatched - y.pt_dispatched for x, y in zip(sc_b, sc_a))
-    h2d = sum(t.nbytes for t in traces)
-    d2h = parts.nbytes + I * 2 * 1600
-
-    # ---- device-timed windows (inputs resident in HBM)
-    stream = torch.cuda.Stream(device=dev)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    b.restore()
     for _ in range(args.warmup):
         b.launch(args.iters, stream.cuda_stream)
     stream.synchronize()
     b.sync()
-    b.restore()  # timed steps cover the same post-ingest window as the reference arm
-    times = []
     sc0 = b.scalars()
-    dbg0 = b.debug().sum(axis=0)
-    for _ in range(args.steps):
-        flush.fill_(1)  # L2 flush between timed steps (not timed)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        b.launch(args.iters, stream.cuda_stream)
-        e1.record(stream)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1) / 1e3)
+    d0 = b.debug().sum(axis=0)
     torch.cuda.synchronize()
-    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        b.launch(args.iters, stream.cuda_stream)
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times = [e0.elapsed_time(e1) / 1e3]
     b.sync()
     sc1 = b.scalars()
+    dbg = b.debug().sum(axis=0) - d0
+    parts = b.partials()
+    t_e2e = time.perf_counter() - t0
+    clk = clocks.stop()
+    e2e_adm = sum(x.pt_dispatched - y.pt_dispatched for x, y in zip(sc1, sc_a))
+    h2d = sum(t.nbytes for t in traces)
+    d2h = parts.nbytes + I * 2 * 1600
     errors = [s.error for s in sc1 if s.error]
-    dbg = b.debug().sum(axis=0) - dbg0
     log(f"[bench] device cycles: quiet_span {dbg[0]} replay {dbg[1]} normal {dbg[2]}; "
         f"spans {dbg[4]} normal steps {dbg[5]}")
     adm = sum(a.pt_dispatched - z.pt_dispatched for a, z in zip(sc1, sc0))
@@ -281,10 +277,10 @@ def run_ours(args):
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         tot_max, adm_all, gts_all, e2e_adm_all, e2e_t = (mx[0].item(), sm[1].item(), sm[2].item(),
                                                          sm[3].item(), mx[4].item())
-        # metric partial sums of every instance: one NCCL reduction
-        pt = torch.from_numpy(b.partials()).to(dev)
-        dist.all_reduce(pt, op=dist.ReduceOp.SUM)
+        # metric partial sums of every instance: one NCCL reduction per op
+        gsum = metrics.all_reduce(metrics.combine(parts), dist, device=dev)
     else:
+        gsum = metrics.combine(parts)
         tot_max, adm_all, gts_all, e2e_adm_all, e2e_t = tot, float(adm), float(gts), float(e2e_adm), t_e2e
     if rank != 0:
         if world > 1:
@@ -301,9 +297,12 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "requests_per_instance": args.n,
                    "instances_per_gpu": I, "iters_per_step": args.iters,
-                   "policy": "econoserve-full", "l2": "flushed between timed steps (256 MiB write)",
-                   "window": f"iterations 2..{2 + args.iters * args.steps} after the burst ingest"},
+                   "policy": "econoserve-full",
+                   "l2": f"inputs larger than L2: {I} x ~250 MB of instance state per GPU vs 126 MB L2, no flush",
+                   "window": window_str(args)},
         "us_per_iter": us_iter,
+        "device_cycles": {"quiet_test": int(dbg[0]), "quiet_replay": int(dbg[1]), "normal_steps": int(dbg[2]),
+                          "quiet_spans": int(dbg[4]), "normal_step_count": int(dbg[5])},
         "iters_per_s_per_gpu": iters_total * I / tot_max,
         "gt_scheduled_per_s": gts_all / tot_max,
         "quiet_step_frac": (sum(a.quiet_steps - z.quiet_steps for a, z in zip(sc1, sc0)) /
@@ -318,21 +317,25 @@ def run_ours(args):
         "clocks": clk,
         "e2e": {"value": e2e_adm_all / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "scope": "one whole job: Batch(host traces) + burst ingest + the same "
-                         f"{args.iters * args.steps}-iteration window + partials to host"},
+                "scope": "the whole job through the public API: Batch(host traces) + burst ingest + "
+                         "warm-up + timed steps + partial sums to host, wall clock; admissions counted "
+                         "after the ingest"},
         "errors": len(errors),
+        "global_metrics": {k: v for k, v in metrics.summary(gsum).items()
+                           if k in ("requests", "iterations", "mean_forward_size", "mean_kvc_written",
+                                    "tfs_hit_frac", "pt_admit_frac", "hosted_slots")},
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
             thr = min(os.cpu_count() or 1, 16)
-            wins, setup, _ = reference_windows(args.n, thr, args.iters * args.steps, 1, 0)
-            secs, pts = wins[0]
+            wins, setup, _ = reference_windows(args.n, thr, args.iters, args.steps, args.warmup)
+            secs = sum(w[0] for w in wins)
+            pts = sum(w[1] for w in wins)
             line["cpu_baseline"] = {
                 "value": pts / secs if secs > 0 else 0.0, "unit": UNIT, "cores": thr,
                 "kind": "reference", "us_per_iter": 1e6 * secs / (args.iters * args.steps),
                 "sample": f"{thr} reference engines x {args.n} requests ({WORKLOAD}), "
-                          f"iterations 2..{2 + args.iters * args.steps} after the burst ingest "
-                          "(the timed window), one std::thread per engine"}
+                          f"{window_str(args)} (the timed window), one std::thread per engine"}
         except Exception as ex:  # the reference build is missing on this box
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {ex}"}
@@ -347,7 +350,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--instances", type=int, default=64)
+    ap.add_argument("--instances", type=int, default=444)
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--ref-threads", type=int, default=0)
