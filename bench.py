@@ -49,11 +49,21 @@ def options(record=False):
     return o
 
 
-def make_traces(gen, n, seeds, threads=32):
+def make_traces(gen, n, seeds, threads=32, pinned=False):
+    """One synthetic trace per seed. pinned=True generates straight into one
+    page-locked host buffer (the e2e contract: inputs copied from pinned host
+    memory), returned as per-instance views."""
     c = W.CONFIGS[WORKLOAD]
+    outs = [None] * len(seeds)
+    if pinned:
+        import torch
+        rec = abi.TRACE_DTYPE.itemsize
+        buf = torch.empty(len(seeds) * n * rec, dtype=torch.uint8, pin_memory=True).numpy()
+        outs = [buf[i * n * rec:(i + 1) * n * rec].view(abi.TRACE_DTYPE) for i in range(len(seeds))]
     with ThreadPoolExecutor(threads) as ex:
-        return list(ex.map(lambda s: gen(n, c["rate"], c["shape"]["prompt"], c["shape"]["rl"], s),
-                           seeds))
+        return list(ex.map(lambda a: gen(n, c["rate"], c["shape"]["prompt"], c["shape"]["rl"], a[0],
+                                         **({"out": a[1]} if pinned else {})),
+                           zip(seeds, outs)))
 
 
 class ClockSampler:
@@ -145,9 +155,10 @@ def reference_windows(n, threads, window, reps, warmup):
     return out, setup, engines
 
 
-def window_str(args):
-    lo = 2 + args.iters * args.warmup
-    return f"scheduler iterations {lo}..{lo + args.iters * args.steps} after the 1M burst ingest"
+def window_str(args, iters=None):
+    it = iters or args.iters
+    lo = 2 + it * args.warmup
+    return f"scheduler iterations {lo}..{lo + it * args.steps} after the 1M burst ingest"
 
 
 def run_reference(args):
@@ -155,22 +166,23 @@ def run_reference(args):
     if rank != 0:
         return
     threads = args.ref_threads or min(os.cpu_count() or 1, 32)
-    wins, setup, _ = reference_windows(args.n, threads, args.iters, args.steps, args.warmup)
+    wins, setup, _ = reference_windows(args.n, threads, args.ref_iters, args.steps, args.warmup)
     secs = sum(w[0] for w in wins)
     adm = sum(w[1] for w in wins)
     value = adm / secs if secs > 0 else 0.0
-    us_iter = 1e6 * secs / (args.iters * len(wins))
+    us_iter = 1e6 * secs / (args.ref_iters * len(wins))
     sample = (f"{threads} reference engines (one std::thread each) x {args.n} requests "
-              f"({WORKLOAD}), {args.iters} step() calls per engine per step; after {args.warmup} warm-up "
-              f"steps the {args.steps} timed steps cover {window_str(args)}")
+              f"({WORKLOAD}), a bounded sample of {args.ref_iters} step() calls per engine per step "
+              f"(~28 ms each at 1M queued); after {args.warmup} warm-up steps the {args.steps} timed "
+              f"steps cover {window_str(args, args.ref_iters)}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / len(wins), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "requests_per_instance": args.n, "instances": threads,
-                   "iters_per_step": args.iters, "policy": "econoserve-full",
-                   "window": window_str(args)},
+                   "iters_per_step": args.ref_iters, "policy": "econoserve-full",
+                   "window": window_str(args, args.ref_iters)},
         "us_per_iter": us_iter,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
@@ -212,7 +224,7 @@ def run_ours(args):
     I = args.instances
     seeds = [1000 + rank * I + i for i in range(I)]
     t0 = time.time()
-    traces = make_traces(generate_trace, args.n, seeds)
+    traces = make_traces(generate_trace, args.n, seeds, pinned=True)
     t_gen = time.time() - t0
 
     # ---- one pass through the public API, from host trace buffers:
@@ -298,7 +310,7 @@ def run_ours(args):
         "config": {"workload": WORKLOAD, "requests_per_instance": args.n,
                    "instances_per_gpu": I, "iters_per_step": args.iters,
                    "policy": "econoserve-full",
-                   "l2": f"inputs larger than L2: {I} x ~250 MB of instance state per GPU vs 126 MB L2, no flush",
+                   "l2": f"inputs larger than L2: {I} x ~184 MB of instance state per GPU vs 126 MB L2, no flush",
                    "window": window_str(args)},
         "us_per_iter": us_iter,
         "device_cycles": {"quiet_test": int(dbg[0]), "quiet_replay": int(dbg[1]), "normal_steps": int(dbg[2]),
@@ -328,14 +340,15 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         try:
             thr = min(os.cpu_count() or 1, 16)
-            wins, setup, _ = reference_windows(args.n, thr, args.iters, args.steps, args.warmup)
+            wins, setup, _ = reference_windows(args.n, thr, args.ref_iters, args.steps, args.warmup)
             secs = sum(w[0] for w in wins)
             pts = sum(w[1] for w in wins)
             line["cpu_baseline"] = {
                 "value": pts / secs if secs > 0 else 0.0, "unit": UNIT, "cores": thr,
-                "kind": "reference", "us_per_iter": 1e6 * secs / (args.iters * args.steps),
+                "kind": "reference", "us_per_iter": 1e6 * secs / (args.ref_iters * args.steps),
                 "sample": f"{thr} reference engines x {args.n} requests ({WORKLOAD}), "
-                          f"{window_str(args)} (the timed window), one std::thread per engine"}
+                          f"{window_str(args, args.ref_iters)} ({args.ref_iters} step() calls per engine per "
+                          f"step: a bounded sample of the same workload), one std::thread per engine"}
         except Exception as ex:  # the reference build is missing on this box
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {ex}"}
@@ -350,8 +363,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--instances", type=int, default=444)
-    ap.add_argument("--iters", type=int, default=100)
+    ap.add_argument("--instances", type=int, default=740,
+                    help="serving instances per GPU (5 per SM; ~184 MB of HBM each at 1M requests)")
+    ap.add_argument("--iters", type=int, default=1000,
+                    help="scheduler iterations per instance per step (one k_engine_steps launch)")
+    ap.add_argument("--ref-iters", type=int, default=100,
+                    help="reference arm / cpu_baseline: step() calls per engine per step (bounded sample)")
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -258,6 +258,15 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* n, 
  * max_steps steps on `stream` (a cudaStream_t, NULL = the handle's stream).
  * Asynchronous: no host synchronisation. */
 int econo_batch_launch(econo_batch* b, int64_t max_steps, void* stream);
+/* n_launches consecutive econo_batch_launch passes, issued as n_lanes (<= 32)
+ * independent launch chains over contiguous instance ranges, each on its own
+ * stream, forked from and joined back into `stream`. Instances never wait
+ * for each other between passes, so one slow instance delays only its lane
+ * (run_sweep's workers likewise never wait for each other, sweep.hpp:127-141).
+ * Set CUDA_DEVICE_MAX_CONNECTIONS=32 before the CUDA context exists so the
+ * lanes map to distinct hardware queues. Asynchronous. */
+int econo_batch_launch_lanes(econo_batch* b, int64_t max_steps, int32_t n_launches, int32_t n_lanes,
+                             void* stream);
 int econo_batch_sync(econo_batch* b, char* err, size_t errlen);
 int econo_batch_scalars(econo_batch* b, EconoScalars* out /* n_inst entries */);
 int econo_batch_engine(econo_batch* b, int32_t i, econo_engine** out); /* borrowed view */
@@ -269,8 +278,10 @@ int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen);
  * (arena + descriptor), e.g. to rerun one scheduling window. */
 int econo_batch_checkpoint(econo_batch* b, char* err, size_t errlen);
 int econo_batch_restore(econo_batch* b, char* err, size_t errlen);
-/* Development counters (8 int64 per instance): device cycles spent in the
- * quiet-span test, quiet-span replay and normal steps, and their counts. */
+/* Development counters (ECONO_DEBUG_WORDS int64 per instance): device cycles
+ * spent in the quiet-span test, quiet-span replay and normal steps (and its
+ * phases), and their counts; layout documented at engine.cuh Inst::prof. */
+#define ECONO_DEBUG_WORDS 16
 int econo_batch_debug(econo_batch* b, int64_t* out);
 void econo_batch_destroy(econo_batch* b);
 

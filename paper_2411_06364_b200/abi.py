@@ -23,6 +23,7 @@ EV_KINDS = ["arrive", "gt_schedule", "hosted", "pt_dispatch", "prefill_done", "c
 MAX_BOUNDS = 8
 MAX_HIST = 256
 PARTIAL_WORDS = 32
+DEBUG_WORDS = 16  # ECONO_DEBUG_WORDS
 
 
 class TraceRecord(C.Structure):

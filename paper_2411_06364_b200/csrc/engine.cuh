@@ -42,6 +42,7 @@
 #define FFS(m) (__ffs(m) - 1)
 #define POPC(m) __popc(m)
 #define LANEMASK_LT ((1u << LANE) - 1u)
+#define SMEM_ADD(p, v) atomicAdd((p), (v))
 #define CLZ64(x) __clzll((long long)(x))
 #define CLZ32(x) __clz((int)(x))
 template <class T> EDEV T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
@@ -65,6 +66,7 @@ EHD uint64_t umulhi64(uint64_t a, uint64_t b) {
 #define FFS(m) ((m) ? 0 : -1)
 #define POPC(m) ((m) ? 1 : 0)
 #define LANEMASK_LT 0u
+#define SMEM_ADD(p, v) (*(p) += (v))
 #define CLZ64(x) __builtin_clzll(x)
 #define CLZ32(x) __builtin_clz(x)
 template <class T> static inline T shfl(T v, int) { return v; }
@@ -126,8 +128,13 @@ struct Inst {
   int32_t error, err_id, status, mt_i, pmt_i, _pad0;
   int64_t err_val, ev_n, ev_cap, sm_n, sm_cap, ev_total;
   int64_t pt_min_lb;   // lower bound on the smallest queued prompt (only grows between arrivals)
+  int32_t bcnt[ECONO_MAX_BOUNDS + 2];  // queued PTs per deadline bucket (ordered mode)
   int64_t quiet_steps, quiet_spans, bcast;
-  int64_t prof[8];     // ECONO_PROF: cycles in quiet_span / quiet_steps / normal steps, counts
+  // device cycle counters (econo_batch_debug): [0] quiet-span tests [1] quiet
+  // replays [2] normal steps [4] spans [5] normal-step count; normal-step
+  // phases [6] ingest [7] GT select+schedule [8] pipelining [9] PT batching
+  // [10] execute_iteration; [11] launch total [12] launches.
+  int64_t prof[16];
   double agg_written, agg_allocated;
   int64_t agg_fs, agg_tfs_hits, agg_pt_iters;
   // ---- per-request SoA (n entries) ----
@@ -401,7 +408,7 @@ EDEV void bm_set_shared(Inst& I, int b, int p) {
 }
 // Largest nonempty prompt class p <= x in bucket b, or -1.
 EDEV int bm_prev(const Inst& I, int b, int64_t xx) {
-  if (xx < 0) return -1;
+  if (xx < 0 || I.bcnt[b] == 0) return -1;
   const int x = (int)(xx > I.pmax ? I.pmax : xx);
   const uint64_t* b1 = I.bm1 + (int64_t)b * I.bm_words;
   const uint64_t* b2 = I.bm2 + (int64_t)b * I.bm_l2;
@@ -896,6 +903,8 @@ EDEVNI void ingest(Inst& I) {
         cls = cls_of(I, b, p);
       }
       const unsigned grp = MATCH_ANY(cls);
+      const unsigned bgrp = MATCH_ANY(ok ? b : -1 - LANE);
+      if (ok && (bgrp & LANEMASK_LT) == 0) SMEM_ADD(&I.bcnt[b], (int32_t)POPC(bgrp));
       int32_t old_tail = -1;
       if (ok) old_tail = I.cls_tail[cls];
       WSYNC();
@@ -934,6 +943,7 @@ EDEV int32_t cls_take(Inst& I, int b, int p, int32_t k, int32_t* out, int32_t no
     }
     I.cls_head[c] = h;
     I.cls_cnt[c] -= k;
+    I.bcnt[b] -= k;
     if (I.cls_cnt[c] == 0) {
       I.cls_tail[c] = -1;
       I.cls_head[c] = -1;
@@ -1166,6 +1176,7 @@ EDEV bool slot_fits(const Inst& I, int32_t host, int32_t abs, int32_t len) {
 
 EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
   // ---- select_gt_groups (queues.hpp:220-263) ----
+  const int64_t tp0 = PROF_NOW();
   int32_t nsel = 0, nselg = 0, whole = 0;
   if (I.free_total > 0) {
     Tok remaining = I.free_total;
@@ -1234,6 +1245,8 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     if (I.error) return;
   }
 
+  const int64_t tp1 = PROF_NOW();
+  LANE0(I.prof[7] += tp1 - tp0);
   // ---- KVC pipelining (econoserve-full, engine.hpp:273-297) ----
   if (I.full && nselg > 0) {
     int32_t nm = 0;  // host members flattened into tmp_b/tmp_c, group bounds in tmp_a
@@ -1284,6 +1297,8 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     }
   }
 
+  const int64_t tp2 = PROF_NOW();
+  LANE0(I.prof[8] += tp2 - tp1);
   // ---- PT batching (engine.hpp:299-324, queues.hpp:279-299) ----
   const Tok tfs_rem = I.tfs - (Tok)I.R;
   const Tok rfree = I.reserve_cap - I.reserved_used;
@@ -1351,6 +1366,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     }
   }
   dispatch_pts(I, npt);
+  LANE0(I.prof[9] += PROF_NOW() - tp2);
 }
 
 EDEVNI void vacate_slot(Inst& I, int32_t id, bool* rehomed) {  // engine.hpp:888-902
@@ -1445,15 +1461,8 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     wsum_pt += tk;
     if (I.prefill_done[id] >= I.prompt[id]) I.flags[id] |= F_PREFILL_FIN;
   }
-  for (int32_t i = LANE; i < I.R; i += W) {
-    const int32_t id = I.run[i];
-    I.exec_t[id] += dt;
-    const int32_t g = ++I.generated[id];
-    I.occupied[id]++;
-    I.written[id]++;
-    if (g == 1 && I.first_tok[id] < 0.0) I.first_tok[id] = I.clock;
-  }
   wsum_pt = wsum(wsum_pt);
+  // every running GT writes exactly one token this iteration
   LANE0(I.written_total += wsum_pt + I.R);
   EconoSample s;
   s.iter = I.iter;
@@ -1467,12 +1476,38 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   s.pt_admittable = I.pt_admittable;
   s._pad = 0;
   s.idle_repeat = 0;
-  // completions, in running order (engine.hpp:784-791)
-  int32_t completed_now = 0;
-  for (int32_t base = 0; base < I.R; base += W) {
+  // One pass over the running set (engine.hpp:763-771, 784-791, 812-817):
+  // decode progress, then completion and under-prediction tests on the new
+  // counts. All fields of a request load in parallel; completions are
+  // processed chunk by chunk in running order. Releasing a finished request
+  // touches only its own counters, regions and the slots it hosts, never
+  // another running request's progress, so it may precede the next chunk's
+  // decode. Under-prediction candidates (generated >= allowance < true_rl)
+  // are collected here in running order; completed requests never qualify.
+  int32_t completed_now = 0, npre = 0;
+  const int32_t R0 = I.R;
+  for (int32_t base = 0; base < R0; base += W) {
     const int32_t i = base + LANE;
-    const int32_t id = i < I.R ? I.run[i] : -1;
-    unsigned m = BALLOT(id >= 0 && I.generated[id] >= I.true_rl[id]);
+    const int32_t id = i < R0 ? I.run[i] : -1;
+    bool fin = false, under = false;
+    if (id >= 0) {
+      const double e = I.exec_t[id];
+      const int32_t g = I.generated[id] + 1;
+      const int32_t oc = I.occupied[id], wr = I.written[id], tr = I.true_rl[id], al = I.allowance[id];
+      const double ft = I.first_tok[id];
+      I.exec_t[id] = e + dt;
+      I.generated[id] = g;
+      I.occupied[id] = oc + 1;
+      I.written[id] = wr + 1;
+      if (g == 1 && ft < 0.0) I.first_tok[id] = I.clock;
+      fin = g >= tr;
+      under = g >= al && g < tr;
+    }
+    const unsigned mu = BALLOT(under);
+    if (under) I.tmp_a[npre + POPC(mu & LANEMASK_LT)] = id;
+    npre += POPC(mu);
+    unsigned m = BALLOT(fin);
+    WSYNC();
     while (m) {
       const int l = FFS(m);
       m &= m - 1;
@@ -1499,17 +1534,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     WSYNC();
     if (I.error) return;
   }
-  // under-prediction (engine.hpp:812-817): candidates fixed up front, handled in order
-  int32_t npre = 0;
-  for (int32_t base = 0; base < I.R; base += W) {
-    const int32_t i = base + LANE;
-    const int32_t id = i < I.R ? I.run[i] : -1;
-    const bool c = id >= 0 && I.generated[id] >= I.allowance[id] && I.generated[id] < I.true_rl[id];
-    const unsigned m = BALLOT(c);
-    if (c) I.tmp_a[npre + POPC(m & LANEMASK_LT)] = id;
-    npre += POPC(m);
-  }
-  WSYNC();
+  // under-prediction (engine.hpp:812-817): candidates fixed up front (above), handled in order
   for (int32_t k = 0; k < npre; ++k) {
     const int32_t id = I.tmp_a[k];
     if (I.state[id] != ST_RUNNING) continue;
@@ -1681,6 +1706,80 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
   return k > 0 ? k : 0;
 }
 
+// Progress of one running request over a replayed span (execute_iteration's
+// decode branch, engine.hpp:744-771, k times; exec_t by sequential adds).
+EDEV void quiet_request(Inst& I, int32_t id, double e, int64_t k, double clk1) {
+  I.exec_t[id] = e;
+  if (I.generated[id] == 0 && I.first_tok[id] < 0.0) I.first_tok[id] = clk1;
+  I.generated[id] += (int32_t)k;
+  I.occupied[id] += (int32_t)k;
+  I.written[id] += (int32_t)k;
+}
+
+// The replay without per-iteration samples (the bench path): every chain the
+// reference advances once per iteration — clock, the in-order sample sums of
+// metrics.hpp:153-162, and each running request's execution_time — advances
+// in ONE loop, so the k-step span costs ~k dependent DADDs instead of one
+// pass per chain. The per-iteration written fractions are computed W at a
+// time across lanes and broadcast (shuffles are off the dependency chain).
+EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double clk1, double af,
+                                 int64_t wt0, double cap) {
+  const bool has_arr = I.arrival_cursor < I.n;
+  const double ta = has_arr ? I.arrival[I.arrival_cursor] : 0.0;
+  const int32_t R = I.R;
+  const int32_t my = LANE < R ? I.run[LANE] : -1;
+  double e = my >= 0 ? I.exec_t[my] : 0.0;
+  double clock = I.clock, aw = I.agg_written, aa = I.agg_allocated;
+  int64_t j = 0;
+  if (!has_arr) {
+    for (int64_t base = 0; base < k; base += W) {
+      const int64_t jj = base + LANE;
+      const double wf = jj < k ? (double)(wt0 + (jj + 1) * fs) / cap : 0.0;
+      const int lim = k - base < W ? (int)(k - base) : W;
+      if (lim == W) {
+#pragma unroll
+        for (int l = 0; l < W; ++l) {
+          const double w = shfl(wf, l);
+          clock += dt; aw += w; aa += af; e += dt;
+        }
+      } else {
+        for (int l = 0; l < lim; ++l) {
+          const double w = shfl(wf, l);
+          clock += dt; aw += w; aa += af; e += dt;
+        }
+      }
+    }
+    j = k;
+  } else {  // the arrival cut-off is re-checked before every replayed step
+    bool stop = false;
+    for (int64_t base = 0; base < k && !stop; base += W) {
+      const int64_t jj = base + LANE;
+      const double wf = jj < k ? (double)(wt0 + (jj + 1) * fs) / cap : 0.0;
+      const int lim = k - base < W ? (int)(k - base) : W;
+      for (int l = 0; l < lim; ++l) {
+        const double w = shfl(wf, l);
+        if (j > 0 && ta <= clock + 1e-12) { stop = true; break; }
+        clock += dt; aw += w; aa += af; e += dt;
+        ++j;
+      }
+    }
+  }
+  k = j;
+  if (my >= 0) quiet_request(I, my, e, k, clk1);
+  for (int32_t i = W + LANE; i < R; i += W) {
+    const int32_t id = I.run[i];
+    double e2 = I.exec_t[id];
+    for (int64_t t = 0; t < k; ++t) e2 += dt;
+    quiet_request(I, id, e2, k, clk1);
+  }
+  WSYNC();
+  LANE0(I.clock = clock; I.written_total = wt0 + k * fs; I.agg_written = aw; I.agg_allocated = aa;
+        I.iter += k; I.steps += k; I.executed += k; I.agg_fs += fs * k;
+        if ((double)fs >= 0.95 * (double)I.tfs) I.agg_tfs_hits += k;
+        I.hist[0] += k; I.quiet_steps += k; I.quiet_spans++);
+  return k;
+}
+
 EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
   const Tok fs = I.R;
   const double dt = iteration_time(I, fs) + 0.0;
@@ -1688,6 +1787,7 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
   const double af = (double)((I.general_cap - I.free_total) + I.reserved_used) / (double)I.capacity;
   const int64_t wt0 = I.written_total;
   const double cap = (double)I.capacity;
+  if (!I.record_samples) return quiet_steps_fused(I, k, fs, dt, clk1, af, wt0, cap);
   // pass 1 (every lane, identical arithmetic): the sequential clock chain and
   // the arrival cut-off — ingest would admit an arrival at the next step.
   double clock = I.clock;
@@ -1757,13 +1857,17 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
 }
 
 EDEVNI void engine_step(Inst& I) {  // Engine::step (engine.hpp:104-116)
+  const int64_t t0 = PROF_NOW();
   ingest(I);
+  LANE0(I.prof[6] += PROF_NOW() - t0);
   form_econoserve(I);
   if (I.error) return;
+  const int64_t t1 = PROF_NOW();
   Tok fs = 0;
   for (int32_t i = LANE; i < I.n_ptiter; i += W) fs += I.ptiter_tok[i];
   fs = wsum(fs) + I.R;
   if (fs == 0) handle_idle(I); else execute_iteration(I, fs);
+  LANE0(I.prof[10] += PROF_NOW() - t1);
   LANE0(I.steps++);
 }
 

@@ -175,12 +175,11 @@ EDEV void engine_record(const Inst& I, int32_t i, EconoRecord& rc) {
 // [15]=executed iters [16]=sum fs [17]=sum written frac [18]=sum allocated
 // frac [19]=tfs hits [20]=pt iters [21]=hosted slots [22]=hosted overruns
 // [23]=completed [24]=pt dispatched [25]=gt scheduled [26]=steps [27]=iter.
-EDEV void engine_partials(const Inst& I, double* out) {
-  double acc[15];
-  for (int k = 0; k < 15; ++k) acc[k] = 0.0;
-  for (int32_t i = LANE; i < I.n; i += W) {
+// acc[0..14] over requests lo, lo+stride, ... < I.n (one thread's share).
+EDEV void partials_accumulate(const Inst& I, int64_t lo, int64_t stride, double* acc) {
+  for (int64_t i = lo; i < I.n; i += stride) {
     EconoRecord rc;
-    engine_record(I, i, rc);
+    engine_record(I, (int32_t)i, rc);
     const double jct = rc.completion_time - rc.arrival;
     acc[0] += 1.0;
     acc[1] += jct;
@@ -200,32 +199,41 @@ EDEV void engine_partials(const Inst& I, double* out) {
     acc[13] += rc.preemption_time;
     acc[14] += rc.scheduling_time_share;
   }
-  for (int k = 0; k < 15; ++k) {
-    if (k == 10) {
-      double v = acc[k];
-      for (int o = W / 2; o > 0; o >>= 1) { const double x = shfl_xor(v, o); v = x > v ? x : v; }
-      acc[k] = v;
-    } else {
-      acc[k] = wsum(acc[k]);
-    }
-  }
-  if (LANE == 0) {
-    for (int k = 0; k < 15; ++k) out[k] = acc[k];
-    out[15] = (double)I.executed;
-    out[16] = (double)I.agg_fs;
-    out[17] = I.agg_written;
-    out[18] = I.agg_allocated;
-    out[19] = (double)I.agg_tfs_hits;
-    out[20] = (double)I.agg_pt_iters;
-    out[21] = (double)I.hosted_total;
-    out[22] = (double)I.hosted_overruns;
-    out[23] = (double)I.completed;
-    out[24] = (double)I.pt_dispatched;
-    out[25] = (double)I.gt_scheduled;
-    out[26] = (double)I.steps;
-    out[27] = (double)I.iter;
-    for (int k = 28; k < ECONO_PARTIAL_WORDS; ++k) out[k] = 0.0;
-  }
+}
+EDEV void partials_combine(double* acc, const double* x) {
+  for (int k = 0; k < 15; ++k) acc[k] = k == 10 ? (x[k] > acc[k] ? x[k] : acc[k]) : acc[k] + x[k];
+}
+// The per-request sums plus the instance's running aggregates.
+EDEV void partials_finish(const Inst& I, const double* acc, double* out) {
+  for (int k = 0; k < 15; ++k) out[k] = acc[k];
+  out[15] = (double)I.executed;
+  out[16] = (double)I.agg_fs;
+  out[17] = I.agg_written;
+  out[18] = I.agg_allocated;
+  out[19] = (double)I.agg_tfs_hits;
+  out[20] = (double)I.agg_pt_iters;
+  out[21] = (double)I.hosted_total;
+  out[22] = (double)I.hosted_overruns;
+  out[23] = (double)I.completed;
+  out[24] = (double)I.pt_dispatched;
+  out[25] = (double)I.gt_scheduled;
+  out[26] = (double)I.steps;
+  out[27] = (double)I.iter;
+  for (int k = 28; k < ECONO_PARTIAL_WORDS; ++k) out[k] = 0.0;
+}
+// Per-instance metric partial sums (metrics.hpp:110-173) for the cross-GPU
+// reduction: [0]=n [1]=sum jct [2]=sum tbt [3]=tbt_n [4]=sum jct/true_rl
+// [5]=met [6]=tokens [7]=preemptions [8]=reserve_draws [9]=alloc failures
+// [10]=max completion [11..14]=sum waiting/execution/preemption/scheduling
+// [15]=executed iters [16]=sum fs [17]=sum written frac [18]=sum allocated
+// frac [19]=tfs hits [20]=pt iters [21]=hosted slots [22]=hosted overruns
+// [23]=completed [24]=pt dispatched [25]=gt scheduled [26]=steps [27]=iter.
+// Host build (tests): one pass in id order.
+EDEV void engine_partials(const Inst& I, double* out) {
+  double acc[15];
+  for (int k = 0; k < 15; ++k) acc[k] = 0.0;
+  partials_accumulate(I, 0, 1, acc);
+  partials_finish(I, acc, out);
 }
 
 }  // namespace econo
@@ -248,10 +256,11 @@ __device__ __forceinline__ void inst_store(Inst* g, const Inst& s) {
 // Per-instance init scratch: [0] first out-of-order arrival, [1] prompt sum,
 // [2] first infeasible request.
 __global__ void __launch_bounds__(256) k_init_soa(Inst* insts, const EconoTraceRecord* const* traces,
-                                                  unsigned long long* scr) {
-  Inst& I = insts[blockIdx.y];
-  const EconoTraceRecord* tr = traces[blockIdx.y];
-  unsigned long long* sc = scr + 4 * blockIdx.y;
+                                                  unsigned long long* scr, int32_t inst0) {
+  const int32_t ii = inst0 + (int32_t)blockIdx.y;
+  Inst& I = insts[ii];
+  const EconoTraceRecord* tr = traces[ii];
+  unsigned long long* sc = scr + 4 * ii;
   int64_t psum = 0;
   long long bad = LLONG_MAX;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I.n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -315,8 +324,10 @@ __global__ void __launch_bounds__(32) k_init_finish(Inst* insts, const unsigned 
 
 __global__ void __launch_bounds__(32) k_engine_steps(Inst* insts, int64_t max_steps) {
   __shared__ Inst I;
+  const int64_t t0 = PROF_NOW();
   inst_load(I, &insts[blockIdx.x]);
   engine_steps(I, max_steps);
+  LANE0(I.prof[11] += PROF_NOW() - t0; I.prof[12]++);
   inst_store(&insts[blockIdx.x], I);
 }
 
@@ -346,8 +357,44 @@ __global__ void k_engine_records(const Inst* inst, EconoRecord* out) {
   }
 }
 
-__global__ void __launch_bounds__(32) k_engine_partials(const Inst* insts, double* out) {
-  engine_partials(insts[blockIdx.x], out + (size_t)blockIdx.x * ECONO_PARTIAL_WORDS);
+// Partial sums, grid-wide: block (x, instance) reduces a strided slice of
+// the instance's requests (one pass over ~89 B of SoA per request, HBM-bound)
+// into scr[instance][x][16]; k_partials_finish then folds the slices in a
+// fixed order, so results are deterministic run to run.
+__global__ void __launch_bounds__(256) k_partials_slices(const Inst* insts, double* scr) {
+  const Inst& I = insts[blockIdx.y];
+  double acc[15];
+  for (int k = 0; k < 15; ++k) acc[k] = 0.0;
+  partials_accumulate(I, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, acc);
+  for (int k = 0; k < 15; ++k) {
+    double v = acc[k];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, v, o);
+      v = k == 10 ? (x > v ? x : v) : v + x;
+    }
+    acc[k] = v;
+  }
+  __shared__ double ws[8][16];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < 15; ++k) ws[w][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot[15];
+    for (int k = 0; k < 15; ++k) tot[k] = ws[0][k];
+    for (int j = 1; j < (int)(blockDim.x >> 5); ++j) partials_combine(tot, ws[j]);
+    double* o = scr + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16;
+    for (int k = 0; k < 15; ++k) o[k] = tot[k];
+  }
+}
+__global__ void __launch_bounds__(32) k_partials_finish(const Inst* insts, const double* scr, int32_t slices,
+                                                        double* out) {
+  if (threadIdx.x != 0) return;
+  const double* s0 = scr + (size_t)blockIdx.x * slices * 16;
+  double acc[15];
+  for (int k = 0; k < 15; ++k) acc[k] = s0[k];
+  for (int j = 1; j < slices; ++j) partials_combine(acc, s0 + (size_t)j * 16);
+  partials_finish(insts[blockIdx.x], acc, out + (size_t)blockIdx.x * ECONO_PARTIAL_WORDS);
 }
 #endif
 
@@ -604,7 +651,11 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   }
   const int64_t cap = I.capacity;
   I.reg_cap = (int32_t)(I.general_cap + 2);
-  I.grp_cap = (int32_t)(n + 1);
+  // Every waiting GT holds KVC (its prompt in the reserve after prefill,
+  // engine.hpp:794-809 / SURVEY A.7, or its regions after an offload-free
+  // preemption, engine.hpp:904-928), and every queued group is non-empty, so
+  // at most `capacity` groups exist at once; freed groups are recycled.
+  I.grp_cap = (int32_t)(imin(n, cap) + 1);
   I.slot_cap = (int32_t)(imin(n, cap) + 1);
   I.run_cap = (int32_t)(imin(n, cap) + 1);
   I.ptiter_cap = (int32_t)(imin(n, I.tfs) + 2);
@@ -688,6 +739,10 @@ struct econo_batch {
   Inst* d_insts = nullptr;
 #ifndef ECONO_HOSTSIM
   cudaStream_t stream = nullptr;
+  // independent launch chains (econo_batch_launch_lanes): one stream per lane
+  std::vector<cudaStream_t> lanes;
+  std::vector<cudaEvent_t> lane_done;
+  cudaEvent_t fork = nullptr;
 #endif
   std::vector<econo_engine*> views;
 };
@@ -777,6 +832,41 @@ void launch_steps(econo_batch* b, int64_t max_steps, void* stream) {
 #endif
 }
 
+// n_launches x (every instance by max_steps), as `n_lanes` independent chains
+// over contiguous instance ranges, forked from and joined back into `stream`.
+int launch_lanes(econo_batch* b, int64_t max_steps, int32_t n_launches, int32_t n_lanes, void* stream) {
+  const int32_t n = (int32_t)b->inst.size();
+  if (n_launches < 0 || n_lanes < 1) return ECONO_ECONFIG;
+  if (n_lanes > n) n_lanes = n;
+  if (n_lanes > 32) n_lanes = 32;  // hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS <= 32)
+#ifdef ECONO_HOSTSIM
+  (void)stream;
+  for (int32_t k = 0; k < n_launches; ++k) launch_steps(b, max_steps, nullptr);
+  return ECONO_OK;
+#else
+  cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
+  if (!b->fork && cudaEventCreateWithFlags(&b->fork, cudaEventDisableTiming) != cudaSuccess) return ECONO_ECUDA;
+  while ((int32_t)b->lanes.size() < n_lanes) {
+    cudaStream_t ls;
+    cudaEvent_t ev;
+    if (cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking) != cudaSuccess) return ECONO_ECUDA;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return ECONO_ECUDA;
+    b->lanes.push_back(ls);
+    b->lane_done.push_back(ev);
+  }
+  cudaEventRecord(b->fork, s);
+  for (int32_t l = 0; l < n_lanes; ++l) {
+    const int32_t lo = (int32_t)((int64_t)n * l / n_lanes), hi = (int32_t)((int64_t)n * (l + 1) / n_lanes);
+    cudaStreamWaitEvent(b->lanes[l], b->fork, 0);
+    for (int32_t k = 0; k < n_launches; ++k)
+      k_engine_steps<<<(unsigned)(hi - lo), 32, 0, b->lanes[l]>>>(b->d_insts + lo, max_steps);
+    cudaEventRecord(b->lane_done[l], b->lanes[l]);
+    cudaStreamWaitEvent(s, b->lane_done[l], 0);
+  }
+  return cudaGetLastError() == cudaSuccess ? ECONO_OK : ECONO_ECUDA;
+#endif
+}
+
 int sync_batch(econo_batch* b, char* err, size_t errlen) {
 #ifndef ECONO_HOSTSIM
   if (cudaStreamSynchronize(b->stream) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
@@ -841,6 +931,9 @@ void econo_batch_destroy(econo_batch* b) {
   dev_free(b->d_insts);
   for (auto* v : b->views) delete v;
 #ifndef ECONO_HOSTSIM
+  for (auto ls : b->lanes) cudaStreamDestroy(ls);
+  for (auto ev : b->lane_done) cudaEventDestroy(ev);
+  if (b->fork) cudaEventDestroy(b->fork);
   if (b->stream) cudaStreamDestroy(b->stream);
 #endif
   delete b;
@@ -983,28 +1076,41 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto ms = [](auto a, auto b2) { return std::chrono::duration<double, std::milli>(b2 - a).count(); };
     const auto t0 = now();
-    size_t total = 0;
-    std::vector<size_t> off((size_t)n_inst);
+    // Traces are staged through two bounded device buffers (double-buffered:
+    // the copy of one group of instances overlaps the AoS->SoA conversion of
+    // the previous group), so staging never costs more than 2 x chunk bytes
+    // of HBM however many instances the batch holds. Pinned host buffers copy
+    // at full link speed; pageable ones go through the driver's bounce buffer.
+    size_t largest = 0, total = 0;
     for (int32_t i = 0; i < n_inst; ++i) {
-      off[(size_t)i] = total;
+      largest = std::max(largest, sizeof(EconoTraceRecord) * (size_t)ns[i]);
       total += sizeof(EconoTraceRecord) * (size_t)ns[i];
     }
-    void* dtr = nullptr;
-    if (dev_alloc(&dtr, total)) {
-      econo_batch_destroy(b);
-      return set_err(err, errlen, "device trace allocation failed"), ECONO_ECUDA;
+    const size_t chunk = std::min(total, std::max(largest, (size_t)256 << 20));
+    const int nbuf = total > chunk ? 2 : 1;
+    void* stage[2] = {nullptr, nullptr};
+    for (int k = 0; k < nbuf; ++k)
+      if (dev_alloc(&stage[k], chunk)) {
+        for (int j = 0; j < k; ++j) dev_free(stage[j]);
+        econo_batch_destroy(b);
+        return set_err(err, errlen, "device trace staging allocation failed"), ECONO_ECUDA;
+      }
+    // instance groups [g0, g1) that fit one chunk
+    std::vector<std::pair<int32_t, int32_t>> groups;
+    for (int32_t i = 0; i < n_inst;) {
+      int32_t j = i;
+      size_t used = 0;
+      while (j < n_inst && used + sizeof(EconoTraceRecord) * (size_t)ns[j] <= chunk) used += sizeof(EconoTraceRecord) * (size_t)ns[j++];
+      groups.emplace_back(i, j);
+      i = j;
     }
-    std::vector<bool> pinned((size_t)n_inst, false);
-    for (int32_t i = 0; i < n_inst; ++i) {
-      const size_t bytes = sizeof(EconoTraceRecord) * (size_t)ns[i];
-      pinned[(size_t)i] = false;  // registering costs as much as the pageable copy (tools/probe_upload.py)
-      cudaMemcpyAsync((char*)dtr + off[(size_t)i], traces[i], bytes, cudaMemcpyHostToDevice, b->stream);
-      d_traces[(size_t)i] = (const EconoTraceRecord*)((char*)dtr + off[(size_t)i]);
+    for (size_t g = 0; g < groups.size(); ++g) {
+      size_t o = 0;
+      for (int32_t i = groups[g].first; i < groups[g].second; ++i) {
+        d_traces[(size_t)i] = (const EconoTraceRecord*)((char*)stage[g % nbuf] + o);
+        o += sizeof(EconoTraceRecord) * (size_t)ns[i];
+      }
     }
-    cudaStreamSynchronize(b->stream);
-    for (int32_t i = 0; i < n_inst; ++i)
-      if (pinned[(size_t)i]) cudaHostUnregister(const_cast<EconoTraceRecord*>(traces[i]));
-    const auto t1 = now();
     void *dt, *ds, *dsc;
     dev_alloc(&dt, sizeof(void*) * (size_t)n_inst);
     dev_alloc(&ds, sizeof(uint64_t) * 2 * (size_t)n_inst);
@@ -1019,10 +1125,36 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
       nmax = imax(nmax, h.desc.n);
       emax = imax(emax, h.desc.n + h.desc.general_cap + (int64_t)h.desc.nbuckets * (h.desc.pmax + 1) + 64);
     }
-    const unsigned gx = (unsigned)imin(imax(1, (nmax + 255) / 256), 1184 / imax(1, n_inst / 8 + 1) + 1);
+    cudaStream_t cs;
+    cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    cudaEvent_t copied[2], converted[2];
+    for (int k = 0; k < 2; ++k) {
+      cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&converted[k], cudaEventDisableTiming);
+    }
+    for (size_t g = 0; g < groups.size(); ++g) {
+      const int k = (int)(g % nbuf);
+      if (g >= (size_t)nbuf) cudaStreamWaitEvent(cs, converted[k], 0);  // buffer k free again
+      for (int32_t i = groups[g].first; i < groups[g].second; ++i)
+        cudaMemcpyAsync(const_cast<EconoTraceRecord*>(d_traces[(size_t)i]), traces[i],
+                        sizeof(EconoTraceRecord) * (size_t)ns[i], cudaMemcpyHostToDevice, cs);
+      cudaEventRecord(copied[k], cs);
+      cudaStreamWaitEvent(b->stream, copied[k], 0);
+      const int32_t cnt = groups[g].second - groups[g].first;
+      const unsigned gx = (unsigned)imin(imax(1, (nmax + 255) / 256), 1184 / imax(1, cnt / 8 + 1) + 1);
+      k_init_soa<<<dim3(gx, (unsigned)cnt), 256, 0, b->stream>>>(b->d_insts, (const EconoTraceRecord* const*)dt,
+                                                                 (unsigned long long*)dsc, groups[g].first);
+      cudaEventRecord(converted[k], b->stream);
+    }
+    cudaStreamSynchronize(b->stream);
+    const auto t1 = now();
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(copied[k]);
+      cudaEventDestroy(converted[k]);
+    }
+    cudaStreamDestroy(cs);
+    for (int k = 0; k < nbuf; ++k) dev_free(stage[k]);
     const unsigned gx2 = (unsigned)imin(imax(1, (emax + 255) / 256), 1184 / imax(1, n_inst / 8 + 1) + 1);
-    k_init_soa<<<dim3(gx, (unsigned)n_inst), 256, 0, b->stream>>>(b->d_insts, (const EconoTraceRecord* const*)dt,
-                                                                  (unsigned long long*)dsc);
     k_init_scalar<<<(unsigned)n_inst, 32, 0, b->stream>>>(b->d_insts, (const uint64_t*)ds,
                                                           (const unsigned long long*)dsc);
     k_init_req<<<dim3(gx2, (unsigned)n_inst), 256, 0, b->stream>>>(b->d_insts, (unsigned long long*)dsc);
@@ -1030,12 +1162,11 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     const int rc = sync_batch(b, err, errlen);
     const auto t2 = now();
     if (verbose)
-      fprintf(stderr, "[econo] create: trace upload %.1f ms (%zu MB), init kernels %.1f ms\n", ms(t0, t1),
+      fprintf(stderr, "[econo] create: trace upload + SoA conversion %.1f ms (%zu MB), init kernels %.1f ms\n", ms(t0, t1),
               total >> 20, ms(t1, t2));
     dev_free(dt);
     dev_free(ds);
     dev_free(dsc);
-    dev_free(dtr);
     if (rc) { econo_batch_destroy(b); return rc; }
   }
 #endif
@@ -1056,6 +1187,11 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
 int econo_batch_launch(econo_batch* b, int64_t max_steps, void* stream) {
   launch_steps(b, max_steps, stream);
   return ECONO_OK;
+}
+
+int econo_batch_launch_lanes(econo_batch* b, int64_t max_steps, int32_t n_launches, int32_t n_lanes,
+                             void* stream) {
+  return launch_lanes(b, max_steps, n_launches, n_lanes, stream);
 }
 
 int econo_batch_sync(econo_batch* b, char* err, size_t errlen) {
@@ -1107,20 +1243,31 @@ int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen) 
   (void)bytes; (void)err; (void)errlen;
   return ECONO_OK;
 #else
-  void* d;
+  const int32_t ni = (int32_t)b->inst.size();
+  int64_t nmax = 1;
+  for (auto& h : b->inst) nmax = imax(nmax, h.desc.n);
+  // enough blocks to fill the machine a few times over, no more than the work
+  const int32_t slices = (int32_t)imax(1, imin((nmax + 255) / 256, (148 * 8 + ni - 1) / ni));
+  void *d, *scr;
   if (dev_alloc(&d, bytes)) return set_err(err, errlen, "device allocation failed"), ECONO_ECUDA;
-  k_engine_partials<<<(unsigned)b->inst.size(), 32, 0, b->stream>>>(b->d_insts, (double*)d);
+  if (dev_alloc(&scr, sizeof(double) * 16 * (size_t)slices * (size_t)ni)) {
+    dev_free(d);
+    return set_err(err, errlen, "device allocation failed"), ECONO_ECUDA;
+  }
+  k_partials_slices<<<dim3((unsigned)slices, (unsigned)ni), 256, 0, b->stream>>>(b->d_insts, (double*)scr);
+  k_partials_finish<<<(unsigned)ni, 32, 0, b->stream>>>(b->d_insts, (const double*)scr, slices, (double*)d);
   int rc = sync_batch(b, err, errlen);
   if (!rc && dev_d2h(out, d, bytes)) rc = ECONO_ECUDA;
+  dev_free(scr);
   dev_free(d);
   return rc;
 #endif
 }
 
-// Development counters: per instance 8 int64 (engine.cuh Inst::prof).
+// Development counters: per instance ECONO_DEBUG_WORDS int64 (engine.cuh Inst::prof).
 int econo_batch_debug(econo_batch* b, int64_t* out) {
   for (size_t i = 0; i < b->inst.size(); ++i)
-    for (int k = 0; k < 8; ++k) out[8 * i + k] = b->inst[i].desc.prof[k];
+    for (int k = 0; k < ECONO_DEBUG_WORDS; ++k) out[ECONO_DEBUG_WORDS * i + k] = b->inst[i].desc.prof[k];
   return ECONO_OK;
 }
 

@@ -22,7 +22,8 @@ LIB_PATH = os.path.join(HERE, "_lib", "libeconoserve_b200.so")
 SYMBOLS = [
     "econo_default_options", "econo_create", "econo_step", "econo_run", "econo_records",
     "econo_report", "econo_events", "econo_samples", "econo_scalars", "econo_snapshot",
-    "econo_destroy", "econo_batch_create", "econo_batch_launch", "econo_batch_sync",
+    "econo_destroy", "econo_batch_create", "econo_batch_launch", "econo_batch_launch_lanes",
+    "econo_batch_sync",
     "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
     "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore", "econo_batch_debug",
 ]
@@ -78,6 +79,7 @@ def load(path=None):
     L.econo_batch_create.argtypes = [C.POINTER(vp), C.POINTER(i64), i32, C.POINTER(abi.Options),
                                      C.c_int, C.POINTER(vp), cp, sz]
     L.econo_batch_launch.argtypes = [vp, i64, vp]
+    L.econo_batch_launch_lanes.argtypes = [vp, i64, i32, i32, vp]
     L.econo_batch_sync.argtypes = [vp, cp, sz]
     L.econo_batch_scalars.argtypes = [vp, C.POINTER(abi.Scalars)]
     L.econo_batch_engine.argtypes = [vp, i32, C.POINTER(vp)]
@@ -92,10 +94,15 @@ def load(path=None):
     return L
 
 
-def generate_trace(n, rate, prompt, rl, seed, lib=None):
-    """generate_synthetic (workload.hpp:104-125): host-side input preparation."""
+def generate_trace(n, rate, prompt, rl, seed, lib=None, out=None):
+    """generate_synthetic (workload.hpp:104-125): host-side input preparation.
+    `out` (optional): a preallocated TRACE_DTYPE array of n records, e.g. a view
+    of pinned host memory so the upload runs at full link speed."""
     L = load(lib)
-    out = np.zeros(n, dtype=abi.TRACE_DTYPE)
+    if out is None:
+        out = np.zeros(n, dtype=abi.TRACE_DTYPE)
+    elif out.dtype != abi.TRACE_DTYPE or len(out) != n or not out.flags.c_contiguous:
+        raise ValueError("out must be a contiguous TRACE_DTYPE array of n records")
     err = C.create_string_buffer(512)
     rc = L.econo_generate_trace(n, rate, C.byref(abi.LengthDist(*prompt)),
                                 C.byref(abi.LengthDist(*rl)), seed, out.ctypes.data, err, 512)
@@ -238,6 +245,12 @@ class Batch:
     def launch(self, max_steps, stream=None):
         self._L.econo_batch_launch(self.h, max_steps, stream)
 
+    def launch_lanes(self, max_steps, n_launches, n_lanes=32, stream=None):
+        """n_launches passes of `max_steps` as independent per-lane launch chains."""
+        rc = self._L.econo_batch_launch_lanes(self.h, max_steps, n_launches, n_lanes, stream)
+        if rc:
+            raise DeviceError(f"econo_batch_launch_lanes failed ({rc})")
+
     def sync(self):
         err = C.create_string_buffer(1024)
         rc = self._L.econo_batch_sync(self.h, err, 1024)
@@ -262,7 +275,7 @@ class Batch:
             _raise(rc, err)
 
     def debug(self):
-        out = np.zeros((self.n, 8), dtype=np.int64)
+        out = np.zeros((self.n, abi.DEBUG_WORDS), dtype=np.int64)
         self._L.econo_batch_debug(self.h, out.ctypes.data)
         return out
 

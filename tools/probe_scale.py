@@ -2,6 +2,8 @@
 per-phase device cycle counters (development tool; run under gpurun)."""
 import argparse
 import os
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 import time
 
@@ -17,7 +19,7 @@ NAMES = ["test", "replay", "normal", "-", "spans", "nsteps", "ingest", "gtsel", 
          "launch", "launches"]
 
 
-def run(traces, iters, launches, warm=3):
+def run(traces, iters, launches, warm=3, lanes=0):
     t0 = time.time()
     b = Batch(traces, bench.options(), device=0)
     s = torch.cuda.Stream()
@@ -31,8 +33,11 @@ def run(traces, iters, launches, warm=3):
     sc0, d0 = b.scalars(), b.debug().copy()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
-    for _ in range(launches):
-        b.launch(iters, s.cuda_stream)
+    if lanes:
+        b.launch_lanes(iters, launches, lanes, s.cuda_stream)
+    else:
+        for _ in range(launches):
+            b.launch(iters, s.cuda_stream)
     e1.record(s)
     e1.synchronize()
     ms = e0.elapsed_time(e1)
@@ -42,7 +47,7 @@ def run(traces, iters, launches, warm=3):
     I = len(traces)
     tot = d.sum(axis=0)
     per = {NAMES[k]: int(tot[k]) // I for k in range(len(NAMES)) if NAMES[k] != "-"}
-    print(f"inst={I} iters={iters} launches={launches}: {ms:.3f} ms total, {1e3 * ms / launches:.1f} us/launch, "
+    print(f"inst={I} iters={iters} launches={launches} lanes={lanes}: {ms:.3f} ms total, {1e3 * ms / launches:.1f} us/launch, "
           f"{1e3 * ms / (launches * iters):.3f} us/iter, adm={adm} -> {adm / ms * 1e3:.0f} req/s, "
           f"create+ingest {t_create:.2f}s, launch cycles max {int(d[:, 11].max())}", flush=True)
     print("   per-instance cycles:", per, flush=True)
@@ -54,6 +59,7 @@ def main():
     ap.add_argument("--counts", default="148,296,444,592,740")
     ap.add_argument("--iters", default="100,1000")
     ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--lanes", default="0")
     a = ap.parse_args()
     counts = [int(x) for x in a.counts.split(",")]
     t0 = time.time()
@@ -61,7 +67,8 @@ def main():
     print(f"tracegen {time.time() - t0:.1f}s", flush=True)
     for c in counts:
         for it in [int(x) for x in a.iters.split(",")]:
-            run(traces[:c], it, max(1, 1000 // it) * 10 if it < 1000 else 10)
+            for ln in [int(x) for x in a.lanes.split(",")]:
+                run(traces[:c], it, max(1, 1000 // it) * 10 if it < 1000 else 10, lanes=ln)
 
 
 if __name__ == "__main__":
