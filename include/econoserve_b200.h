@@ -258,15 +258,6 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* n, 
  * max_steps steps on `stream` (a cudaStream_t, NULL = the handle's stream).
  * Asynchronous: no host synchronisation. */
 int econo_batch_launch(econo_batch* b, int64_t max_steps, void* stream);
-/* n_launches consecutive econo_batch_launch passes, issued as n_lanes (<= 32)
- * independent launch chains over contiguous instance ranges, each on its own
- * stream, forked from and joined back into `stream`. Instances never wait
- * for each other between passes, so one slow instance delays only its lane
- * (run_sweep's workers likewise never wait for each other, sweep.hpp:127-141).
- * Set CUDA_DEVICE_MAX_CONNECTIONS=32 before the CUDA context exists so the
- * lanes map to distinct hardware queues. Asynchronous. */
-int econo_batch_launch_lanes(econo_batch* b, int64_t max_steps, int32_t n_launches, int32_t n_lanes,
-                             void* stream);
 int econo_batch_sync(econo_batch* b, char* err, size_t errlen);
 int econo_batch_scalars(econo_batch* b, EconoScalars* out /* n_inst entries */);
 int econo_batch_engine(econo_batch* b, int32_t i, econo_engine** out); /* borrowed view */
@@ -274,6 +265,27 @@ int econo_batch_engine(econo_batch* b, int32_t i, econo_engine** out); /* borrow
  * (metrics.hpp:110-173) into `out` (ECONO_PARTIAL_WORDS doubles per instance). */
 #define ECONO_PARTIAL_WORDS 32
 int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen);
+/* aggregate() (metrics.hpp:96-175) for every instance, computed on the device:
+ * per-request sums from the partials (reordered: 1e-6 relative), p5/p95 JCT
+ * exact (radix select of the order statistics, then percentile()'s
+ * interpolation, metrics.hpp:81-89), counts and the completion histogram
+ * exact. trace_hash = 0 (econo_report computes it for one engine). */
+int econo_batch_reports(econo_batch* b, EconoReport* out /* n_inst entries */, char* err, size_t errlen);
+/* JCT order statistics. JCT keys are JCT doubles mapped to uint64 so that
+ * unsigned order == double order (econo_jct_key_to_double inverts it).
+ * econo_batch_jct_prepare materialises the keys of every instance (call it
+ * after the last launch); econo_batch_jct_hist is one MSB-first radix-select
+ * pass over ALL instances of the batch: for each of n_targets (<= 8) prefixes
+ * (the top consumed_bits of the key), hist[t][d] counts keys with that prefix
+ * whose next digit_bits (<= 11) bits equal d. Histograms from several
+ * devices add up, so a cross-GPU select all-reduces them (metrics.py).
+ * econo_batch_jct_percentiles: per-instance exact percentile() values for
+ * nq <= 4 quantiles (out: n_inst x nq). */
+int econo_batch_jct_prepare(econo_batch* b, char* err, size_t errlen);
+int econo_batch_jct_hist(econo_batch* b, int32_t n_targets, const uint64_t* prefixes, int32_t consumed_bits,
+                         int32_t digit_bits, uint64_t* hist, char* err, size_t errlen);
+int econo_batch_jct_percentiles(econo_batch* b, const double* q, int32_t nq, double* out, char* err, size_t errlen);
+double econo_jct_key_to_double(uint64_t key);
 /* Device-side checkpoint / restore of every instance's complete state
  * (arena + descriptor), e.g. to rerun one scheduling window. */
 int econo_batch_checkpoint(econo_batch* b, char* err, size_t errlen);

@@ -236,6 +236,32 @@ EDEV void engine_partials(const Inst& I, double* out) {
   partials_finish(I, acc, out);
 }
 
+// ---- JCT order statistics (aggregate()'s percentile, metrics.hpp:81-89) ----
+// JCT = completion_time - arrival with completion_time built exactly as
+// finalize() does (engine.hpp:970-971), mapped to a uint64 whose unsigned
+// order is the double order, so exact k-th smallest values come from an
+// MSB-first radix select (11-bit digits, 6 passes) instead of a sort.
+EDEV uint64_t jct_key(const Inst& I, int64_t i) {
+  const double extra = I.penalty[i] + I.sched_share[i];
+  const double ct = I.compl_clock[i] + extra;
+  const double j = ct - I.arrival[i];
+  uint64_t b;
+  memcpy(&b, &j, sizeof(b));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+EHD double key_double(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFULL) : ~k;
+  double d;
+  memcpy(&d, &b, sizeof(d));
+  return d;
+}
+EHD bool key_matches(uint64_t k, uint64_t prefix, int consumed) {
+  return consumed == 0 || (k >> (64 - consumed)) == prefix;
+}
+EHD uint32_t key_digit(uint64_t k, int consumed, int dbits) {
+  return (uint32_t)((k >> (64 - consumed - dbits)) & ((1ULL << dbits) - 1));
+}
+
 }  // namespace econo
 
 #ifndef ECONO_HOSTSIM
@@ -395,6 +421,42 @@ __global__ void __launch_bounds__(32) k_partials_finish(const Inst* insts, const
   for (int k = 0; k < 15; ++k) acc[k] = s0[k];
   for (int j = 1; j < slices; ++j) partials_combine(acc, s0 + (size_t)j * 16);
   partials_finish(insts[blockIdx.x], acc, out + (size_t)blockIdx.x * ECONO_PARTIAL_WORDS);
+}
+
+// Materialises every instance's JCT keys (one pass over 32 B of SoA per
+// request -> 8 B key): keys[off[inst] + i].
+__global__ void __launch_bounds__(256) k_jct_keys(const Inst* insts, const int64_t* off, uint64_t* keys) {
+  const Inst& I = insts[blockIdx.y];
+  uint64_t* out = keys + off[blockIdx.y];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I.n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = jct_key(I, i);
+}
+// One radix-select pass: for each of `nt` targets, a histogram of the next
+// `dbits` bits of the keys whose top `consumed` bits equal the target's
+// prefix. Per-instance mode (hist/prefixes indexed by instance) or global
+// mode (one histogram over every instance). Shared-memory counters, flushed
+// with one global atomic per non-empty bin.
+__global__ void __launch_bounds__(256) k_jct_hist(const Inst* insts, const int64_t* off, const uint64_t* keys,
+                                                  int32_t per_instance, int32_t nt, const uint64_t* prefixes,
+                                                  int32_t consumed, int32_t dbits, unsigned long long* hist) {
+  extern __shared__ uint32_t sh[];
+  const int bins = 1 << dbits;
+  for (int j = threadIdx.x; j < nt * bins; j += blockDim.x) sh[j] = 0;
+  __syncthreads();
+  const int64_t n = insts[blockIdx.y].n;
+  const uint64_t* kk = keys + off[blockIdx.y];
+  const uint64_t* pf = prefixes + (per_instance ? (size_t)blockIdx.y * nt : 0);
+  uint64_t p[8];
+  for (int t = 0; t < nt; ++t) p[t] = pf[t];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = kk[i];
+    for (int t = 0; t < nt; ++t)
+      if (key_matches(k, p[t], consumed)) atomicAdd(&sh[t * bins + key_digit(k, consumed, dbits)], 1u);
+  }
+  __syncthreads();
+  unsigned long long* h = hist + (per_instance ? (size_t)blockIdx.y * nt * bins : 0);
+  for (int j = threadIdx.x; j < nt * bins; j += blockDim.x)
+    if (sh[j]) atomicAdd(&h[j], (unsigned long long)sh[j]);
 }
 #endif
 
@@ -737,12 +799,13 @@ struct econo_batch {
   char* ckpt_block = nullptr;
   std::vector<HostInst> inst;
   Inst* d_insts = nullptr;
+  // JCT keys for the percentile radix select (econo_batch_jct_prepare)
+  uint64_t* d_keys = nullptr;
+  int64_t* d_koff = nullptr;
+  int64_t keys_total = 0;
+  std::vector<uint64_t> h_keys;  // host build
 #ifndef ECONO_HOSTSIM
   cudaStream_t stream = nullptr;
-  // independent launch chains (econo_batch_launch_lanes): one stream per lane
-  std::vector<cudaStream_t> lanes;
-  std::vector<cudaEvent_t> lane_done;
-  cudaEvent_t fork = nullptr;
 #endif
   std::vector<econo_engine*> views;
 };
@@ -832,41 +895,6 @@ void launch_steps(econo_batch* b, int64_t max_steps, void* stream) {
 #endif
 }
 
-// n_launches x (every instance by max_steps), as `n_lanes` independent chains
-// over contiguous instance ranges, forked from and joined back into `stream`.
-int launch_lanes(econo_batch* b, int64_t max_steps, int32_t n_launches, int32_t n_lanes, void* stream) {
-  const int32_t n = (int32_t)b->inst.size();
-  if (n_launches < 0 || n_lanes < 1) return ECONO_ECONFIG;
-  if (n_lanes > n) n_lanes = n;
-  if (n_lanes > 32) n_lanes = 32;  // hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS <= 32)
-#ifdef ECONO_HOSTSIM
-  (void)stream;
-  for (int32_t k = 0; k < n_launches; ++k) launch_steps(b, max_steps, nullptr);
-  return ECONO_OK;
-#else
-  cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
-  if (!b->fork && cudaEventCreateWithFlags(&b->fork, cudaEventDisableTiming) != cudaSuccess) return ECONO_ECUDA;
-  while ((int32_t)b->lanes.size() < n_lanes) {
-    cudaStream_t ls;
-    cudaEvent_t ev;
-    if (cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking) != cudaSuccess) return ECONO_ECUDA;
-    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return ECONO_ECUDA;
-    b->lanes.push_back(ls);
-    b->lane_done.push_back(ev);
-  }
-  cudaEventRecord(b->fork, s);
-  for (int32_t l = 0; l < n_lanes; ++l) {
-    const int32_t lo = (int32_t)((int64_t)n * l / n_lanes), hi = (int32_t)((int64_t)n * (l + 1) / n_lanes);
-    cudaStreamWaitEvent(b->lanes[l], b->fork, 0);
-    for (int32_t k = 0; k < n_launches; ++k)
-      k_engine_steps<<<(unsigned)(hi - lo), 32, 0, b->lanes[l]>>>(b->d_insts + lo, max_steps);
-    cudaEventRecord(b->lane_done[l], b->lanes[l]);
-    cudaStreamWaitEvent(s, b->lane_done[l], 0);
-  }
-  return cudaGetLastError() == cudaSuccess ? ECONO_OK : ECONO_ECUDA;
-#endif
-}
-
 int sync_batch(econo_batch* b, char* err, size_t errlen) {
 #ifndef ECONO_HOSTSIM
   if (cudaStreamSynchronize(b->stream) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
@@ -875,6 +903,160 @@ int sync_batch(econo_batch* b, char* err, size_t errlen) {
   }
 #endif
   if (pull_descs(b)) return set_err(err, errlen, "device copy failed"), ECONO_ECUDA;
+  return ECONO_OK;
+}
+
+// ---- JCT radix select (host driver; kernels k_jct_keys / k_jct_hist) ------
+const int kDigitBits[6] = {11, 11, 11, 11, 11, 9};
+
+int jct_prepare(econo_batch* b, char* err, size_t errlen) {
+  int rc = sync_batch(b, err, errlen);
+  if (rc) return rc;
+  const int32_t ni = (int32_t)b->inst.size();
+  std::vector<int64_t> off((size_t)ni + 1, 0);
+  for (int32_t i = 0; i < ni; ++i) off[(size_t)i + 1] = off[(size_t)i] + b->inst[(size_t)i].desc.n;
+  const int64_t total = off[(size_t)ni];
+#ifdef ECONO_HOSTSIM
+  b->h_keys.resize((size_t)total);
+  for (int32_t i = 0; i < ni; ++i)
+    for (int64_t k = 0; k < b->inst[(size_t)i].desc.n; ++k)
+      b->h_keys[(size_t)(off[(size_t)i] + k)] = jct_key(b->inst[(size_t)i].desc, k);
+#else
+  if (total != b->keys_total) {
+    dev_free(b->d_keys);
+    dev_free(b->d_koff);
+    b->d_keys = nullptr;
+    b->d_koff = nullptr;
+    void *pk, *po;
+    if (dev_alloc(&pk, sizeof(uint64_t) * (size_t)total)) return set_err(err, errlen, "key allocation failed"), ECONO_ECUDA;
+    if (dev_alloc(&po, sizeof(int64_t) * off.size())) {
+      dev_free(pk);
+      return set_err(err, errlen, "key allocation failed"), ECONO_ECUDA;
+    }
+    b->d_keys = (uint64_t*)pk;
+    b->d_koff = (int64_t*)po;
+    if (dev_h2d(b->d_koff, off.data(), sizeof(int64_t) * off.size())) return set_err(err, errlen, "copy failed"), ECONO_ECUDA;
+  }
+  int64_t nmax = 1;
+  for (auto& h : b->inst) nmax = imax(nmax, h.desc.n);
+  const unsigned gx = (unsigned)imax(1, imin((nmax + 255) / 256, (148 * 8 + ni - 1) / ni));
+  k_jct_keys<<<dim3(gx, (unsigned)ni), 256, 0, b->stream>>>(b->d_insts, b->d_koff, b->d_keys);
+  rc = sync_batch(b, err, errlen);
+  if (rc) return rc;
+#endif
+  b->keys_total = total;
+  return cuda_check(err, errlen, "k_jct_keys");
+}
+
+// One pass: hist[g][t][2^dbits] for groups g (instances, or one global group).
+int jct_hist(econo_batch* b, int per_instance, int nt, const uint64_t* prefixes, int consumed, int dbits,
+             uint64_t* hist, char* err, size_t errlen) {
+  const int32_t ni = (int32_t)b->inst.size();
+  const int groups = per_instance ? ni : 1;
+  const size_t bins = (size_t)1 << dbits;
+  if (nt < 1 || nt > 8 || dbits < 1 || dbits > 11 || consumed < 0 || consumed + dbits > 64)
+    return set_err(err, errlen, "jct_hist: bad arguments"), ECONO_ECONFIG;
+  if (b->keys_total <= 0) return set_err(err, errlen, "jct keys not prepared"), ECONO_ECONFIG;
+#ifdef ECONO_HOSTSIM
+  std::fill(hist, hist + (size_t)groups * nt * bins, 0);
+  int64_t o = 0;
+  for (int32_t i = 0; i < ni; ++i) {
+    const int64_t n = b->inst[(size_t)i].desc.n;
+    const int g = per_instance ? i : 0;
+    for (int64_t k = 0; k < n; ++k) {
+      const uint64_t key = b->h_keys[(size_t)(o + k)];
+      for (int t = 0; t < nt; ++t)
+        if (key_matches(key, prefixes[(size_t)g * nt + t], consumed))
+          hist[((size_t)g * nt + t) * bins + key_digit(key, consumed, dbits)]++;
+    }
+    o += n;
+  }
+  return ECONO_OK;
+#else
+  void *dp, *dh;
+  const size_t hbytes = sizeof(uint64_t) * (size_t)groups * nt * bins;
+  if (dev_alloc(&dp, sizeof(uint64_t) * (size_t)groups * nt)) return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
+  if (dev_alloc(&dh, hbytes)) {
+    dev_free(dp);
+    return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
+  }
+  dev_h2d(dp, prefixes, sizeof(uint64_t) * (size_t)groups * nt);
+  int64_t nmax = 1;
+  for (auto& h : b->inst) nmax = imax(nmax, h.desc.n);
+  const unsigned gx = (unsigned)imax(1, imin((nmax + 255) / 256, (148 * 4 + ni - 1) / ni));
+  k_jct_hist<<<dim3(gx, (unsigned)ni), 256, sizeof(uint32_t) * nt * bins, b->stream>>>(
+      b->d_insts, b->d_koff, b->d_keys, per_instance, nt, (const uint64_t*)dp, consumed, dbits,
+      (unsigned long long*)dh);
+  int rc = sync_batch(b, err, errlen);
+  if (!rc) rc = cuda_check(err, errlen, "k_jct_hist");
+  if (!rc && dev_d2h(hist, dh, hbytes)) {
+    set_err(err, errlen, "copy failed");
+    rc = ECONO_ECUDA;
+  }
+  dev_free(dp);
+  dev_free(dh);
+  return rc;
+#endif
+}
+
+// Exact k-th smallest keys: ranks[g][t] (0-based) -> keys[g][t].
+int jct_select(econo_batch* b, int per_instance, int nt, const uint64_t* ranks, uint64_t* keys, char* err,
+               size_t errlen) {
+  const int groups = per_instance ? (int)b->inst.size() : 1;
+  std::vector<uint64_t> pre((size_t)groups * nt, 0), rk(ranks, ranks + (size_t)groups * nt);
+  int consumed = 0;
+  for (int pass = 0; pass < 6; ++pass) {
+    const int db = kDigitBits[pass];
+    const size_t bins = (size_t)1 << db;
+    std::vector<uint64_t> h((size_t)groups * nt * bins);
+    int rc = jct_hist(b, per_instance, nt, pre.data(), consumed, db, h.data(), err, errlen);
+    if (rc) return rc;
+    for (size_t gt = 0; gt < (size_t)groups * nt; ++gt) {
+      uint64_t cum = 0;
+      size_t d = 0;
+      for (; d < bins; ++d) {
+        const uint64_t c = h[gt * bins + d];
+        if (rk[gt] < cum + c) break;
+        cum += c;
+      }
+      if (d == bins) return set_err(err, errlen, "radix select: rank beyond the key count"), ECONO_ESIM;
+      rk[gt] -= cum;
+      pre[gt] = (pre[gt] << db) | (uint64_t)d;
+    }
+    consumed += db;
+  }
+  std::copy(pre.begin(), pre.end(), keys);
+  return ECONO_OK;
+}
+
+// percentile() (metrics.hpp:81-89) per instance from exact order statistics.
+int jct_percentiles(econo_batch* b, const double* q, int nq, double* out, char* err, size_t errlen) {
+  if (nq < 1 || nq > 4) return set_err(err, errlen, "1..4 quantiles per call"), ECONO_ECONFIG;
+  int rc = jct_prepare(b, err, errlen);
+  if (rc) return rc;
+  const int32_t ni = (int32_t)b->inst.size();
+  const int nt = 2 * nq;
+  std::vector<uint64_t> ranks((size_t)ni * nt), keys((size_t)ni * nt);
+  std::vector<double> frac((size_t)ni * nq);
+  for (int32_t i = 0; i < ni; ++i) {
+    const int64_t n = b->inst[(size_t)i].desc.n;
+    for (int k = 0; k < nq; ++k) {
+      const double rank = q[k] * (double)(n - 1);
+      const uint64_t lo = (uint64_t)rank;
+      const uint64_t hi = std::min<uint64_t>(lo + 1, (uint64_t)(n - 1));
+      frac[(size_t)i * nq + k] = rank - (double)lo;
+      ranks[(size_t)i * nt + 2 * k] = lo;
+      ranks[(size_t)i * nt + 2 * k + 1] = hi;
+    }
+  }
+  rc = jct_select(b, 1, nt, ranks.data(), keys.data(), err, errlen);
+  if (rc) return rc;
+  for (int32_t i = 0; i < ni; ++i)
+    for (int k = 0; k < nq; ++k) {
+      const double vlo = key_double(keys[(size_t)i * nt + 2 * k]), vhi = key_double(keys[(size_t)i * nt + 2 * k + 1]);
+      const double f = frac[(size_t)i * nq + k];
+      out[(size_t)i * nq + k] = vlo * (1.0 - f) + vhi * f;
+    }
   return ECONO_OK;
 }
 
@@ -929,11 +1111,10 @@ void econo_batch_destroy(econo_batch* b) {
     dev_free(h.d_sm);
   }
   dev_free(b->d_insts);
+  dev_free(b->d_keys);
+  dev_free(b->d_koff);
   for (auto* v : b->views) delete v;
 #ifndef ECONO_HOSTSIM
-  for (auto ls : b->lanes) cudaStreamDestroy(ls);
-  for (auto ev : b->lane_done) cudaEventDestroy(ev);
-  if (b->fork) cudaEventDestroy(b->fork);
   if (b->stream) cudaStreamDestroy(b->stream);
 #endif
   delete b;
@@ -1189,10 +1370,6 @@ int econo_batch_launch(econo_batch* b, int64_t max_steps, void* stream) {
   return ECONO_OK;
 }
 
-int econo_batch_launch_lanes(econo_batch* b, int64_t max_steps, int32_t n_launches, int32_t n_lanes,
-                             void* stream) {
-  return launch_lanes(b, max_steps, n_launches, n_lanes, stream);
-}
 
 int econo_batch_sync(econo_batch* b, char* err, size_t errlen) {
   int rc = sync_batch(b, err, errlen);
@@ -1262,6 +1439,84 @@ int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen) 
   dev_free(d);
   return rc;
 #endif
+}
+
+int econo_batch_jct_prepare(econo_batch* b, char* err, size_t errlen) { return jct_prepare(b, err, errlen); }
+
+int econo_batch_jct_hist(econo_batch* b, int32_t n_targets, const uint64_t* prefixes, int32_t consumed_bits,
+                         int32_t digit_bits, uint64_t* hist, char* err, size_t errlen) {
+  return jct_hist(b, 0, n_targets, prefixes, consumed_bits, digit_bits, hist, err, errlen);
+}
+
+int econo_batch_jct_percentiles(econo_batch* b, const double* q, int32_t nq, double* out, char* err, size_t errlen) {
+  return jct_percentiles(b, q, nq, out, err, errlen);
+}
+
+double econo_jct_key_to_double(uint64_t key) { return key_double(key); }
+
+// aggregate() (metrics.hpp:96-175) for every instance at once: sums from the
+// device partials (cross-request sums in a different order: the 1e-6 tier),
+// p5/p95 exact from the radix select, counts and the completion histogram
+// exact. trace_hash is left 0 (FNV-1a over the CSV bytes is inherently
+// sequential; econo_report computes it for a single engine).
+int econo_batch_reports(econo_batch* b, EconoReport* out, char* err, size_t errlen) {
+  const int32_t ni = (int32_t)b->inst.size();
+  std::vector<double> parts((size_t)ni * ECONO_PARTIAL_WORDS), pct((size_t)ni * 2);
+  int rc = econo_batch_partials(b, parts.data(), err, errlen);
+  if (rc) return rc;
+  const double q[2] = {0.05, 0.95};
+  rc = jct_percentiles(b, q, 2, pct.data(), err, errlen);
+  if (rc) return rc;
+  for (int32_t i = 0; i < ni; ++i) {
+    const double* p = parts.data() + (size_t)i * ECONO_PARTIAL_WORDS;
+    const Inst& I = b->inst[(size_t)i].desc;
+    EconoReport& r = out[i];
+    memset(&r, 0, sizeof(r));
+    const double n = p[0];
+    r.mean_jct = p[1] / n;
+    r.p5_jct = pct[(size_t)i * 2];
+    r.p95_jct = pct[(size_t)i * 2 + 1];
+    r.mean_tbt = p[3] > 0 ? p[2] / p[3] : 0.0;
+    r.ssr = p[5] / n;
+    r.normalized_latency = p[4] / n;
+    r.makespan = p[10];
+    if (r.makespan > 0.0) {
+      r.throughput_rps = n / r.makespan;
+      r.throughput_tps = p[6] / r.makespan;
+      r.goodput_rps = p[5] / r.makespan;
+    }
+    r.allocation_failure_pct = 100.0 * p[9] / n;
+    r.preemptions = (int64_t)p[7];
+    r.reserve_draws = (int64_t)p[8];
+    r.mean_waiting = p[11] / n;
+    r.mean_execution = p[12] / n;
+    r.mean_preemption = p[13] / n;
+    r.mean_scheduling = p[14] / n;
+    const int64_t ex = I.executed;
+    r.iterations = ex;
+    if (ex > 0) {
+      r.mean_forward_size = (double)I.agg_fs / (double)ex;
+      r.mean_kvc_written = I.agg_written / (double)ex;
+      r.mean_kvc_allocated = I.agg_allocated / (double)ex;
+      r.tfs_hit_frac = (double)I.agg_tfs_hits / (double)ex;
+      r.pt_admit_frac = (double)I.agg_pt_iters / (double)ex;
+      std::vector<int64_t> hist((size_t)I.hist_cap);
+      if (dev_d2h(hist.data(), I.hist, sizeof(int64_t) * hist.size()))
+        return set_err(err, errlen, "device copy failed"), ECONO_ECUDA;
+      int k = 0;
+      for (int c = 0; c < I.hist_cap && k < ECONO_MAX_HIST; ++c)
+        if (hist[(size_t)c]) {
+          r.hist_count[k] = c;
+          r.hist_frac[k] = (double)hist[(size_t)c] / (double)ex;
+          ++k;
+        }
+      r.n_hist = k;
+    }
+    r.hosted_slots = I.hosted_total;
+    r.hosted_overruns = I.hosted_overruns;
+    r.trace_hash = 0;
+  }
+  return ECONO_OK;
 }
 
 // Development counters: per instance ECONO_DEBUG_WORDS int64 (engine.cuh Inst::prof).

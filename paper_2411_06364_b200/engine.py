@@ -22,10 +22,11 @@ LIB_PATH = os.path.join(HERE, "_lib", "libeconoserve_b200.so")
 SYMBOLS = [
     "econo_default_options", "econo_create", "econo_step", "econo_run", "econo_records",
     "econo_report", "econo_events", "econo_samples", "econo_scalars", "econo_snapshot",
-    "econo_destroy", "econo_batch_create", "econo_batch_launch", "econo_batch_launch_lanes",
-    "econo_batch_sync",
+    "econo_destroy", "econo_batch_create", "econo_batch_launch", "econo_batch_sync",
     "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
     "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore", "econo_batch_debug",
+    "econo_batch_reports", "econo_batch_jct_prepare", "econo_batch_jct_hist", "econo_batch_jct_percentiles",
+    "econo_jct_key_to_double",
 ]
 
 
@@ -79,7 +80,6 @@ def load(path=None):
     L.econo_batch_create.argtypes = [C.POINTER(vp), C.POINTER(i64), i32, C.POINTER(abi.Options),
                                      C.c_int, C.POINTER(vp), cp, sz]
     L.econo_batch_launch.argtypes = [vp, i64, vp]
-    L.econo_batch_launch_lanes.argtypes = [vp, i64, i32, i32, vp]
     L.econo_batch_sync.argtypes = [vp, cp, sz]
     L.econo_batch_scalars.argtypes = [vp, C.POINTER(abi.Scalars)]
     L.econo_batch_engine.argtypes = [vp, i32, C.POINTER(vp)]
@@ -88,6 +88,12 @@ def load(path=None):
     L.econo_batch_checkpoint.argtypes = [vp, cp, sz]
     L.econo_batch_restore.argtypes = [vp, cp, sz]
     L.econo_batch_debug.argtypes = [vp, vp]
+    L.econo_batch_reports.argtypes = [vp, vp, cp, sz]
+    L.econo_batch_jct_prepare.argtypes = [vp, cp, sz]
+    L.econo_batch_jct_hist.argtypes = [vp, i32, vp, i32, i32, vp, cp, sz]
+    L.econo_batch_jct_percentiles.argtypes = [vp, vp, i32, vp, cp, sz]
+    L.econo_jct_key_to_double.argtypes = [C.c_uint64]
+    L.econo_jct_key_to_double.restype = C.c_double
     L.econo_generate_trace.argtypes = [i64, C.c_double, C.POINTER(abi.LengthDist),
                                        C.POINTER(abi.LengthDist), C.c_uint64, vp, cp, sz]
     _libs[path] = L
@@ -245,12 +251,6 @@ class Batch:
     def launch(self, max_steps, stream=None):
         self._L.econo_batch_launch(self.h, max_steps, stream)
 
-    def launch_lanes(self, max_steps, n_launches, n_lanes=32, stream=None):
-        """n_launches passes of `max_steps` as independent per-lane launch chains."""
-        rc = self._L.econo_batch_launch_lanes(self.h, max_steps, n_launches, n_lanes, stream)
-        if rc:
-            raise DeviceError(f"econo_batch_launch_lanes failed ({rc})")
-
     def sync(self):
         err = C.create_string_buffer(1024)
         rc = self._L.econo_batch_sync(self.h, err, 1024)
@@ -278,6 +278,45 @@ class Batch:
         out = np.zeros((self.n, abi.DEBUG_WORDS), dtype=np.int64)
         self._L.econo_batch_debug(self.h, out.ctypes.data)
         return out
+
+    def reports(self):
+        """aggregate() per instance, on the device (econo_batch_reports)."""
+        out = (abi.Report * self.n)()
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_batch_reports(self.h, out, err, 1024)
+        if rc:
+            _raise(rc, err)
+        return list(out)
+
+    def jct_percentiles(self, qs):
+        """Exact per-instance percentile() of JCT (metrics.hpp:81-89): (n_inst, len(qs))."""
+        q = np.asarray(qs, dtype=np.float64)
+        out = np.zeros((self.n, len(q)), dtype=np.float64)
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_batch_jct_percentiles(self.h, q.ctypes.data, len(q), out.ctypes.data, err, 1024)
+        if rc:
+            _raise(rc, err)
+        return out
+
+    def jct_prepare(self):
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_batch_jct_prepare(self.h, err, 1024)
+        if rc:
+            _raise(rc, err)
+
+    def jct_hist(self, prefixes, consumed_bits, digit_bits):
+        """One radix-select pass over all instances: (len(prefixes), 2**digit_bits) counts."""
+        pf = np.ascontiguousarray(prefixes, dtype=np.uint64)
+        out = np.zeros((len(pf), 1 << digit_bits), dtype=np.uint64)
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_batch_jct_hist(self.h, len(pf), pf.ctypes.data, consumed_bits, digit_bits,
+                                          out.ctypes.data, err, 1024)
+        if rc:
+            _raise(rc, err)
+        return out
+
+    def key_to_double(self, key):
+        return self._L.econo_jct_key_to_double(int(key))
 
     def partials(self):
         out = np.zeros((self.n, abi.PARTIAL_WORDS), dtype=np.float64)

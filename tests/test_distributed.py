@@ -33,13 +33,20 @@ def options():
     return o
 
 
-def local_partials(rank, world):
+def local_batch(rank, world):
     from paper_2411_06364_b200.engine import Batch
     _, trs = shard_traces(rank, world)
     b = Batch(trs, options(), lib=HOSTSIM)
     b.launch(1 << 40)
     b.sync()
-    return b.partials()
+    return b
+
+
+def local_partials(rank, world):
+    return local_batch(rank, world).partials()
+
+
+QS = [0.05, 0.5, 0.95]
 
 
 def _worker(rank, world, port_, out):
@@ -47,10 +54,12 @@ def _worker(rank, world, port_, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port_)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    p = metrics.combine(local_partials(rank, world))
+    b = local_batch(rank, world)
+    p = metrics.combine(b.partials())
     red = metrics.all_reduce(p, dist)
+    pct = metrics.global_percentiles(b, QS, dist=dist)  # 6 histogram all-reduces
     if rank == 0:
-        out.put(red)
+        out.put((red, pct))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -71,12 +80,14 @@ def test_gloo_world2_metric_reduction_matches_single_process():
     procs = [ctx.Process(target=_worker, args=(r, world, port_, q)) for r in range(world)]
     for p in procs:
         p.start()
-    red = q.get(timeout=300)
+    red, pct = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    single = metrics.combine(local_partials(0, 1))
+    b1 = local_batch(0, 1)
+    single = metrics.combine(b1.partials())
     assert np.allclose(red, single, rtol=1e-12, atol=0)
+    assert pct == metrics.global_percentiles(b1, QS)  # exact order statistics
     s = metrics.summary(red)
     assert s["requests"] == N_INST * 400
     assert s["iterations"] > 0

@@ -33,11 +33,8 @@ def run(traces, iters, launches, warm=3, lanes=0):
     sc0, d0 = b.scalars(), b.debug().copy()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
-    if lanes:
-        b.launch_lanes(iters, launches, lanes, s.cuda_stream)
-    else:
-        for _ in range(launches):
-            b.launch(iters, s.cuda_stream)
+    for _ in range(launches):
+        b.launch(iters, s.cuda_stream)
     e1.record(s)
     e1.synchronize()
     ms = e0.elapsed_time(e1)
