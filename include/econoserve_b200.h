@@ -310,6 +310,26 @@ int econo_generate_trace(int64_t n, double arrival_rate, const EconoLengthDist* 
                          const EconoLengthDist* rl, uint64_t seed, EconoTraceRecord* out,
                          char* err, size_t errlen);
 
+/* ---- wire formats either side of the path (host; wire.cpp) --------------- */
+/* load_trace_csv (workload.hpp:142-194): same header check, validation order
+ * and messages ("<name>: line N: ..."). Two-call pattern: out = NULL counts. */
+int econo_parse_trace_csv(const char* text, int64_t len, const char* name, EconoTraceRecord* out, int64_t cap,
+                          int64_t* n, char* err, size_t errlen);
+int econo_load_trace_csv(const char* path, EconoTraceRecord* out, int64_t cap, int64_t* n, char* err,
+                         size_t errlen);
+/* write_trace_csv (workload.hpp:127-134), "%.17g" arrivals; *len = bytes
+ * needed (out, when non-NULL, receives min(len, cap-1) bytes + NUL). */
+int econo_write_trace_csv(const EconoTraceRecord* trace, int64_t n, char* out, int64_t cap, int64_t* len);
+/* FNV-1a over write_trace_csv's bytes (metrics.hpp:320-328, the report's trace_hash). */
+uint64_t econo_trace_hash(const EconoTraceRecord* trace, int64_t n);
+/* to_json(report, with_records).dump(indent) (metrics.hpp:181-240), byte for
+ * byte as nlohmann::ordered_json prints it; recs = NULL omits "records";
+ * indent < 0 = compact. */
+int econo_report_to_json(const char* policy, const EconoReport* report, const EconoRecord* recs, int64_t n_recs,
+                         int32_t indent, char* out, int64_t cap, int64_t* len);
+/* nlohmann's double printer alone (Grisu2 digits + its layout rules). */
+int econo_json_double(double v, char* out, int64_t cap, int64_t* len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,7 +33,7 @@ def lib():
         L.ref_samples.restype = C.c_int64
         L.ref_finalize.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(abi.Report),
                                    C.c_char_p, C.c_size_t]
-        L.ref_report_json.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, C.c_int]
+        L.ref_report_json.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, C.c_int, C.c_int]
         L.ref_report_json.restype = C.c_int64
         L.ref_scalars.argtypes = [C.c_void_p, C.POINTER(abi.Scalars)]
         L.ref_snapshot.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
@@ -56,6 +56,12 @@ def lib():
         L.ref_predict.argtypes = [C.POINTER(abi.Options), C.c_uint64, C.c_void_p, C.c_int64,
                                   C.c_void_p]
         L.ref_predict.restype = C.c_int64
+        L.ref_json_double.argtypes = [C.c_double, C.c_char_p, C.c_int64]
+        L.ref_json_double.restype = C.c_int64
+        L.ref_parse_csv.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_void_p, C.c_int64,
+                                    C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]
+        L.ref_write_csv.argtypes = [C.c_void_p, C.c_int64, C.c_char_p, C.c_int64]
+        L.ref_write_csv.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -168,10 +174,10 @@ class RefEngine:
     def report(self):
         return self.finalize()
 
-    def report_json(self, with_records=True):
-        n = lib().ref_report_json(self.h, None, 0, int(with_records))
+    def report_json(self, with_records=True, indent=-1):
+        n = lib().ref_report_json(self.h, None, 0, int(with_records), indent)
         buf = C.create_string_buffer(n + 1)
-        lib().ref_report_json(self.h, buf, n + 1, int(with_records))
+        lib().ref_report_json(self.h, buf, n + 1, int(with_records), indent)
         return buf.value.decode()
 
     def scalars(self):
@@ -195,3 +201,31 @@ class RefEngine:
         pt = C.c_int64()
         secs = lib().ref_time_steps(self.h, steps, C.byref(pt))
         return secs, pt.value
+
+
+def json_double(v):
+    """nlohmann::ordered_json(v).dump() (the reports' double printer)."""
+    buf = C.create_string_buffer(64)
+    n = lib().ref_json_double(float(v), buf, 64)
+    return buf.value[:n].decode()
+
+
+def parse_csv(text, name="<stream>"):
+    """load_trace_csv on text: (trace, None) or (None, (code, message))."""
+    b = text.encode() if isinstance(text, str) else text
+    n = C.c_int64()
+    err = C.create_string_buffer(1024)
+    rc = lib().ref_parse_csv(b, len(b), name.encode(), None, 0, C.byref(n), err, 1024)
+    if rc:
+        return None, (rc, err.value.decode())
+    out = np.zeros(n.value, dtype=abi.TRACE_DTYPE)
+    lib().ref_parse_csv(b, len(b), name.encode(), out.ctypes.data, n.value, C.byref(n), err, 1024)
+    return out, None
+
+
+def write_csv(trace):
+    t = abi.trace_array(trace)
+    n = lib().ref_write_csv(t.ctypes.data, len(t), None, 0)
+    buf = C.create_string_buffer(n + 1)
+    lib().ref_write_csv(t.ctypes.data, len(t), buf, n + 1)
+    return buf.value[:n].decode()

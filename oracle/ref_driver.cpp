@@ -321,12 +321,12 @@ int ref_finalize(void* hv, EconoRecord* recs, int64_t cap, EconoReport* rep_out,
   }
 }
 
-// to_json(report).dump() of the finished run (byte-level report schema).
-int64_t ref_report_json(void* hv, char* out, int64_t cap, int with_records) {
+// to_json(report).dump(indent) of the finished run (byte-level report schema).
+int64_t ref_report_json(void* hv, char* out, int64_t cap, int with_records, int indent) {
   auto* h = static_cast<RefEngine*>(hv);
   try {
     MetricsReport rep = h->eng->report();
-    std::string s = to_json(rep, with_records != 0).dump();
+    std::string s = to_json(rep, with_records != 0).dump(indent);
     if (out && cap > 0) std::snprintf(out, static_cast<size_t>(cap), "%s", s.c_str());
     return static_cast<int64_t>(s.size());
   } catch (const std::exception&) {
@@ -605,6 +605,47 @@ int64_t ref_predict(const EconoOptions* o, uint64_t seed, const int64_t* true_rl
   for (int64_t i = 0; i < n; ++i)
     out[i] = apply_padding(predict_rl(true_rl[i], e.predictor, g), e.predictor.padding_ratio);
   return n;
+}
+
+// nlohmann::ordered_json(v).dump(): the double printer the reports use.
+int64_t ref_json_double(double v, char* out, int64_t cap) {
+  const std::string s = Json(v).dump();
+  if (out && cap > 0) std::snprintf(out, static_cast<size_t>(cap), "%s", s.c_str());
+  return static_cast<int64_t>(s.size());
+}
+
+// load_trace_csv(istream, name) (workload.hpp:142-194) on an in-memory text.
+int ref_parse_csv(const char* text, int64_t len, const char* name, EconoTraceRecord* out, int64_t cap,
+                  int64_t* n, char* err, size_t errlen) {
+  try {
+    std::istringstream in(std::string(text, static_cast<size_t>(len)));
+    Trace t = load_trace_csv(in, name);
+    *n = static_cast<int64_t>(t.size());
+    for (int64_t i = 0; i < *n && i < cap; ++i) {
+      out[i].arrival_time = t[static_cast<size_t>(i)].arrival_time;
+      out[i].prompt_len = t[static_cast<size_t>(i)].prompt_len;
+      out[i].true_rl = t[static_cast<size_t>(i)].true_rl;
+    }
+    return ECONO_OK;
+  } catch (const ConfigError& e) {
+    set_err(err, errlen, e.what());
+    return ECONO_ECONFIG;
+  }
+}
+
+// write_trace_csv (workload.hpp:127-134).
+int64_t ref_write_csv(const EconoTraceRecord* t, int64_t n, char* out, int64_t cap) {
+  Trace tr(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    tr[static_cast<size_t>(i)].arrival_time = t[i].arrival_time;
+    tr[static_cast<size_t>(i)].prompt_len = t[i].prompt_len;
+    tr[static_cast<size_t>(i)].true_rl = t[i].true_rl;
+  }
+  std::ostringstream oss;
+  write_trace_csv(oss, tr);
+  const std::string s = oss.str();
+  if (out && cap > 0) std::snprintf(out, static_cast<size_t>(cap), "%s", s.c_str());
+  return static_cast<int64_t>(s.size());
 }
 
 }  // extern "C"

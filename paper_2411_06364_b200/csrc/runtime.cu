@@ -448,10 +448,17 @@ __global__ void __launch_bounds__(256) k_jct_hist(const Inst* insts, const int64
   const uint64_t* pf = prefixes + (per_instance ? (size_t)blockIdx.y * nt : 0);
   uint64_t p[8];
   for (int t = 0; t < nt; ++t) p[t] = pf[t];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = kk[i];
-    for (int t = 0; t < nt; ++t)
-      if (key_matches(k, p[t], consumed)) atomicAdd(&sh[t * bins + key_digit(k, consumed, dbits)], 1u);
+  // JCTs cluster, so many lanes hit the same bin: lanes with equal (target,
+  // digit) are merged with one match_any and their leader adds the count.
+  const int64_t n_pad = (n + 31) & ~(int64_t)31;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool in = i < n;
+    const uint64_t k = in ? kk[i] : 0;
+    for (int t = 0; t < nt; ++t) {
+      const int bin = in && key_matches(k, p[t], consumed) ? (int)(t * bins + key_digit(k, consumed, dbits)) : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      if (bin >= 0 && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&sh[bin], (uint32_t)__popc(peers));
+    }
   }
   __syncthreads();
   unsigned long long* h = hist + (per_instance ? (size_t)blockIdx.y * nt * bins : 0);
@@ -973,26 +980,55 @@ int jct_hist(econo_batch* b, int per_instance, int nt, const uint64_t* prefixes,
   }
   return ECONO_OK;
 #else
+  // identical prefixes (e.g. every target in the first pass) share one histogram
+  std::vector<uint64_t> up;
+  std::vector<int> map_t((size_t)groups * nt);
+  int nu = 0;
+  for (int g = 0; g < groups; ++g) {
+    std::vector<uint64_t> u;
+    for (int t = 0; t < nt; ++t) {
+      const uint64_t pfx = prefixes[(size_t)g * nt + t];
+      size_t j = 0;
+      while (j < u.size() && u[j] != pfx) ++j;
+      if (j == u.size()) u.push_back(pfx);
+      map_t[(size_t)g * nt + t] = (int)j;
+    }
+    nu = std::max(nu, (int)u.size());
+  }
+  up.assign((size_t)groups * nu, 0);
+  for (int g = 0; g < groups; ++g)
+    for (int t = 0; t < nt; ++t) up[(size_t)g * nu + map_t[(size_t)g * nt + t]] = prefixes[(size_t)g * nt + t];
+  static bool smem_set = false;
+  if (!smem_set) {
+    cudaFuncSetAttribute(k_jct_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2048 * 4);
+    smem_set = true;
+  }
   void *dp, *dh;
-  const size_t hbytes = sizeof(uint64_t) * (size_t)groups * nt * bins;
-  if (dev_alloc(&dp, sizeof(uint64_t) * (size_t)groups * nt)) return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
+  const size_t hbytes = sizeof(uint64_t) * (size_t)groups * nu * bins;
+  if (dev_alloc(&dp, sizeof(uint64_t) * (size_t)groups * nu)) return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
   if (dev_alloc(&dh, hbytes)) {
     dev_free(dp);
     return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
   }
-  dev_h2d(dp, prefixes, sizeof(uint64_t) * (size_t)groups * nt);
+  dev_h2d(dp, up.data(), sizeof(uint64_t) * (size_t)groups * nu);
   int64_t nmax = 1;
   for (auto& h : b->inst) nmax = imax(nmax, h.desc.n);
   const unsigned gx = (unsigned)imax(1, imin((nmax + 255) / 256, (148 * 4 + ni - 1) / ni));
-  k_jct_hist<<<dim3(gx, (unsigned)ni), 256, sizeof(uint32_t) * nt * bins, b->stream>>>(
-      b->d_insts, b->d_koff, b->d_keys, per_instance, nt, (const uint64_t*)dp, consumed, dbits,
+  k_jct_hist<<<dim3(gx, (unsigned)ni), 256, sizeof(uint32_t) * nu * bins, b->stream>>>(
+      b->d_insts, b->d_koff, b->d_keys, per_instance, nu, (const uint64_t*)dp, consumed, dbits,
       (unsigned long long*)dh);
   int rc = sync_batch(b, err, errlen);
   if (!rc) rc = cuda_check(err, errlen, "k_jct_hist");
-  if (!rc && dev_d2h(hist, dh, hbytes)) {
+  std::vector<uint64_t> hu((size_t)groups * nu * bins);
+  if (!rc && dev_d2h(hu.data(), dh, hbytes)) {
     set_err(err, errlen, "copy failed");
     rc = ECONO_ECUDA;
   }
+  if (!rc)
+    for (int g = 0; g < groups; ++g)
+      for (int t = 0; t < nt; ++t)
+        memcpy(hist + ((size_t)g * nt + t) * bins, hu.data() + ((size_t)g * nu + map_t[(size_t)g * nt + t]) * bins,
+               sizeof(uint64_t) * bins);
   dev_free(dp);
   dev_free(dh);
   return rc;
