@@ -113,6 +113,20 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def measured_traffic(instances, iters):
+    """DRAM bytes per k_engine_steps launch from the committed ncu capture of
+    this exact configuration (profiles/r01_traffic.json), else None."""
+    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    c = d.get("config", {})
+    if c.get("instances_per_gpu") == instances and c.get("iters_per_step") == iters:
+        return d["dram_bytes_per_launch"]
+    return None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -282,6 +296,12 @@ def run_ours(args):
     abytes = algorithmic_bytes(sc0, sc1, args.iters * args.steps, I)
     t = torch.tensor([tot, float(adm), float(gts), float(e2e_adm), t_e2e], dtype=torch.float64,
                      device=dev)
+    # end-of-run report reduction (after the e2e window): exact global p5/p95
+    # JCT by radix select, one histogram all-reduce per digit pass
+    torch.cuda.synchronize()
+    tr0 = time.perf_counter()
+    pct = metrics.global_percentiles(b, [0.05, 0.95], dist=dist if world > 1 else None, device=dev)
+    t_pct = time.perf_counter() - tr0
     if world > 1:
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -323,9 +343,13 @@ def run_ours(args):
         "tracegen_s": t_gen,
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak,
+                     "traffic": measured_traffic(I, args.iters),
+                     "per_launch_algorithmic_bytes": abytes / args.steps, "peak_kind": peak_kind,
                      "kernel": "k_engine_steps",
-                     "note": "latency-bound dependency chain; see DESIGN.md §5"},
+                     "note": "latency-bound dependency chain (one warp per instance); algorithmic bytes = "
+                             "the state each simulated iteration updates (DESIGN.md §5); traffic = ncu DRAM "
+                             "bytes per launch of this config (profiles/r01_traffic.json): most of it hits L2"},
         "clocks": clk,
         "e2e": {"value": e2e_adm_all / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
@@ -333,6 +357,10 @@ def run_ours(args):
                          "warm-up + timed steps + partial sums to host, wall clock; admissions counted "
                          "after the ingest"},
         "errors": len(errors),
+        "report_reduction": {"global_jct_p5_p95": pct, "ms": 1e3 * t_pct,
+                             "how": "k_jct_keys + 6 k_jct_hist radix-select passes, histograms all-reduced "
+                                    "across ranks (NCCL) per pass; JCT of requests not yet complete is "
+                                    "completion -1 by the reference's convention"},
         "global_metrics": {k: v for k, v in metrics.summary(gsum).items()
                            if k in ("requests", "iterations", "mean_forward_size", "mean_kvc_written",
                                     "tfs_hit_frac", "pt_admit_frac", "hosted_slots")},

@@ -22,6 +22,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -402,6 +403,72 @@ class Engine {
 inline MetricsReport run(Trace trace, const EngineOptions& opt) {
   Engine engine(std::move(trace), opt);
   return engine.run();
+}
+
+// ---- wire formats (workload.hpp:127-194, metrics.hpp:181-240, 320-328) ----
+// load_trace_csv / write_trace_csv with the reference's validation and bytes.
+inline Trace load_trace_csv(const std::string& path) {
+  char err[1024] = {0};
+  int64_t n = 0;
+  int rc = econo_load_trace_csv(path.c_str(), nullptr, 0, &n, err, sizeof(err));
+  if (rc) detail::raise(rc, err);
+  Trace t(static_cast<size_t>(n));
+  rc = econo_load_trace_csv(path.c_str(), reinterpret_cast<EconoTraceRecord*>(t.data()), n, &n, err, sizeof(err));
+  if (rc) detail::raise(rc, err);
+  return t;
+}
+inline std::string write_trace_csv(const Trace& trace) {
+  int64_t len = 0;
+  const auto* p = reinterpret_cast<const EconoTraceRecord*>(trace.data());
+  econo_write_trace_csv(p, static_cast<int64_t>(trace.size()), nullptr, 0, &len);
+  std::string s(static_cast<size_t>(len) + 1, '\0');
+  econo_write_trace_csv(p, static_cast<int64_t>(trace.size()), &s[0], len + 1, &len);
+  s.resize(static_cast<size_t>(len));
+  return s;
+}
+// to_json(report, with_records).dump(indent) as a string, byte-identical to the
+// reference's nlohmann::ordered_json output (the CLI writes dump(2) + "\n").
+inline std::string to_json_string(const MetricsReport& m, bool with_records = true, int indent = -1) {
+  EconoReport r;
+  std::memset(&r, 0, sizeof(r));
+  r.trace_hash = m.trace_hash;
+  r.mean_jct = m.mean_jct; r.p5_jct = m.p5_jct; r.p95_jct = m.p95_jct; r.mean_tbt = m.mean_tbt; r.ssr = m.ssr;
+  r.throughput_rps = m.throughput_rps; r.throughput_tps = m.throughput_tps; r.goodput_rps = m.goodput_rps;
+  r.normalized_latency = m.normalized_latency; r.mean_kvc_written = m.mean_kvc_written;
+  r.mean_kvc_allocated = m.mean_kvc_allocated; r.mean_forward_size = m.mean_forward_size;
+  r.allocation_failure_pct = m.allocation_failure_pct; r.tfs_hit_frac = m.tfs_hit_frac;
+  r.pt_admit_frac = m.pt_admit_frac; r.iterations = m.iterations; r.makespan = m.makespan;
+  r.preemptions = m.preemptions; r.reserve_draws = m.reserve_draws; r.hosted_slots = m.hosted_slots;
+  r.hosted_overruns = m.hosted_overruns; r.mean_waiting = m.mean_waiting; r.mean_execution = m.mean_execution;
+  r.mean_preemption = m.mean_preemption; r.mean_scheduling = m.mean_scheduling;
+  for (const auto& kv : m.iteration_completion_histogram) {
+    if (r.n_hist >= ECONO_MAX_HIST) break;
+    r.hist_count[r.n_hist] = kv.first;
+    r.hist_frac[r.n_hist] = kv.second;
+    ++r.n_hist;
+  }
+  std::vector<EconoRecord> recs;
+  if (with_records) {
+    recs.reserve(m.records.size());
+    for (const auto& q : m.records) {
+      EconoRecord x;
+      std::memset(&x, 0, sizeof(x));
+      x.id = q.id; x.arrival = q.arrival; x.first_token_time = q.first_token_time;
+      x.completion_time = q.completion_time; x.waiting_time = q.waiting_time; x.execution_time = q.execution_time;
+      x.preemption_time = q.preemption_time; x.scheduling_time_share = q.scheduling_time_share;
+      x.preempt_count = q.preempt_count; x.reserve_draws = q.reserve_draws; x.met_slo = q.met_slo ? 1 : 0;
+      x.prompt_len = q.prompt_len; x.true_rl = q.true_rl; x.slo_deadline = q.slo_deadline;
+      x.alloc_failure = q.alloc_failure ? 1 : 0;
+      recs.push_back(x);
+    }
+  }
+  const EconoRecord* rp = with_records ? recs.data() : nullptr;
+  int64_t len = 0;
+  econo_report_to_json(m.policy.c_str(), &r, rp, static_cast<int64_t>(recs.size()), indent, nullptr, 0, &len);
+  std::string s(static_cast<size_t>(len) + 1, '\0');
+  econo_report_to_json(m.policy.c_str(), &r, rp, static_cast<int64_t>(recs.size()), indent, &s[0], len + 1, &len);
+  s.resize(static_cast<size_t>(len));
+  return s;
 }
 
 }  // namespace econosim_b200

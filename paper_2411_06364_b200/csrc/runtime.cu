@@ -450,14 +450,24 @@ __global__ void __launch_bounds__(256) k_jct_hist(const Inst* insts, const int64
   for (int t = 0; t < nt; ++t) p[t] = pf[t];
   // JCTs cluster, so many lanes hit the same bin: lanes with equal (target,
   // digit) are merged with one match_any and their leader adds the count.
+  // After the first pass almost no key matches a target's prefix, and a warp
+  // with no match skips straight to its next load (a pure HBM stream).
   const int64_t n_pad = (n + 31) & ~(int64_t)31;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += (int64_t)gridDim.x * blockDim.x) {
-    const bool in = i < n;
-    const uint64_t k = in ? kk[i] : 0;
-    for (int t = 0; t < nt; ++t) {
-      const int bin = in && key_matches(k, p[t], consumed) ? (int)(t * bins + key_digit(k, consumed, dbits)) : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, bin);
-      if (bin >= 0 && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&sh[bin], (uint32_t)__popc(peers));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += 2 * stride) {
+    const bool in0 = i < n, in1 = i + stride < n;
+    const uint64_t k0 = in0 ? __ldcs(kk + i) : 0, k1 = in1 ? __ldcs(kk + i + stride) : 0;
+#pragma unroll 2
+    for (int h = 0; h < 2; ++h) {
+      const uint64_t k = h ? k1 : k0;
+      const bool in = h ? in1 : in0;
+      for (int t = 0; t < nt; ++t) {
+        const bool m = in && key_matches(k, p[t], consumed);
+        if (!__any_sync(0xffffffffu, m)) continue;
+        const int bin = m ? (int)(t * bins + key_digit(k, consumed, dbits)) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        if (m && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&sh[bin], (uint32_t)__popc(peers));
+      }
     }
   }
   __syncthreads();
@@ -1013,7 +1023,7 @@ int jct_hist(econo_batch* b, int per_instance, int nt, const uint64_t* prefixes,
   dev_h2d(dp, up.data(), sizeof(uint64_t) * (size_t)groups * nu);
   int64_t nmax = 1;
   for (auto& h : b->inst) nmax = imax(nmax, h.desc.n);
-  const unsigned gx = (unsigned)imax(1, imin((nmax + 255) / 256, (148 * 4 + ni - 1) / ni));
+  const unsigned gx = (unsigned)imax(1, imin((nmax + 511) / 512, (148 * 16 + ni - 1) / ni));
   k_jct_hist<<<dim3(gx, (unsigned)ni), 256, sizeof(uint32_t) * nu * bins, b->stream>>>(
       b->d_insts, b->d_koff, b->d_keys, per_instance, nu, (const uint64_t*)dp, consumed, dbits,
       (unsigned long long*)dh);

@@ -166,6 +166,33 @@ int main() {
     }
     CHECK(threw);
   }
+  {  // wire formats: write_trace_csv -> load_trace_csv round trip; the report as the CLI writes it
+    Trace t = saturating_trace(60, 30.0, 8, 40, 8, 40, 5);
+    const std::string csv = write_trace_csv(t);
+    CHECK(csv.rfind("arrival_time,prompt_len,response_len\n", 0) == 0);
+    const char* path = "/tmp/econosim_b200_facade_trace.csv";
+    FILE* f = std::fopen(path, "w");
+    std::fputs(csv.c_str(), f);
+    std::fclose(f);
+    Trace back = load_trace_csv(path);
+    CHECK(back.size() == t.size());
+    bool same = true;
+    for (size_t i = 0; i < t.size(); ++i)
+      same = same && back[i].arrival_time == t[i].arrival_time && back[i].prompt_len == t[i].prompt_len &&
+             back[i].true_rl == t[i].true_rl;
+    CHECK(same);
+    MetricsReport rep = run(back, base_options(PolicyKind::EconoFull));
+    const std::string js = to_json_string(rep, true, 2);
+    CHECK(js.rfind("{\n  \"policy\": \"econoserve-full\",\n  \"trace_hash\": ", 0) == 0);
+    CHECK(to_json_string(rep, false).find("\"records\"") == std::string::npos);
+    bool threw = false;
+    try {
+      load_trace_csv("/nonexistent/trace.csv");
+    } catch (const ConfigError& ex) {
+      threw = std::string(ex.what()).find("cannot open trace file") != std::string::npos;
+    }
+    CHECK(threw);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "all facade checks passed", failures);
   return failures ? 1 : 0;
 }
