@@ -238,7 +238,8 @@ def run_ours(args):
     I = args.instances
     seeds = [1000 + rank * I + i for i in range(I)]
     t0 = time.time()
-    traces = make_traces(generate_trace, args.n, seeds, pinned=True)
+    # host trace generation shares the box's cores between the ranks
+    traces = make_traces(generate_trace, args.n, seeds, threads=max(2, (os.cpu_count() or 2) // world), pinned=True)
     t_gen = time.time() - t0
 
     # ---- one pass through the public API, from host trace buffers:
