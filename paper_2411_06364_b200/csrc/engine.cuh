@@ -518,13 +518,40 @@ EDEV void tree_set(Inst& I, int64_t id, int32_t v) {
 // ------------------------------------------------------------------------
 // KVC block manager (kvc.hpp:35-424) over the address-sorted region array.
 // ------------------------------------------------------------------------
-EDEV int32_t addr_lower(const Inst& I, Tok start) {  // first position with start >= start
-  int32_t lo = 0, hi = I.n_regions;
+// First position p in [0, n) with pred(p) true for a monotone predicate
+// (false...false true...true), n if none. One warp-wide round probes W
+// evenly spaced positions in parallel, so a search costs ceil(log_W n)
+// dependent round trips instead of log2 n (the host build bisects).
+template <class F>
+EDEV int32_t warp_search(int32_t n, F pred) {
+  int32_t lo = 0, hi = n;  // answer in [lo, hi]; pred(hi) is true or hi == n
+#ifdef __CUDACC__
+  while (hi - lo > W) {
+    const int32_t step = (hi - lo + W - 1) / W;
+    const int32_t q = lo + (LANE + 1) * step - 1;  // last position of block LANE
+    const bool t = q >= hi || pred(q);
+    const unsigned m = BALLOT(t);
+    if (!m) return hi;  // every block's last position (up to hi - 1) is false
+    const int b = FFS(m);
+    const int32_t qb = lo + (b + 1) * step - 1;
+    lo += b * step;
+    if (qb < hi) hi = qb;
+  }
+  const int32_t q = lo + LANE;
+  const unsigned m = BALLOT(q < hi && pred(q));
+  return m ? lo + FFS(m) : hi;
+#else
   while (lo < hi) {
     const int32_t mid = (lo + hi) >> 1;
-    if (I.rg_start[I.addr[mid]] < start) lo = mid + 1; else hi = mid;
+    if (pred(mid)) hi = mid; else lo = mid + 1;
   }
   return lo;
+#endif
+}
+EDEV int32_t addr_lower(const Inst& I, Tok start) {  // first position with start >= start
+  const int32_t* addr = I.addr;
+  const int32_t* rs = I.rg_start;
+  return warp_search(I.n_regions, [&](int32_t p) { return (Tok)rs[addr[p]] >= start; });
 }
 EDEV void addr_insert_region(Inst& I, int32_t r) {
   const int32_t pos = addr_lower(I, I.rg_start[r]);
@@ -541,16 +568,17 @@ EDEV int32_t region_new(Inst& I, int32_t owner, Tok start, Tok len) {  // all la
   if (I.reg_free_top <= 0) { set_error(I, ERR_TABLE_OVERFLOW, owner, 2); return -1; }
   const int32_t r = I.reg_free[I.reg_free_top - 1];
   WSYNC();
-  if (LANE == 0) {
+  if (LANE == 0) {  // the owner's list fields are loaded before any store
+    const int32_t cnt = I.reg_cnt[owner], tail = I.reg_tail[owner], hd = I.held[owner];
     I.reg_free_top--;
     I.rg_start[r] = (int32_t)start;
     I.rg_len[r] = (int32_t)len;
     I.rg_owner[r] = owner;
     I.rg_next[r] = -1;
-    if (I.reg_cnt[owner] == 0) I.reg_head[owner] = r; else I.rg_next[I.reg_tail[owner]] = r;
+    if (cnt == 0) I.reg_head[owner] = r; else I.rg_next[tail] = r;
     I.reg_tail[owner] = r;
-    I.reg_cnt[owner]++;
-    I.held[owner] += (int32_t)len;
+    I.reg_cnt[owner] = cnt + 1;
+    I.held[owner] = hd + (int32_t)len;
   }
   WSYNC();
   return r;
@@ -698,13 +726,17 @@ EDEVNI void kvc_remove_slot(Inst& I, int32_t hosted) {
 }
 
 // release (kvc.hpp:165-217)
+// release (kvc.hpp:165-217). The request's own fields are loaded once up
+// front; nothing below changes them except this function's final stores.
 EDEVNI void kvc_release(Inst& I, int32_t id) {
-  const bool had = I.reg_cnt[id] > 0;
-  if (!had && !(I.flags[id] & F_HAS_RESERVED) && !(I.flags[id] & F_HAS_SLOT)) {
+  const int32_t cnt = I.reg_cnt[id], head = I.reg_head[id], rsv = I.reserved[id], wr = I.written[id];
+  const uint8_t f0 = I.flags[id];
+  const bool had = cnt > 0;
+  if (!had && !(f0 & F_HAS_RESERVED) && !(f0 & F_HAS_SLOT)) {
     set_error(I, ERR_RELEASE_UNKNOWN, id, 0);
     return;
   }
-  kvc_remove_slot(I, id);
+  if (f0 & F_HAS_SLOT) kvc_remove_slot(I, id);
   if (had) {
     // promoted slots (host == id), in slot order
     int32_t np = 0;
@@ -718,10 +750,13 @@ EDEVNI void kvc_release(Inst& I, int32_t id) {
     WSYNC();
     // drop the host's regions from the address order
     Tok freed = 0;
-    for (int32_t r = I.reg_head[id]; r >= 0; r = I.rg_next[r]) {
-      addr_remove_region(I, r);
-      freed += I.rg_len[r];
-      LANE0(I.reg_free[I.reg_free_top++] = r);
+    for (int32_t r = head; r >= 0;) {
+      const int32_t st = I.rg_start[r], ln = I.rg_len[r], nx = I.rg_next[r];
+      const int32_t pos = addr_lower(I, st);
+      arr_erase(I.addr, I.n_regions, pos, 1);
+      LANE0(I.n_regions--; I.reg_free[I.reg_free_top++] = r);
+      freed += ln;
+      r = nx;
     }
     LANE0(I.reg_cnt[id] = 0; I.reg_head[id] = -1; I.reg_tail[id] = -1; I.held[id] = 0);
     for (int32_t k = 0; k < np; ++k) {
@@ -748,8 +783,10 @@ EDEVNI void kvc_release(Inst& I, int32_t id) {
     }
     LANE0(I.free_total += freed);
   }
-  kvc_release_reserved(I, id);
-  LANE0(I.written_total -= I.written[id]; I.written[id] = 0);
+  // release_reserved (kvc.hpp:152-159) and the written count (kvc.hpp:92-101)
+  LANE0(if (f0 & F_HAS_RESERVED) { I.reserved_used -= rsv; I.reserved[id] = 0; }
+        I.flags[id] = (uint8_t)(f0 & ~(F_HAS_RESERVED | F_HAS_SLOT));
+        I.written_total -= wr; I.written[id] = 0);
 }
 
 // ------------------------------------------------------------------------
@@ -766,20 +803,22 @@ EDEV bool gkey_less(const Inst& I, int32_t a, int32_t b) {
   return I.gr_seq[a] < I.gr_seq[b];
 }
 EDEV int32_t gq_upper(const Inst& I, int32_t g) {  // upper_bound by key
-  int32_t lo = 0, hi = I.G;
-  while (lo < hi) {
-    const int32_t mid = (lo + hi) >> 1;
-    if (gkey_less(I, g, I.gq[mid])) hi = mid; else lo = mid + 1;
-  }
-  return lo;
+  const uint64_t hg = gkey_hi(I, g), sg = I.gr_seq[g];
+  const int32_t* gq = I.gq;
+  return warp_search(I.G, [&](int32_t p) {
+    const int32_t x = gq[p];
+    const uint64_t hx = gkey_hi(I, x);
+    return hg != hx ? hg < hx : sg < I.gr_seq[x];
+  });
 }
 EDEV int32_t gq_pos(const Inst& I, int32_t g) {  // position of g (keys unique)
-  int32_t lo = 0, hi = I.G;
-  while (lo < hi) {
-    const int32_t mid = (lo + hi) >> 1;
-    if (gkey_less(I, I.gq[mid], g)) lo = mid + 1; else hi = mid;
-  }
-  return lo;
+  const uint64_t hg = gkey_hi(I, g), sg = I.gr_seq[g];
+  const int32_t* gq = I.gq;
+  return warp_search(I.G, [&](int32_t p) {
+    const int32_t x = gq[p];
+    const uint64_t hx = gkey_hi(I, x);
+    return !(hx != hg ? hx < hg : I.gr_seq[x] < sg);
+  });
 }
 EDEV void gq_rekey(Inst& I, int32_t g, double now) {  // place(): make_key (queues.hpp:187-193), lane 0
   if (I.ordered) {
@@ -813,20 +852,33 @@ EDEV Tok member_demand(const Inst& I, int32_t id) {  // gt_member_demand (engine
 // group_insert_gt (queues.hpp:141-166). A waiting member's demand cannot
 // change while it waits (its holdings and progress are frozen), so it is
 // cached at join time and summed per group.
-EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline, int32_t occ, double now) {
-  const Tok d = member_demand(I, id);
+EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline, int32_t occ, double now,
+                            Tok d) {
   LANE0(I.dem[id] = (int32_t)d; I.gt_next[id] = -1);
   if (I.grouping) {
     const int32_t g = rl_find(I, padded);
     if (g >= 0) {
       const int32_t pos = gq_pos(I, g);
       arr_erase(I.gq, I.G, pos, 1);
-      LANE0(I.G--;
-            if (I.gr_cnt[g] == 0) I.gr_head[g] = id; else I.gt_next[I.gr_tail[g]] = id;
-            I.gr_tail[g] = id; I.gr_cnt[g]++; I.gr_dem[g] += d;
-            I.gr_mindl[g] = dmin(I.gr_mindl[g], deadline);
-            I.gr_maxocc[g] = (int32_t)tmax(I.gr_maxocc[g], occ);
-            gq_rekey(I, g, now));
+      if (LANE == 0) {
+        const int32_t cnt = I.gr_cnt[g], tail = I.gr_tail[g], mo = I.gr_maxocc[g];
+        const int64_t gd = I.gr_dem[g];
+        const double md = I.gr_mindl[g];
+        I.G--;
+        if (cnt == 0) I.gr_head[g] = id; else I.gt_next[tail] = id;
+        I.gr_tail[g] = id;
+        I.gr_cnt[g] = cnt + 1;
+        I.gr_dem[g] = gd + d;
+        const double nmd = dmin(md, deadline);
+        const int32_t nmo = (int32_t)tmax(mo, occ);
+        I.gr_mindl[g] = nmd;
+        I.gr_maxocc[g] = nmo;
+        if (I.ordered) {  // place(): make_key (queues.hpp:187-193)
+          I.gr_db[g] = bucket_d(I, dmax(0.0, nmd - now));
+          I.gr_kb[g] = bucket_k(I, nmo);
+        }
+      }
+      WSYNC();
       const int32_t p2 = gq_upper(I, g);
       arr_insert(I.gq, I.G, p2, g);
       LANE0(I.G++);
@@ -839,23 +891,35 @@ EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline
   LANE0(I.grp_free_top--;
         I.gr_id[g] = I.next_group_id++; I.gr_rl[g] = padded; I.gr_head[g] = id; I.gr_tail[g] = id;
         I.gr_cnt[g] = 1; I.gr_dem[g] = d; I.gr_formed[g] = now; I.gr_mindl[g] = deadline;
-        I.gr_maxocc[g] = occ; I.gr_seq[g] = I.gt_next_seq++; I.gr_db[g] = 0; I.gr_kb[g] = 0;
-        gq_rekey(I, g, now); rl_set(I, padded, g));
+        I.gr_maxocc[g] = occ; I.gr_seq[g] = I.gt_next_seq++;
+        I.gr_db[g] = I.ordered ? bucket_d(I, dmax(0.0, deadline - now)) : 0;
+        I.gr_kb[g] = I.ordered ? bucket_k(I, occ) : 0;
+        rl_set(I, padded, g));
   const int32_t p2 = gq_upper(I, g);
   arr_insert(I.gq, I.G, p2, g);
   LANE0(I.G++);
+}
+EDEV void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline, int32_t occ, double now) {
+  group_insert_gt(I, id, padded, deadline, occ, now, member_demand(I, id));
 }
 
 // ------------------------------------------------------------------------
 // engine (engine.hpp:216-994), econoserve family
 // ------------------------------------------------------------------------
-EDEV void begin_gt_run(Inst& I, int32_t id, bool hosted) {  // engine.hpp:350-363 (lane 0)
-  I.flags[id] = hosted ? (I.flags[id] | F_HOSTED) : (I.flags[id] & ~F_HOSTED);
-  I.allowance[id] = I.generated[id] + I.padded[id];
-  I.gen_epoch[id] = I.generated[id];
-  const double wait = dmax(0.0, I.clock - I.last_enq[id]);
-  if (I.flags[id] & F_WAS_PREEMPTED) I.preempt_t[id] += wait; else I.waiting[id] += wait;
-  I.flags[id] &= ~F_WAS_PREEMPTED;
+// begin_gt_run (engine.hpp:350-363), lane 0. Every field is loaded before
+// the first store: stores through the SoA pointers may alias later loads as
+// far as the compiler knows, so interleaving them would serialise one
+// memory round trip per field.
+EDEV void begin_gt_run(Inst& I, int32_t id, bool hosted) {
+  const uint8_t f = I.flags[id];
+  const int32_t gen = I.generated[id], pad = I.padded[id];
+  const double le = I.last_enq[id], wt = I.waiting[id], pt = I.preempt_t[id];
+  const double wait = dmax(0.0, I.clock - le);
+  uint8_t nf = hosted ? (uint8_t)(f | F_HOSTED) : (uint8_t)(f & ~F_HOSTED);
+  I.flags[id] = (uint8_t)(nf & ~F_WAS_PREEMPTED);
+  I.allowance[id] = gen + pad;
+  I.gen_epoch[id] = gen;
+  if (f & F_WAS_PREEMPTED) I.preempt_t[id] = pt + wait; else I.waiting[id] = wt + wait;
   I.state[id] = ST_RUNNING;
   I.run[I.R++] = id;
   I.adm[I.n_adm++] = id;
@@ -955,28 +1019,64 @@ EDEV int32_t cls_take(Inst& I, int b, int p, int32_t k, int32_t* out, int32_t no
   return nout + k;
 }
 
-EDEVNI void dispatch_pts(Inst& I, int32_t npt) {  // dispatch_pt_reserved / _common (engine.hpp:365-381)
-  for (int32_t i = 0; i < npt; ++i) {
-    const int32_t id = I.tmp_a[i];
-    const Tok p = I.prompt[id];
-    if (!kvc_draw_reserved(I, id, p)) { set_error(I, ERR_RESERVED_DRAW, id, 0); return; }
-    if (LANE == 0) {
+// dispatch_pt_reserved / _common (engine.hpp:365-381) for the npt selected
+// PTs in I.tmp_a, lane-parallel: every lane loads its PT's fields at once,
+// a prefix sum of the prompts replays draw_reserved's sequential capacity
+// test (kvc.hpp:144-150) and the first failing draw is the error, exactly
+// where the sequential loop would stop. Event slots, ptiter and adm
+// positions are assigned in selection order.
+EDEVNI void dispatch_pts(Inst& I, int32_t npt) {
+  for (int32_t base = 0; base < npt; base += W) {
+    const int32_t j = base + LANE;
+    const bool on = j < npt;
+    int32_t id = 0, p = 0, rsv = 0;
+    uint8_t f = 0;
+    double arr = 0.0, wt = 0.0;
+    if (on) {
+      id = I.tmp_a[j];
+      p = I.prompt[id];
+      rsv = I.reserved[id];
+      f = I.flags[id];
+      arr = I.arrival[id];
+      wt = I.waiting[id];
+    }
+    Tok incl = on ? p : 0;  // inclusive prefix of prompt tokens within the chunk
+    for (int o = 1; o < W; o <<= 1) {
+      const Tok y = shfl(incl, LANE - o >= 0 ? LANE - o : 0);
+      if (LANE >= o) incl += y;
+    }
+    const Tok used0 = I.reserved_used;
+    const bool fits = !on || used0 + incl <= I.reserve_cap;
+    const unsigned bad = BALLOT(!fits);
+    const int32_t cnt = bad ? FFS(bad) : (npt - base < W ? npt - base : W);
+    if (on && LANE < cnt) {
+      I.reserved[id] = rsv + p;
+      I.flags[id] = (uint8_t)(f | F_HAS_RESERVED);
       I.state[id] = ST_RUNNING;
       I.dispatch_t[id] = I.clock;
-      I.waiting[id] += I.clock - I.arrival[id];
-      I.ptiter_id[I.n_ptiter] = id;
-      I.ptiter_tok[I.n_ptiter] = (int32_t)p;
-      I.n_ptiter++;
-      I.adm[I.n_adm++] = id;
-      I.pts_admitted_iter++;
-      I.pt_dispatched++;
+      I.waiting[id] = wt + (I.clock - arr);
+      I.ptiter_id[I.n_ptiter + LANE] = id;
+      I.ptiter_tok[I.n_ptiter + LANE] = p;
+      I.adm[I.n_adm + LANE] = id;
+      if (I.record_events && I.ev_n + LANE < I.ev_cap) {
+        EconoEvent& e = I.ev[I.ev_n + LANE];
+        e.iter = I.iter; e.clock = I.clock; e.kind = ECONO_EV_PT_DISPATCH; e.id = id; e.a = 0; e.b = 0;
+      }
     }
-    logev(I, ECONO_EV_PT_DISPATCH, id, 0, 0);
+    const Tok took = shfl(incl, cnt > 0 ? cnt - 1 : 0);
+    const int32_t bad_id = shfl(id, cnt < W ? cnt : 0);
     WSYNC();
+    LANE0(I.reserved_used = used0 + (cnt > 0 ? took : 0); I.n_ptiter += cnt; I.n_adm += cnt;
+          I.pts_admitted_iter += cnt; I.pt_dispatched += cnt; I.ev_total += cnt;
+          if (I.record_events) I.ev_n += cnt);
+    if (bad) { set_error(I, ERR_RESERVED_DRAW, bad_id, 0); return; }
   }
 }
 
-EDEVNI void schedule_gt_member(Inst& I, int32_t id) {  // engine.hpp:327-348
+// schedule_gt_member (engine.hpp:327-348): exact allocation, then the
+// reserve release (kvc.hpp:152-159), written/occupied accounting and
+// begin_gt_run in one lane-0 block whose loads all precede its stores.
+EDEVNI void schedule_gt_member(Inst& I, int32_t id) {
   const Tok prompt = I.prompt[id], gen = I.generated[id], pad = I.padded[id];
   const Tok target = block_round(prompt + gen + pad, I.block);
   const Tok held = I.held[id];
@@ -986,15 +1086,30 @@ EDEVNI void schedule_gt_member(Inst& I, int32_t id) {  // engine.hpp:327-348
   else if (held < target) ok = kvc_alloc_region(I, id, target - held);
   if (I.error) return;
   if (!ok) { set_error(I, ERR_ALLOC_FAIL, id, 0); return; }
-  kvc_release_reserved(I, id);
   if (LANE == 0) {
-    const Tok cur = I.written[id];
-    if (cur < resident) kvc_add_written(I, id, resident - cur);
+    const uint8_t f = I.flags[id];
+    const int32_t rsv = I.reserved[id], cur = I.written[id];
+    const double le = I.last_enq[id], wt = I.waiting[id], pt = I.preempt_t[id];
+    if (f & F_HAS_RESERVED) {
+      I.reserved_used -= rsv;
+      I.reserved[id] = 0;
+    }
+    if (cur < resident) {
+      I.written[id] = (int32_t)resident;
+      I.written_total += resident - cur;
+    }
     I.occupied[id] = (int32_t)resident;
-    begin_gt_run(I, id, false);
+    const double wait = dmax(0.0, I.clock - le);
+    I.flags[id] = (uint8_t)(f & ~(F_HAS_RESERVED | F_HOSTED | F_WAS_PREEMPTED));
+    I.allowance[id] = (int32_t)(gen + pad);
+    I.gen_epoch[id] = (int32_t)gen;
+    if (f & F_WAS_PREEMPTED) I.preempt_t[id] = pt + wait; else I.waiting[id] = wt + wait;
+    I.state[id] = ST_RUNNING;
+    I.run[I.R++] = id;
+    I.adm[I.n_adm++] = id;
     I.gt_scheduled++;
   }
-  logev(I, ECONO_EV_GT_SCHEDULE, id, I.padded[id], 0);
+  logev(I, ECONO_EV_GT_SCHEDULE, id, pad, 0);
   WSYNC();
 }
 
@@ -1183,35 +1298,37 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     int32_t gi = 0;
     while (gi < I.G) {
       const int32_t g = I.gq[gi];
+      const Tok total = I.gr_dem[g];  // the group's fields load together
+      const int32_t cnt = I.gr_cnt[g], head = I.gr_head[g], grl = I.gr_rl[g];
       LANE0(I.exam_count++);
-      const Tok total = I.gr_dem[g];
-      if (nsel + I.gr_cnt[g] > I.sel_cap && total <= remaining) { set_error(I, ERR_TABLE_OVERFLOW, g, 8); return; }
+      if (nsel + cnt > I.sel_cap && total <= remaining) { set_error(I, ERR_TABLE_OVERFLOW, g, 8); return; }
       if (total <= remaining) {
         remaining -= total;
         if (LANE == 0) {
           I.selg_start[nselg] = nsel;
-          I.selg_rl[nselg] = I.gr_rl[g];
-          int32_t m = I.gr_head[g];
-          for (int32_t i = 0; i < I.gr_cnt[g]; ++i) { I.sel_ids[nsel + i] = m; m = I.gt_next[m]; }
+          I.selg_rl[nselg] = grl;
+          int32_t m = head;
+          for (int32_t i = 0; i < cnt; ++i) { I.sel_ids[nsel + i] = m; m = I.gt_next[m]; }
         }
         WSYNC();
-        nsel += I.gr_cnt[g];
+        nsel += cnt;
         nselg++;
         whole++;
         gi++;
         continue;
       }
-      int32_t taken = 0, m = I.gr_head[g];
+      int32_t taken = 0, m = head;
       Tok pd = 0;
       if (LANE == 0) {
         while (m >= 0) {
           const Tok d = I.dem[m];
+          const int32_t nx = I.gt_next[m];
           I.exam_count++;
           if (pd + d > remaining) break;
           pd += d;
           I.sel_ids[nsel + taken] = m;
           taken++;
-          m = I.gt_next[m];
+          m = nx;
         }
       }
       taken = shfl(taken, 0);
@@ -1454,12 +1571,15 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   for (int32_t i = LANE; i < I.n_ptiter; i += W) {
     const int32_t id = I.ptiter_id[i];
     const int32_t tk = I.ptiter_tok[i];
-    I.exec_t[id] += dt;
-    I.prefill_done[id] += tk;
-    I.written[id] += tk;
-    I.occupied[id] += tk;
+    const double e = I.exec_t[id];
+    const int32_t pd = I.prefill_done[id] + tk, wr = I.written[id], oc = I.occupied[id], pr = I.prompt[id];
+    const uint8_t f = I.flags[id];
+    I.exec_t[id] = e + dt;
+    I.prefill_done[id] = pd;
+    I.written[id] = wr + tk;
+    I.occupied[id] = oc + tk;
     wsum_pt += tk;
-    if (I.prefill_done[id] >= I.prompt[id]) I.flags[id] |= F_PREFILL_FIN;
+    if (pd >= pr) I.flags[id] = (uint8_t)(f | F_PREFILL_FIN);
   }
   wsum_pt = wsum(wsum_pt);
   // every running GT writes exactly one token this iteration
@@ -1525,11 +1645,20 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   // prefill transitions (engine.hpp:794-809)
   for (int32_t i = 0; i < I.n_ptiter; ++i) {
     const int32_t id = I.ptiter_id[i];
-    if (!(I.flags[id] & F_PREFILL_FIN)) continue;
-    LANE0(I.flags[id] &= ~F_PREFILL_FIN);
-    if (I.state[id] != ST_RUNNING) continue;
+    const uint8_t f = I.flags[id];
+    const uint8_t st = I.state[id];
+    const int32_t pad = I.padded[id], oc = I.occupied[id], pr = I.prompt[id], gen = I.generated[id];
+    const int32_t hd = I.held[id];
+    const double slo = I.slo[id];
+    if (!(f & F_PREFILL_FIN)) continue;
+    WSYNC();
+    LANE0(I.flags[id] = (uint8_t)(f & ~F_PREFILL_FIN));
+    if (st != ST_RUNNING) continue;
     LANE0(I.state[id] = ST_WAITING_GT; I.last_enq[id] = I.clock);
-    group_insert_gt(I, id, I.padded[id], I.slo[id], I.occupied[id], I.clock);
+    // gt_member_demand (engine.hpp:238-247) from the fields loaded above
+    const Tok tgt = block_round((Tok)pr + gen + pad, I.block);
+    const Tok dl = tgt - hd;
+    group_insert_gt(I, id, pad, slo, oc, I.clock, dl > 0 ? block_round(dl, I.block) : 0);
     logev(I, ECONO_EV_PREFILL_DONE, id, 0, 0);
     WSYNC();
     if (I.error) return;
@@ -1666,13 +1795,32 @@ EDEV int64_t step_event_bound(const Inst& I) {
 // a span of them is replayed with the same sequential FP adds (never k*dt).
 // ------------------------------------------------------------------------
 EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
-  if (I.R == 0 || I.n_ptiter != 0 || I.n_adm != 0 || budget <= 0) return 0;
-  if (I.arrival_cursor < I.n && I.arrival[I.arrival_cursor] <= I.clock + 1e-12) return 0;
-  if (I.free_total > 0 && I.G > 0) {  // queues.hpp:220-263 would take >= 1 member
-    const int32_t g = I.gq[0];
-    if (I.gr_dem[g] <= I.free_total || I.dem[I.gr_head[g]] <= I.free_total) return 0;
+  const int32_t R = I.R;
+  if (R == 0 || I.n_ptiter != 0 || I.n_adm != 0 || budget <= 0) return 0;
+  // The independent probes are issued together (three dependent levels in
+  // all): the next arrival, the GT queue head, and the running requests.
+  const bool has_arr = I.arrival_cursor < I.n;
+  const Tok free_tok = I.free_total;
+  const bool gt_check = free_tok > 0 && I.G > 0;
+  const double ta = has_arr ? I.arrival[I.arrival_cursor] : 0.0;
+  const int32_t g = gt_check ? I.gq[0] : 0;
+  const int32_t id0 = LANE < R ? I.run[LANE] : -1;
+  int64_t gd = 0;
+  int32_t gh = 0;
+  if (gt_check) {
+    gd = I.gr_dem[g];
+    gh = I.gr_head[g];
   }
-  const Tok C0 = tmin(I.tfs - (Tok)I.R, I.reserve_cap - I.reserved_used);
+  int64_t kev = INT64_MAX;
+  if (id0 >= 0) {
+    const int32_t tr = I.true_rl[id0], al = I.allowance[id0], ge = I.generated[id0];
+    kev = (int64_t)(tr < al ? tr : al) - ge;
+  }
+  if (has_arr && ta <= I.clock + 1e-12) return 0;
+  if (gt_check) {  // queues.hpp:220-263 would take >= 1 member
+    if (gd <= free_tok || I.dem[gh] <= free_tok) return 0;
+  }
+  const Tok C0 = tmin(I.tfs - (Tok)R, I.reserve_cap - I.reserved_used);
   if (C0 >= 1 && I.pt_count > 0 && C0 >= I.pt_min_lb) {  // queues.hpp:279-299 would take a PT
     bool fit = false;
     if (I.ordered) {
@@ -1684,8 +1832,7 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
     LANE0(I.pt_min_lb = C0 + 1);
   }
   // first decode-side event: completion / under-prediction / slot deadline
-  int64_t kev = INT64_MAX;
-  for (int32_t i = LANE; i < I.R; i += W) {
+  for (int32_t i = W + LANE; i < R; i += W) {
     const int32_t id = I.run[i];
     const int64_t lim = I.true_rl[id] < I.allowance[id] ? I.true_rl[id] : I.allowance[id];
     const int64_t e = lim - I.generated[id];
