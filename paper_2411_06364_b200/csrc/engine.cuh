@@ -81,6 +81,15 @@ static inline uint64_t umulhi64(uint64_t a, uint64_t b) {
 #else
 #define PROF_NOW() ((int64_t)0)
 #endif
+// Per-phase cycle counters (prof[3], [6..10], [13..15]) cost ~10 instructions
+// each; they are compiled in only with -DECONO_PROF_PHASES (tools/probe_scale).
+#ifdef ECONO_PROF_PHASES
+#define PHASE_NOW() PROF_NOW()
+#define PHASE_ADD(k, v) LANE0(I.prof[k] += (v))
+#else
+#define PHASE_NOW() ((int64_t)0)
+#define PHASE_ADD(k, v) ((void)0)
+#endif
 
 #define LANE0(stmt) \
   do {              \
@@ -133,7 +142,9 @@ struct Inst {
   // device cycle counters (econo_batch_debug): [0] quiet-span tests [1] quiet
   // replays [2] normal steps [4] spans [5] normal-step count; normal-step
   // phases [6] ingest [7] GT select+schedule [8] pipelining [9] PT batching
-  // [10] execute_iteration; [11] launch total [12] launches.
+  // [10] execute_iteration; [11] launch total [12] launches; inside
+  // execute_iteration [3] running-set pass + completions [13] prefill + sample
+  // [14] prefill transitions [15] under-prediction, slot deadlines, tail.
   int64_t prof[16];
   double agg_written, agg_allocated;
   int64_t agg_fs, agg_tfs_hits, agg_pt_iters;
@@ -177,7 +188,18 @@ struct Inst {
 // ------------------------------------------------------------------------
 // scalar helpers (common.hpp:26-35; std::min/max semantics kept for doubles)
 // ------------------------------------------------------------------------
-EDEV Tok block_round(Tok t, Tok b) { return t <= 0 ? 0 : (t + b - 1) / b * b; }
+// block_round (common.hpp:26-29); power-of-two blocks (the usual case) take
+// a mask instead of a 64-bit division.
+EDEV Tok block_round(Tok t, Tok b) {
+  if (t <= 0) return 0;
+  if ((b & (b - 1)) == 0) return (t + b - 1) & ~(b - 1);
+  return (t + b - 1) / b * b;
+}
+// a / b for nonnegative a, positive b: 32-bit division when both fit.
+EDEV Tok udiv(Tok a, Tok b) {
+  if (((uint64_t)a | (uint64_t)b) < (1ULL << 32)) return (Tok)((uint32_t)a / (uint32_t)b);
+  return a / b;
+}
 EDEV Tok ceil_tokens(double v) { return (Tok)ceil(v - 1e-9); }
 EDEV double dmax(double a, double b) { return (a < b) ? b : a; }
 EDEV double dmin(double a, double b) { return (b < a) ? b : a; }
@@ -1291,7 +1313,7 @@ EDEV bool slot_fits(const Inst& I, int32_t host, int32_t abs, int32_t len) {
 
 EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
   // ---- select_gt_groups (queues.hpp:220-263) ----
-  const int64_t tp0 = PROF_NOW();
+  const int64_t tp0 = PHASE_NOW();
   int32_t nsel = 0, nselg = 0, whole = 0;
   if (I.free_total > 0) {
     Tok remaining = I.free_total;
@@ -1362,8 +1384,8 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     if (I.error) return;
   }
 
-  const int64_t tp1 = PROF_NOW();
-  LANE0(I.prof[7] += tp1 - tp0);
+  const int64_t tp1 = PHASE_NOW();
+  PHASE_ADD(7, tp1 - tp0);
   // ---- KVC pipelining (econoserve-full, engine.hpp:273-297) ----
   if (I.full && nselg > 0) {
     int32_t nm = 0;  // host members flattened into tmp_b/tmp_c, group bounds in tmp_a
@@ -1414,8 +1436,8 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     }
   }
 
-  const int64_t tp2 = PROF_NOW();
-  LANE0(I.prof[8] += tp2 - tp1);
+  const int64_t tp2 = PHASE_NOW();
+  PHASE_ADD(8, tp2 - tp1);
   // ---- PT batching (engine.hpp:299-324, queues.hpp:279-299) ----
   const Tok tfs_rem = I.tfs - (Tok)I.R;
   const Tok rfree = I.reserve_cap - I.reserved_used;
@@ -1445,7 +1467,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
             const int p = bm_prev(I, b, x);
             if (p < 1) break;
             const int32_t cnt = I.cls_cnt[cls_of(I, b, p)];
-            const Tok fit = C / p;
+            const Tok fit = udiv(C, p);
             const int32_t k = (int32_t)(fit < cnt ? fit : cnt);
             npt = cls_take(I, b, p, k, I.tmp_a, npt);
             C -= (Tok)k * p;
@@ -1483,7 +1505,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     }
   }
   dispatch_pts(I, npt);
-  LANE0(I.prof[9] += PROF_NOW() - tp2);
+  PHASE_ADD(9, PHASE_NOW() - tp2);
 }
 
 EDEVNI void vacate_slot(Inst& I, int32_t id, bool* rehomed) {  // engine.hpp:888-902
@@ -1559,6 +1581,7 @@ EDEV void run_compact(Inst& I) {
 }
 
 EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
+  const int64_t tx0 = PHASE_NOW();
   const double dt = iteration_time(I, fs) + 0.0;
   LANE0(I.clock += dt; I.iter++);
   const double sched = (double)I.exam_count * I.sched_cost;
@@ -1604,6 +1627,8 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   // another running request's progress, so it may precede the next chunk's
   // decode. Under-prediction candidates (generated >= allowance < true_rl)
   // are collected here in running order; completed requests never qualify.
+  const int64_t tx1 = PHASE_NOW();
+  PHASE_ADD(13, tx1 - tx0);
   int32_t completed_now = 0, npre = 0;
   const int32_t R0 = I.R;
   for (int32_t base = 0; base < R0; base += W) {
@@ -1642,6 +1667,8 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     }
   }
   if (completed_now) run_compact(I);
+  const int64_t tx2 = PHASE_NOW();
+  PHASE_ADD(3, tx2 - tx1);
   // prefill transitions (engine.hpp:794-809)
   for (int32_t i = 0; i < I.n_ptiter; ++i) {
     const int32_t id = I.ptiter_id[i];
@@ -1663,6 +1690,8 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     WSYNC();
     if (I.error) return;
   }
+  const int64_t tx3 = PHASE_NOW();
+  PHASE_ADD(14, tx3 - tx2);
   // under-prediction (engine.hpp:812-817): candidates fixed up front (above), handled in order
   for (int32_t k = 0; k < npre; ++k) {
     const int32_t id = I.tmp_a[k];
@@ -1718,6 +1747,9 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     I.exam_count = 0;
     I.pts_admitted_iter = 0;
     I.pt_admittable = 0;
+#ifdef ECONO_PROF_PHASES
+    I.prof[15] += PROF_NOW() - tx3;
+#endif
   }
   WSYNC();
 }
@@ -2004,17 +2036,17 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
 }
 
 EDEVNI void engine_step(Inst& I) {  // Engine::step (engine.hpp:104-116)
-  const int64_t t0 = PROF_NOW();
+  const int64_t t0 = PHASE_NOW();
   ingest(I);
-  LANE0(I.prof[6] += PROF_NOW() - t0);
+  PHASE_ADD(6, PHASE_NOW() - t0);
   form_econoserve(I);
   if (I.error) return;
-  const int64_t t1 = PROF_NOW();
+  const int64_t t1 = PHASE_NOW();
   Tok fs = 0;
   for (int32_t i = LANE; i < I.n_ptiter; i += W) fs += I.ptiter_tok[i];
   fs = wsum(fs) + I.R;
   if (fs == 0) handle_idle(I); else execute_iteration(I, fs);
-  LANE0(I.prof[10] += PROF_NOW() - t1);
+  PHASE_ADD(10, PHASE_NOW() - t1);
   LANE0(I.steps++);
 }
 

@@ -15,8 +15,8 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 from paper_2411_06364_b200.engine import Batch, generate_trace  # noqa: E402
 
-NAMES = ["test", "replay", "normal", "-", "spans", "nsteps", "ingest", "gtsel", "plan", "pt", "exec",
-         "launch", "launches"]
+NAMES = ["test", "replay", "normal", "x_runpass", "spans", "nsteps", "ingest", "gtsel", "plan", "pt", "exec",
+         "launch", "launches", "x_prefill", "x_transit", "x_tail"]
 
 
 def run(traces, iters, launches, warm=3, lanes=0):
