@@ -258,6 +258,15 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* n, 
  * max_steps steps on `stream` (a cudaStream_t, NULL = the handle's stream).
  * Asynchronous: no host synchronisation. */
 int econo_batch_launch(econo_batch* b, int64_t max_steps, void* stream);
+/* Grid-wide ingest of the arrivals every instance would admit at the start of
+ * its next step (ingest_arrivals, engine.hpp:216-235): the same class lists,
+ * bitmaps and counters the in-kernel ingest builds, produced for large bursts
+ * by a stable radix sort of the batch by PT class instead of one warp per
+ * instance. Semantically a no-op reordering (it is the first part of the
+ * next step, run early); applies to ordered-queue policies with event
+ * recording off and batches of at least ECONO_BULK_INGEST_MIN (env, default
+ * 32768) arrivals; other instances ingest in-kernel as usual. Synchronous. */
+int econo_batch_ingest(econo_batch* b, char* err, size_t errlen);
 int econo_batch_sync(econo_batch* b, char* err, size_t errlen);
 int econo_batch_scalars(econo_batch* b, EconoScalars* out /* n_inst entries */);
 int econo_batch_engine(econo_batch* b, int32_t i, econo_engine** out); /* borrowed view */

@@ -1946,9 +1946,10 @@ EHD double fp_repeat_add(double x, double d, int64_t k) {
     }
     uint64_t X = (xb & ((1ULL << 52) - 1)) | (1ULL << 52);
     const uint64_t top = (1ULL << 53) - 1;
-    if (cmp == 0 && ((X + q) & 1)) {  // first tie step from an odd X
-      if (X + q + 1 > top) { x = x + d; --k; continue; }
-      X += q + 1;
+    if (cmp == 0) {  // first tie step: round to the even neighbour, X is even afterwards
+      const uint64_t c0 = (X + q) & 1;
+      if (X + q + c0 > top) { x = x + d; --k; continue; }
+      X += q + c0;
       --k;
       if (k == 0) { x = dfrom(((uint64_t)ex << 52) | (X & ((1ULL << 52) - 1))); break; }
     }

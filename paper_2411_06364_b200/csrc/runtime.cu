@@ -383,6 +383,231 @@ __global__ void k_engine_records(const Inst* inst, EconoRecord* out) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk ingest of a large arrival batch, grid-wide (econo_batch_ingest).
+// ingest_arrivals (engine.hpp:216-235) appends every due arrival to its PT
+// class (deadline bucket, prompt) in id order. For a burst that is a stable
+// group-by over up to n arrivals: keys (class) are sorted by an LSD radix
+// sort (8-bit digits, 4096-key tiles, stable in-tile ranks from warp
+// match_any), then each class segment is spliced onto its class list.
+// ---------------------------------------------------------------------------
+struct BulkJob {
+  int32_t inst, tiles;
+  int64_t first, k, off, hoff;   // arrivals [first, first+k); key offset; histogram offset
+  unsigned long long minp;       // min prompt of the batch
+  unsigned long long bcnt[ECONO_MAX_BOUNDS + 2];
+};
+constexpr int kBulkTile = 4096;
+
+__global__ void __launch_bounds__(256) k_bulk_keys(const Inst* insts, BulkJob* jobs, uint32_t* key, uint32_t* val) {
+  BulkJob& J = jobs[blockIdx.y];
+  if ((int)blockIdx.x >= J.tiles) return;
+  const Inst& I = insts[J.inst];
+  __shared__ unsigned long long sb[ECONO_MAX_BOUNDS + 2];
+  __shared__ unsigned long long smin;
+  if (threadIdx.x < ECONO_MAX_BOUNDS + 2) sb[threadIdx.x] = 0;
+  if (threadIdx.x == 0) smin = ~0ULL;
+  __syncthreads();
+  const int64_t t0 = (int64_t)blockIdx.x * kBulkTile;
+  unsigned long long mn = ~0ULL;
+  for (int e = threadIdx.x; e < kBulkTile; e += blockDim.x) {
+    const int64_t i = t0 + e;
+    if (i >= J.k) break;
+    const int64_t id = J.first + i;
+    const int b = bucket_d(I, dmax(0.0, I.slo[id] - I.clock));
+    const int32_t p = I.prompt[id];
+    key[J.off + i] = (uint32_t)cls_of(I, b, p);
+    val[J.off + i] = (uint32_t)id;
+    mn = (unsigned long long)p < mn ? (unsigned long long)p : mn;
+    atomicAdd(&sb[b], 1ULL);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, mn, o);
+    mn = x < mn ? x : mn;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMin(&smin, mn);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMin(&J.minp, smin);
+  if (threadIdx.x < ECONO_MAX_BOUNDS + 2 && sb[threadIdx.x]) atomicAdd(&J.bcnt[threadIdx.x], sb[threadIdx.x]);
+}
+
+// Per-tile digit histograms, digit-major: hist[hoff + d * tiles + t].
+__global__ void __launch_bounds__(256) k_radix_hist(const BulkJob* jobs, const uint32_t* key, int shift,
+                                                    uint32_t* hist) {
+  const BulkJob& J = jobs[blockIdx.y];
+  if ((int)blockIdx.x >= J.tiles) return;
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t t0 = (int64_t)blockIdx.x * kBulkTile;
+  for (int e = threadIdx.x; e < kBulkTile && t0 + e < J.k; e += blockDim.x)
+    atomicAdd(&h[(key[J.off + t0 + e] >> shift) & 255], 1u);
+  __syncthreads();
+  hist[J.hoff + (int64_t)threadIdx.x * J.tiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Exclusive scan of one job's 256 x tiles histogram (one CTA per job).
+__global__ void __launch_bounds__(1024) k_radix_scan(const BulkJob* jobs, uint32_t* hist) {
+  const BulkJob& J = jobs[blockIdx.x];
+  const int64_t m = 256LL * J.tiles;
+  uint32_t* h = hist + J.hoff;
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < m; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const uint32_t v = i < m ? h[i] : 0;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t w = ws[threadIdx.x];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (threadIdx.x >= o) w += y;
+      }
+      ws[threadIdx.x] = w;
+    }
+    __syncthreads();
+    const uint32_t wpre = (threadIdx.x >> 5) ? ws[(threadIdx.x >> 5) - 1] : 0;
+    if (i < m) h[i] = carry + wpre + x - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry += wpre + x;
+    __syncthreads();
+  }
+}
+
+// Stable scatter of one tile: each warp ranks its 512 keys in order with
+// match_any, warps are offset by the digit counts of the warps before them.
+__global__ void __launch_bounds__(256) k_radix_scatter(const BulkJob* jobs, const uint32_t* kin, const uint32_t* vin,
+                                                       uint32_t* kout, uint32_t* vout, int shift,
+                                                       const uint32_t* hist) {
+  const BulkJob& J = jobs[blockIdx.y];
+  if ((int)blockIdx.x >= J.tiles) return;
+  __shared__ uint32_t sk[kBulkTile];
+  __shared__ uint32_t cnt[8][256];
+  const int64_t t0 = (int64_t)blockIdx.x * kBulkTile;
+  const int n = (int)(J.k - t0 < kBulkTile ? J.k - t0 : kBulkTile);
+  for (int e = threadIdx.x; e < kBulkTile; e += blockDim.x) sk[e] = e < n ? kin[J.off + t0 + e] : 0;
+  for (int d = threadIdx.x; d < 8 * 256; d += blockDim.x) (&cnt[0][0])[d] = 0;
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t rank[kBulkTile / 256];
+#pragma unroll
+  for (int r = 0; r < kBulkTile / 256; ++r) {
+    const int e = w * (kBulkTile / 8) + r * 32 + lane;
+    const int d = e < n ? (int)((sk[e] >> shift) & 255) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    uint32_t base = 0;
+    if (d >= 0) base = cnt[w][d];
+    __syncwarp();
+    if (d >= 0 && (peers & ((1u << lane) - 1u)) == 0) cnt[w][d] = base + __popc(peers);
+    __syncwarp();
+    rank[r] = base + __popc(peers & ((1u << lane) - 1u));
+  }
+  __syncthreads();
+  {  // exclusive prefix over warps, one thread per digit
+    const int d = threadIdx.x;
+    uint32_t run = 0;
+    for (int ww = 0; ww < 8; ++ww) {
+      const uint32_t c = cnt[ww][d];
+      cnt[ww][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  const uint32_t* hb = hist + J.hoff;
+#pragma unroll
+  for (int r = 0; r < kBulkTile / 256; ++r) {
+    const int e = w * (kBulkTile / 8) + r * 32 + lane;
+    if (e < n) {
+      const uint32_t kv = sk[e];
+      const int d = (int)((kv >> shift) & 255);
+      const int64_t pos = (int64_t)hb[(int64_t)d * J.tiles + blockIdx.x] + cnt[w][d] + rank[r];
+      kout[J.off + pos] = kv;
+      vout[J.off + pos] = vin[J.off + t0 + e];
+    }
+  }
+}
+
+// Class segments of the sorted batch: heads splice onto the old class tail
+// (or become the head) and set the class bitmaps.
+__global__ void __launch_bounds__(256) k_bulk_heads(Inst* insts, const BulkJob* jobs, const uint32_t* key,
+                                                    const uint32_t* val) {
+  const BulkJob& J = jobs[blockIdx.y];
+  if ((int)blockIdx.x >= J.tiles) return;
+  Inst& I = insts[J.inst];
+  const int64_t t0 = (int64_t)blockIdx.x * kBulkTile;
+  for (int e = threadIdx.x; e < kBulkTile && t0 + e < J.k; e += blockDim.x) {
+    const int64_t j = t0 + e;
+    const uint32_t c = key[J.off + j];
+    if (j > 0 && key[J.off + j - 1] == c) continue;
+    const int32_t id = (int32_t)val[J.off + j];
+    const int32_t old_tail = I.cls_tail[c];
+    if (old_tail >= 0) I.pt_next[old_tail] = id; else I.cls_head[c] = id;
+    const int b = (int)(c / (uint32_t)(I.pmax + 1)), p = (int)(c % (uint32_t)(I.pmax + 1));
+    atomicOr(reinterpret_cast<unsigned long long*>(&I.bm1[(int64_t)b * I.bm_words + (p >> 6)]), 1ULL << (p & 63));
+    atomicOr(reinterpret_cast<unsigned long long*>(&I.bm2[(int64_t)b * I.bm_l2 + (p >> 12)]),
+             1ULL << ((p >> 6) & 63));
+  }
+}
+// Links inside segments, new class tails, class counts (warp-aggregated).
+__global__ void __launch_bounds__(256) k_bulk_tails(Inst* insts, const BulkJob* jobs, const uint32_t* key,
+                                                    const uint32_t* val) {
+  const BulkJob& J = jobs[blockIdx.y];
+  if ((int)blockIdx.x >= J.tiles) return;
+  Inst& I = insts[J.inst];
+  const int64_t t0 = (int64_t)blockIdx.x * kBulkTile;
+  for (int e = threadIdx.x; e < kBulkTile; e += blockDim.x) {
+    const int64_t j = t0 + e;
+    const bool in = j < J.k;
+    const uint32_t c = in ? key[J.off + j] : 0xffffffffu;
+    if (in) {
+      const int32_t id = (int32_t)val[J.off + j];
+      const bool tail = j + 1 == J.k || key[J.off + j + 1] != c;
+      I.pt_next[id] = tail ? -1 : (int32_t)val[J.off + j + 1];
+      if (tail) I.cls_tail[c] = id;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, c);
+    if (in && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&I.cls_cnt[c], (int32_t)__popc(peers));
+  }
+}
+// The instance scalars ingest() updates (engine.hpp:216-235).
+__global__ void k_bulk_finish(Inst* insts, const BulkJob* jobs) {
+  const BulkJob& J = jobs[blockIdx.x];
+  if (threadIdx.x != 0) return;
+  Inst& I = insts[J.inst];
+  I.arrival_cursor = J.first + J.k;
+  I.pt_count += (int32_t)J.k;
+  I.ev_total += J.k;
+  if ((int64_t)J.minp < I.pt_min_lb) I.pt_min_lb = (int64_t)J.minp;
+  for (int b = 0; b < I.nbuckets; ++b) I.bcnt[b] += (int32_t)J.bcnt[b];
+}
+// Per instance: the arrivals ingest() would admit at the current clock.
+__global__ void k_bulk_plan(const Inst* insts, int64_t* plan) {
+  const Inst& I = insts[blockIdx.x];
+  if (threadIdx.x != 0) return;
+  int64_t first = I.arrival_cursor, k = 0;
+  if (I.ordered && !I.record_events && !I.error && first < I.n) {
+    const double lim = I.clock + 1e-12;
+    if (I.arrival[first] <= lim) {
+      int64_t lo = first + 1, hi = I.n;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (I.arrival[mid] <= lim) lo = mid + 1; else hi = mid;
+      }
+      k = lo - first;
+    }
+  }
+  plan[2 * blockIdx.x] = first;
+  plan[2 * blockIdx.x + 1] = k;
+}
+
 // Partial sums, grid-wide: block (x, instance) reduces a strided slice of
 // the instance's requests (one pass over ~89 B of SoA per request, HBM-bound)
 // into scr[instance][x][16]; k_partials_finish then folds the slices in a
@@ -1489,6 +1714,98 @@ int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen) 
   if (!rc && dev_d2h(out, d, bytes)) rc = ECONO_ECUDA;
   dev_free(scr);
   dev_free(d);
+  return rc;
+#endif
+}
+
+int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
+#ifdef ECONO_HOSTSIM
+  (void)b; (void)err; (void)errlen;
+  return ECONO_OK;  // the host build ingests inside step()
+#else
+  const int32_t ni = (int32_t)b->inst.size();
+  void* dplan;
+  if (dev_alloc(&dplan, sizeof(int64_t) * 2 * (size_t)ni)) return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
+  k_bulk_plan<<<(unsigned)ni, 32, 0, b->stream>>>(b->d_insts, (int64_t*)dplan);
+  std::vector<int64_t> plan(2 * (size_t)ni);
+  int rc = sync_batch(b, err, errlen);
+  if (!rc && dev_d2h(plan.data(), dplan, sizeof(int64_t) * plan.size())) rc = ECONO_ECUDA;
+  dev_free(dplan);
+  if (rc) return rc;
+  const char* env = getenv("ECONO_BULK_INGEST_MIN");
+  const int64_t thr = env ? atoll(env) : 32768;
+  std::vector<BulkJob> jobs;
+  int bits = 1;
+  for (int32_t i = 0; i < ni; ++i) {
+    const Inst& I = b->inst[(size_t)i].desc;
+    const int64_t k = plan[2 * (size_t)i + 1];
+    const uint64_t ncls = (uint64_t)I.nbuckets * (uint64_t)(I.pmax + 1);
+    if (k < thr || k < 1 || ncls > 0xffffffffULL) continue;
+    BulkJob J;
+    memset(&J, 0, sizeof(J));
+    J.inst = i;
+    J.first = plan[2 * (size_t)i];
+    J.k = k;
+    J.tiles = (int32_t)((k + kBulkTile - 1) / kBulkTile);
+    J.minp = ~0ULL;
+    jobs.push_back(J);
+    while (bits < 32 && (ncls - 1) >> bits) ++bits;
+  }
+  if (jobs.empty()) return ECONO_OK;
+  const int passes = (bits + 7) / 8;
+  const int64_t budget = (int64_t)64 << 20;  // keys per group (4 x 4 B each of temp)
+  void *k0 = nullptr, *k1 = nullptr, *v0 = nullptr, *v1 = nullptr, *dh = nullptr, *dj = nullptr;
+  int64_t cap_keys = 0, cap_hist = 0;
+  for (size_t g0 = 0; g0 < jobs.size() && !rc;) {
+    size_t g1 = g0;
+    int64_t off = 0, hoff = 0;
+    int32_t tmax = 0;
+    while (g1 < jobs.size() && (g1 == g0 || off + jobs[g1].k <= budget)) {
+      jobs[g1].off = off;
+      jobs[g1].hoff = hoff;
+      off += jobs[g1].k;
+      hoff += 256LL * jobs[g1].tiles;
+      tmax = std::max(tmax, jobs[g1].tiles);
+      ++g1;
+    }
+    if (off > cap_keys) {
+      for (void* q : {k0, k1, v0, v1}) dev_free(q);
+      if (dev_alloc(&k0, 4 * (size_t)off) || dev_alloc(&k1, 4 * (size_t)off) || dev_alloc(&v0, 4 * (size_t)off) ||
+          dev_alloc(&v1, 4 * (size_t)off)) {
+        set_err(err, errlen, "bulk ingest allocation failed");
+        rc = ECONO_ECUDA;
+        break;
+      }
+      cap_keys = off;
+    }
+    if (hoff > cap_hist) {
+      dev_free(dh);
+      if (dev_alloc(&dh, 4 * (size_t)hoff)) { set_err(err, errlen, "allocation failed"); rc = ECONO_ECUDA; break; }
+      cap_hist = hoff;
+    }
+    const int32_t nj = (int32_t)(g1 - g0);
+    dev_free(dj);
+    if (dev_alloc(&dj, sizeof(BulkJob) * (size_t)nj)) { set_err(err, errlen, "allocation failed"); rc = ECONO_ECUDA; break; }
+    dev_h2d(dj, jobs.data() + g0, sizeof(BulkJob) * (size_t)nj);
+    const dim3 grid((unsigned)tmax, (unsigned)nj);
+    BulkJob* J = (BulkJob*)dj;
+    uint32_t *kin = (uint32_t*)k0, *kout = (uint32_t*)k1, *vin = (uint32_t*)v0, *vout = (uint32_t*)v1;
+    k_bulk_keys<<<grid, 256, 0, b->stream>>>(b->d_insts, J, kin, vin);
+    for (int pass = 0; pass < passes; ++pass) {
+      k_radix_hist<<<grid, 256, 0, b->stream>>>(J, kin, 8 * pass, (uint32_t*)dh);
+      k_radix_scan<<<(unsigned)nj, 1024, 0, b->stream>>>(J, (uint32_t*)dh);
+      k_radix_scatter<<<grid, 256, 0, b->stream>>>(J, kin, vin, kout, vout, 8 * pass, (const uint32_t*)dh);
+      std::swap(kin, kout);
+      std::swap(vin, vout);
+    }
+    k_bulk_heads<<<grid, 256, 0, b->stream>>>(b->d_insts, J, kin, vin);
+    k_bulk_tails<<<grid, 256, 0, b->stream>>>(b->d_insts, J, kin, vin);
+    k_bulk_finish<<<(unsigned)nj, 32, 0, b->stream>>>(b->d_insts, J);
+    rc = sync_batch(b, err, errlen);
+    if (!rc) rc = cuda_check(err, errlen, "bulk ingest");
+    g0 = g1;
+  }
+  for (void* q : {k0, k1, v0, v1, dh, dj}) dev_free(q);
   return rc;
 #endif
 }

@@ -38,6 +38,10 @@ def test_repeat_add_matches_sequential():
         x = float(rng.choice([0.0, rng.random(), rng.random() * 1e3, rng.random() * 1e-3, rng.random() * 1e6]))
         d = float(rng.choice([rng.random() * 1e-2, rng.random(), rng.random() * 1e-9, 0.005 + rng.random() * 1e-3]))
         cases.append((x, d, int(rng.integers(0, 3000))))
+    for t in range(20000):  # clock / execution_time shapes: dt-like steps from 0 or small starts
+        x = 0.0 if t % 5 == 0 else float(rng.random() * rng.choice([1e-3, 1.0, 10.0, 100.0, 1e5]))
+        d = float(rng.choice([0.005 + rng.integers(1, 200) * 1e-4, rng.random(), rng.random() * 1e-6]))
+        cases.append((x, d, int(rng.integers(1, 400))))
     for _ in range(2000):  # ties: d an odd multiple of half an ulp of x
         e = int(rng.integers(-20, 20))
         x = float(np.ldexp(1.0 + rng.integers(0, 2 ** 20) * 2.0 ** -20, e))
