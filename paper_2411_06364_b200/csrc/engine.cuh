@@ -1997,7 +1997,7 @@ EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double c
     // constant addends: closed-form jumps (fp_repeat_add)
     clock = fp_repeat_add(clock, dt, k);
     aa = fp_repeat_add(aa, af, k);
-    e = fp_repeat_add(e, dt, k);
+    if (my >= 0) e = fp_repeat_add(e, dt, k);  // idle lanes would walk up from 0 binade by binade
     // the written fractions vary per step: W steps at a time, each lane
     // rounds its addend against aw's ulp and the whole ulps are summed in
     // integers; a chunk with a tie or a binade crossing is added sequentially

@@ -26,7 +26,7 @@ SYMBOLS = [
     "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
     "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore", "econo_batch_debug",
     "econo_batch_reports", "econo_batch_jct_prepare", "econo_batch_jct_hist", "econo_batch_jct_percentiles",
-    "econo_jct_key_to_double",
+    "econo_jct_key_to_double", "econo_batch_ingest",
 ]
 
 
@@ -89,6 +89,7 @@ def load(path=None):
     L.econo_batch_restore.argtypes = [vp, cp, sz]
     L.econo_batch_debug.argtypes = [vp, vp]
     L.econo_batch_reports.argtypes = [vp, vp, cp, sz]
+    L.econo_batch_ingest.argtypes = [vp, cp, sz]
     L.econo_batch_jct_prepare.argtypes = [vp, cp, sz]
     L.econo_batch_jct_hist.argtypes = [vp, i32, vp, i32, i32, vp, cp, sz]
     L.econo_batch_jct_percentiles.argtypes = [vp, vp, i32, vp, cp, sz]
@@ -277,6 +278,22 @@ class Batch:
     def debug(self):
         out = np.zeros((self.n, abi.DEBUG_WORDS), dtype=np.int64)
         self._L.econo_batch_debug(self.h, out.ctypes.data)
+        return out
+
+    def ingest(self):
+        """Grid-wide ingest of every instance's due arrivals (econo_batch_ingest)."""
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_batch_ingest(self.h, err, 1024)
+        if rc:
+            _raise(rc, err)
+
+    def snapshot(self, i):
+        """Canonical state snapshot of instance i (econo_snapshot on a batch view)."""
+        v = C.c_void_p()
+        self._L.econo_batch_engine(self.h, i, C.byref(v))
+        n = self._L.econo_snapshot(v, None, 0)
+        out = np.zeros(n, dtype=np.int64)
+        self._L.econo_snapshot(v, out.ctypes.data, n)
         return out
 
     def reports(self):
