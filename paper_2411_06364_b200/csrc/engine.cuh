@@ -27,7 +27,6 @@
 #pragma once
 #include <math.h>
 #include <stdint.h>
-#include <string.h>
 
 #include "econoserve_b200.h"
 
@@ -1886,88 +1885,6 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
   return k > 0 ? k : 0;
 }
 
-// ------------------------------------------------------------------------
-// Exact jumps over chains of repeated floating-point additions. A quiet span
-// advances clock, execution_time and the sample sums by k sequential adds
-// (x <- fl(x + d)). Within one binade of x (ulp u, x = X*u) and with d no
-// larger than x's binade, fl(x + d) = (X + q + c)*u where d = q*u + r,
-// 0 <= r < u, and c rounds r to nearest-even: c = [r > u/2], or on a tie
-// c = [X + q odd]. Without a tie the increment is constant; with a tie it is
-// constant from the second step on (X is even afterwards). So X jumps by
-// n*delta in integer arithmetic until the next binade boundary, where one
-// real DADD crosses it. The result is bit-identical to the k sequential adds.
-// ------------------------------------------------------------------------
-EHD uint64_t dbits(double v) {
-  uint64_t b;
-  memcpy(&b, &v, sizeof(b));
-  return b;
-}
-EHD double dfrom(uint64_t b) {
-  double v;
-  memcpy(&v, &b, sizeof(v));
-  return v;
-}
-// How d splits against the ulp of a normal x whose biased exponent is ex:
-// q whole ulps and the rounding class of the remainder (-1 below half,
-// 0 tie, +1 above). Returns false if d's binade exceeds x's.
-EHD bool ulp_split(int ex, double d, uint64_t* q, int* cmp) {
-  const uint64_t db = dbits(d);
-  const int ed = (int)((db >> 52) & 0x7ff);
-  const uint64_t D = ed ? ((db & ((1ULL << 52) - 1)) | (1ULL << 52)) : (db & ((1ULL << 52) - 1));
-  const int sh = ex - (ed ? ed : 1);  // u / ulp(d) = 2^sh
-  if (sh < 0) return false;
-  if (sh >= 64) {  // d < u / 2^11: rounds away entirely
-    *q = 0;
-    *cmp = -1;
-    return true;
-  }
-  *q = D >> sh;
-  const uint64_t rem = sh ? (D & ((1ULL << sh) - 1)) : 0;
-  if (sh == 0) {
-    *cmp = -1;
-  } else {
-    const uint64_t half = 1ULL << (sh - 1);
-    *cmp = rem < half ? -1 : (rem > half ? 1 : 0);
-  }
-  return true;
-}
-// x after k sequential x = x + d (d >= 0, x >= 0, both finite).
-EHD double fp_repeat_add(double x, double d, int64_t k) {
-  if (d == 0.0) return k > 0 ? x + 0.0 : x;
-  while (k > 0) {
-    const uint64_t xb = dbits(x);
-    const int ex = (int)((xb >> 52) & 0x7ff);
-    uint64_t q;
-    int cmp;
-    if (ex == 0 || ex == 0x7ff || !ulp_split(ex, d, &q, &cmp)) {
-      x = x + d;  // subnormal/zero x, or d from a higher binade: one real add
-      --k;
-      continue;
-    }
-    uint64_t X = (xb & ((1ULL << 52) - 1)) | (1ULL << 52);
-    const uint64_t top = (1ULL << 53) - 1;
-    if (cmp == 0) {  // first tie step: round to the even neighbour, X is even afterwards
-      const uint64_t c0 = (X + q) & 1;
-      if (X + q + c0 > top) { x = x + d; --k; continue; }
-      X += q + c0;
-      --k;
-      if (k == 0) { x = dfrom(((uint64_t)ex << 52) | (X & ((1ULL << 52) - 1))); break; }
-    }
-    const uint64_t delta = q + (cmp > 0 ? 1 : (cmp == 0 ? (q & 1) : 0));
-    if (delta == 0) { x = dfrom(((uint64_t)ex << 52) | (X & ((1ULL << 52) - 1))); break; }
-    const uint64_t room = (top - X) / delta;
-    const uint64_t n = (uint64_t)k < room ? (uint64_t)k : room;
-    X += n * delta;
-    k -= (int64_t)n;
-    x = dfrom(((uint64_t)ex << 52) | (X & ((1ULL << 52) - 1)));
-    if (k > 0) {  // the next add leaves the binade
-      x = x + d;
-      --k;
-    }
-  }
-  return x;
-}
-
 // Progress of one running request over a replayed span (execute_iteration's
 // decode branch, engine.hpp:744-771, k times; exec_t by sequential adds).
 EDEV void quiet_request(Inst& I, int32_t id, double e, int64_t k, double clk1) {
@@ -1994,30 +1911,21 @@ EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double c
   double clock = I.clock, aw = I.agg_written, aa = I.agg_allocated;
   int64_t j = 0;
   if (!has_arr) {
-    // constant addends: closed-form jumps (fp_repeat_add)
-    clock = fp_repeat_add(clock, dt, k);
-    aa = fp_repeat_add(aa, af, k);
-    if (my >= 0) e = fp_repeat_add(e, dt, k);  // idle lanes would walk up from 0 binade by binade
-    // the written fractions vary per step: W steps at a time, each lane
-    // rounds its addend against aw's ulp and the whole ulps are summed in
-    // integers; a chunk with a tie or a binade crossing is added sequentially
     for (int64_t base = 0; base < k; base += W) {
       const int64_t jj = base + LANE;
-      const bool in = jj < k;
-      const double wf = in ? (double)(wt0 + (jj + 1) * fs) / cap : 0.0;
+      const double wf = jj < k ? (double)(wt0 + (jj + 1) * fs) / cap : 0.0;
       const int lim = k - base < W ? (int)(k - base) : W;
-      const uint64_t ab = dbits(aw);
-      const int ea = (int)((ab >> 52) & 0x7ff);
-      uint64_t q = 0;
-      int cmp = -1;
-      const bool ok = !in || (ea != 0 && ea != 0x7ff && ulp_split(ea, wf, &q, &cmp) && cmp != 0);
-      const uint64_t inc = in ? q + (cmp > 0 ? 1 : 0) : 0;
-      const uint64_t tot = wsum(inc);
-      const uint64_t A = (ab & ((1ULL << 52) - 1)) | (1ULL << 52);
-      if (BALLOT(!ok) == 0 && A + tot <= (1ULL << 53) - 1) {
-        aw = dfrom(((uint64_t)ea << 52) | ((A + tot) & ((1ULL << 52) - 1)));
+      if (lim == W) {
+#pragma unroll
+        for (int l = 0; l < W; ++l) {
+          const double w = shfl(wf, l);
+          clock += dt; aw += w; aa += af; e += dt;
+        }
       } else {
-        for (int l = 0; l < lim; ++l) aw += shfl(wf, l);
+        for (int l = 0; l < lim; ++l) {
+          const double w = shfl(wf, l);
+          clock += dt; aw += w; aa += af; e += dt;
+        }
       }
     }
     j = k;
@@ -2039,7 +1947,9 @@ EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double c
   if (my >= 0) quiet_request(I, my, e, k, clk1);
   for (int32_t i = W + LANE; i < R; i += W) {
     const int32_t id = I.run[i];
-    quiet_request(I, id, fp_repeat_add(I.exec_t[id], dt, k), k, clk1);
+    double e2 = I.exec_t[id];
+    for (int64_t t = 0; t < k; ++t) e2 += dt;
+    quiet_request(I, id, e2, k, clk1);
   }
   WSYNC();
   LANE0(I.clock = clock; I.written_total = wt0 + k * fs; I.agg_written = aw; I.agg_allocated = aa;

@@ -1333,12 +1333,6 @@ int jct_percentiles(econo_batch* b, const double* q, int nq, double* out, char* 
 
 }  // namespace
 
-#ifdef ECONO_HOSTSIM
-// Test-only export of the host build (tests/test_fp_jump.py): the closed-form
-// jump over k repeated additions, to be compared with k sequential adds.
-extern "C" double econo_hostsim_repeat_add(double x, double d, int64_t k) { return fp_repeat_add(x, d, k); }
-#endif
-
 extern "C" {
 
 void econo_default_options(EconoOptions* o) {

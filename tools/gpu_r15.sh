@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests/test_nolog_parity.py tests/test_gpu_bulk_ingest.py -m gpu -x -q > gpurun_out/r15_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r15_pytest_gpu.log
+timeout 900 python tools/probe_scale.py --counts 740 --iters 1000 --lanes 0 > gpurun_out/r15_scale.log 2>&1; echo "rc=$?" >> gpurun_out/r15_scale.log
