@@ -1313,7 +1313,7 @@ EDEV bool slot_fits(const Inst& I, int32_t host, int32_t abs, int32_t len) {
 
 EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
   // ---- select_gt_groups (queues.hpp:220-263) ----
-  const int64_t tp0 = PHASE_NOW();
+  [[maybe_unused]] const int64_t tp0 = PHASE_NOW();
   int32_t nsel = 0, nselg = 0, whole = 0;
   if (I.free_total > 0) {
     Tok remaining = I.free_total;
@@ -1384,7 +1384,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     if (I.error) return;
   }
 
-  const int64_t tp1 = PHASE_NOW();
+  [[maybe_unused]] const int64_t tp1 = PHASE_NOW();
   PHASE_ADD(7, tp1 - tp0);
   // ---- KVC pipelining (econoserve-full, engine.hpp:273-297) ----
   if (I.full && nselg > 0) {
@@ -1436,7 +1436,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     }
   }
 
-  const int64_t tp2 = PHASE_NOW();
+  [[maybe_unused]] const int64_t tp2 = PHASE_NOW();
   PHASE_ADD(8, tp2 - tp1);
   // ---- PT batching (engine.hpp:299-324, queues.hpp:279-299) ----
   const Tok tfs_rem = I.tfs - (Tok)I.R;
@@ -1581,7 +1581,7 @@ EDEV void run_compact(Inst& I) {
 }
 
 EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
-  const int64_t tx0 = PHASE_NOW();
+  [[maybe_unused]] const int64_t tx0 = PHASE_NOW();
   const double dt = iteration_time(I, fs) + 0.0;
   LANE0(I.clock += dt; I.iter++);
   const double sched = (double)I.exam_count * I.sched_cost;
@@ -1627,7 +1627,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   // another running request's progress, so it may precede the next chunk's
   // decode. Under-prediction candidates (generated >= allowance < true_rl)
   // are collected here in running order; completed requests never qualify.
-  const int64_t tx1 = PHASE_NOW();
+  [[maybe_unused]] const int64_t tx1 = PHASE_NOW();
   PHASE_ADD(13, tx1 - tx0);
   int32_t completed_now = 0, npre = 0;
   const int32_t R0 = I.R;
@@ -1667,7 +1667,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     }
   }
   if (completed_now) run_compact(I);
-  const int64_t tx2 = PHASE_NOW();
+  [[maybe_unused]] const int64_t tx2 = PHASE_NOW();
   PHASE_ADD(3, tx2 - tx1);
   // prefill transitions (engine.hpp:794-809)
   for (int32_t i = 0; i < I.n_ptiter; ++i) {
@@ -1690,7 +1690,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     WSYNC();
     if (I.error) return;
   }
-  const int64_t tx3 = PHASE_NOW();
+  [[maybe_unused]] const int64_t tx3 = PHASE_NOW();
   PHASE_ADD(14, tx3 - tx2);
   // under-prediction (engine.hpp:812-817): candidates fixed up front (above), handled in order
   for (int32_t k = 0; k < npre; ++k) {
@@ -2036,12 +2036,12 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
 }
 
 EDEVNI void engine_step(Inst& I) {  // Engine::step (engine.hpp:104-116)
-  const int64_t t0 = PHASE_NOW();
+  [[maybe_unused]] const int64_t t0 = PHASE_NOW();
   ingest(I);
   PHASE_ADD(6, PHASE_NOW() - t0);
   form_econoserve(I);
   if (I.error) return;
-  const int64_t t1 = PHASE_NOW();
+  [[maybe_unused]] const int64_t t1 = PHASE_NOW();
   Tok fs = 0;
   for (int32_t i = LANE; i < I.n_ptiter; i += W) fs += I.ptiter_tok[i];
   fs = wsum(fs) + I.R;

@@ -409,21 +409,33 @@ __global__ void __launch_bounds__(256) k_bulk_keys(const Inst* insts, BulkJob* j
   if (threadIdx.x == 0) smin = ~0ULL;
   __syncthreads();
   const int64_t t0 = (int64_t)blockIdx.x * kBulkTile;
+  const double now = I.clock;
+  const int pm1 = I.pmax + 1;
   unsigned long long mn = ~0ULL;
+  uint32_t cnt[ECONO_MAX_BOUNDS + 2];  // per-thread bucket counts (registers: unrolled compares)
+#pragma unroll
+  for (int bb = 0; bb < ECONO_MAX_BOUNDS + 2; ++bb) cnt[bb] = 0;
   for (int e = threadIdx.x; e < kBulkTile; e += blockDim.x) {
     const int64_t i = t0 + e;
     if (i >= J.k) break;
     const int64_t id = J.first + i;
-    const int b = bucket_d(I, dmax(0.0, I.slo[id] - I.clock));
+    const int b = bucket_d(I, dmax(0.0, I.slo[id] - now));
     const int32_t p = I.prompt[id];
-    key[J.off + i] = (uint32_t)cls_of(I, b, p);
+    key[J.off + i] = (uint32_t)(b * pm1 + p);
     val[J.off + i] = (uint32_t)id;
     mn = (unsigned long long)p < mn ? (unsigned long long)p : mn;
-    atomicAdd(&sb[b], 1ULL);
+#pragma unroll
+    for (int bb = 0; bb < ECONO_MAX_BOUNDS + 2; ++bb) cnt[bb] += b == bb;
   }
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long x = __shfl_xor_sync(0xffffffffu, mn, o);
     mn = x < mn ? x : mn;
+  }
+#pragma unroll
+  for (int bb = 0; bb < ECONO_MAX_BOUNDS + 2; ++bb) {
+    uint32_t c = cnt[bb];
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&sb[bb], (unsigned long long)c);
   }
   if ((threadIdx.x & 31) == 0) atomicMin(&smin, mn);
   __syncthreads();
@@ -483,25 +495,35 @@ __global__ void __launch_bounds__(1024) k_radix_scan(const BulkJob* jobs, uint32
 }
 
 // Stable scatter of one tile: each warp ranks its 512 keys in order with
-// match_any, warps are offset by the digit counts of the warps before them.
+// match_any, warps are offset by the digit counts of the warps before them;
+// the tile is first reordered by digit in shared memory so that every digit's
+// run is written to global memory contiguously (coalesced), not key by key.
 __global__ void __launch_bounds__(256) k_radix_scatter(const BulkJob* jobs, const uint32_t* kin, const uint32_t* vin,
                                                        uint32_t* kout, uint32_t* vout, int shift,
                                                        const uint32_t* hist) {
   const BulkJob& J = jobs[blockIdx.y];
   if ((int)blockIdx.x >= J.tiles) return;
+  constexpr int PER = kBulkTile / 256;  // keys per thread
   __shared__ uint32_t sk[kBulkTile];
+  __shared__ uint32_t sv[kBulkTile];
   __shared__ uint32_t cnt[8][256];
+  __shared__ uint32_t tstart[256];
   const int64_t t0 = (int64_t)blockIdx.x * kBulkTile;
   const int n = (int)(J.k - t0 < kBulkTile ? J.k - t0 : kBulkTile);
-  for (int e = threadIdx.x; e < kBulkTile; e += blockDim.x) sk[e] = e < n ? kin[J.off + t0 + e] : 0;
   for (int d = threadIdx.x; d < 8 * 256; d += blockDim.x) (&cnt[0][0])[d] = 0;
-  __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t rank[kBulkTile / 256];
+  uint32_t kr[PER], vr[PER], rank[PER];
 #pragma unroll
-  for (int r = 0; r < kBulkTile / 256; ++r) {
+  for (int r = 0; r < PER; ++r) {  // warp w owns keys [w*512, (w+1)*512) in order
     const int e = w * (kBulkTile / 8) + r * 32 + lane;
-    const int d = e < n ? (int)((sk[e] >> shift) & 255) : -1;
+    kr[r] = e < n ? kin[J.off + t0 + e] : 0;
+    vr[r] = e < n ? vin[J.off + t0 + e] : 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const int e = w * (kBulkTile / 8) + r * 32 + lane;
+    const int d = e < n ? (int)((kr[r] >> shift) & 255) : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     uint32_t base = 0;
     if (d >= 0) base = cnt[w][d];
@@ -511,7 +533,7 @@ __global__ void __launch_bounds__(256) k_radix_scatter(const BulkJob* jobs, cons
     rank[r] = base + __popc(peers & ((1u << lane) - 1u));
   }
   __syncthreads();
-  {  // exclusive prefix over warps, one thread per digit
+  {  // per digit: exclusive prefix over warps, and the digit's total in the tile
     const int d = threadIdx.x;
     uint32_t run = 0;
     for (int ww = 0; ww < 8; ++ww) {
@@ -519,19 +541,43 @@ __global__ void __launch_bounds__(256) k_radix_scatter(const BulkJob* jobs, cons
       cnt[ww][d] = run;
       run += c;
     }
+    tstart[d] = run;
+  }
+  __syncthreads();
+  {  // exclusive scan of the 256 digit totals -> start of each digit's run in the tile
+    const uint32_t v = tstart[threadIdx.x];
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    __shared__ uint32_t ws[8];
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int ww = 0; ww < w; ++ww) pre += ws[ww];
+    __syncthreads();
+    tstart[threadIdx.x] = pre + x - v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const int e = w * (kBulkTile / 8) + r * 32 + lane;
+    if (e < n) {
+      const int d = (int)((kr[r] >> shift) & 255);
+      const uint32_t lp = tstart[d] + cnt[w][d] + rank[r];
+      sk[lp] = kr[r];
+      sv[lp] = vr[r];
+    }
   }
   __syncthreads();
   const uint32_t* hb = hist + J.hoff;
-#pragma unroll
-  for (int r = 0; r < kBulkTile / 256; ++r) {
-    const int e = w * (kBulkTile / 8) + r * 32 + lane;
-    if (e < n) {
-      const uint32_t kv = sk[e];
-      const int d = (int)((kv >> shift) & 255);
-      const int64_t pos = (int64_t)hb[(int64_t)d * J.tiles + blockIdx.x] + cnt[w][d] + rank[r];
-      kout[J.off + pos] = kv;
-      vout[J.off + pos] = vin[J.off + t0 + e];
-    }
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const uint32_t kv = sk[e];
+    const int d = (int)((kv >> shift) & 255);
+    const int64_t pos = (int64_t)hb[(int64_t)d * J.tiles + blockIdx.x] + (e - (int)tstart[d]);
+    kout[J.off + pos] = kv;
+    vout[J.off + pos] = sv[e];
   }
 }
 
@@ -2300,7 +2346,6 @@ struct Mt64 {
   uint64_t x[312];
   int32_t i;
   explicit Mt64(uint64_t s) { mt_seed(x, i, s); }
-  uint64_t next() { return mt_next(x, i); }
   double canon() { return canonical(x, i); }
 };
 double cdf(double v) { return 0.5 * std::erfc(-v / std::sqrt(2.0)); }

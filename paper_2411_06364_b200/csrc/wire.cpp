@@ -151,7 +151,7 @@ void layout(const char* dig, int k, int dexp, std::string& out) {
     out += 'e';
     out += x < 0 ? '-' : '+';
     if (x < 0) x = -x;
-    char e[8];
+    char e[16];
     snprintf(e, sizeof(e), "%02d", x);
     out += e;
   }
