@@ -1793,57 +1793,55 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
   }
   if (jobs.empty()) return ECONO_OK;
   const int passes = (bits + 7) / 8;
-  const int64_t budget = (int64_t)64 << 20;  // keys per group (4 x 4 B each of temp)
-  void *k0 = nullptr, *k1 = nullptr, *v0 = nullptr, *v1 = nullptr, *dh = nullptr, *dj = nullptr;
-  int64_t cap_keys = 0, cap_hist = 0;
-  for (size_t g0 = 0; g0 < jobs.size() && !rc;) {
+  // groups of jobs whose keys fit the temp budget; offsets are per group
+  const int64_t budget = (int64_t)256 << 20;  // keys per group (4 x 4 B of temp each)
+  std::vector<size_t> gstart;
+  int64_t max_off = 0, max_hoff = 0;
+  for (size_t g0 = 0; g0 < jobs.size();) {
     size_t g1 = g0;
     int64_t off = 0, hoff = 0;
-    int32_t tmax = 0;
     while (g1 < jobs.size() && (g1 == g0 || off + jobs[g1].k <= budget)) {
       jobs[g1].off = off;
       jobs[g1].hoff = hoff;
       off += jobs[g1].k;
       hoff += 256LL * jobs[g1].tiles;
-      tmax = std::max(tmax, jobs[g1].tiles);
       ++g1;
     }
-    if (off > cap_keys) {
-      for (void* q : {k0, k1, v0, v1}) dev_free(q);
-      if (dev_alloc(&k0, 4 * (size_t)off) || dev_alloc(&k1, 4 * (size_t)off) || dev_alloc(&v0, 4 * (size_t)off) ||
-          dev_alloc(&v1, 4 * (size_t)off)) {
-        set_err(err, errlen, "bulk ingest allocation failed");
-        rc = ECONO_ECUDA;
-        break;
+    gstart.push_back(g0);
+    max_off = std::max(max_off, off);
+    max_hoff = std::max(max_hoff, hoff);
+    g0 = g1;
+  }
+  gstart.push_back(jobs.size());
+  void *k0 = nullptr, *k1 = nullptr, *v0 = nullptr, *v1 = nullptr, *dh = nullptr, *dj = nullptr;
+  auto raw = [](void** q, size_t bytes) { return cudaMalloc(q, bytes ? bytes : 8) != cudaSuccess; };
+  if (raw(&k0, 4 * (size_t)max_off) || raw(&k1, 4 * (size_t)max_off) || raw(&v0, 4 * (size_t)max_off) ||
+      raw(&v1, 4 * (size_t)max_off) || raw(&dh, 4 * (size_t)max_hoff) || raw(&dj, sizeof(BulkJob) * jobs.size())) {
+    set_err(err, errlen, "bulk ingest allocation failed");
+    rc = ECONO_ECUDA;
+  } else {
+    dev_h2d(dj, jobs.data(), sizeof(BulkJob) * jobs.size());
+    for (size_t g = 0; g + 1 < gstart.size(); ++g) {  // stream-ordered; one sync at the end
+      const int32_t nj = (int32_t)(gstart[g + 1] - gstart[g]);
+      int32_t tmax = 0;
+      for (size_t q = gstart[g]; q < gstart[g + 1]; ++q) tmax = std::max(tmax, jobs[q].tiles);
+      const dim3 grid((unsigned)tmax, (unsigned)nj);
+      BulkJob* J = (BulkJob*)dj + gstart[g];
+      uint32_t *kin = (uint32_t*)k0, *kout = (uint32_t*)k1, *vin = (uint32_t*)v0, *vout = (uint32_t*)v1;
+      k_bulk_keys<<<grid, 256, 0, b->stream>>>(b->d_insts, J, kin, vin);
+      for (int pass = 0; pass < passes; ++pass) {
+        k_radix_hist<<<grid, 256, 0, b->stream>>>(J, kin, 8 * pass, (uint32_t*)dh);
+        k_radix_scan<<<(unsigned)nj, 1024, 0, b->stream>>>(J, (uint32_t*)dh);
+        k_radix_scatter<<<grid, 256, 0, b->stream>>>(J, kin, vin, kout, vout, 8 * pass, (const uint32_t*)dh);
+        std::swap(kin, kout);
+        std::swap(vin, vout);
       }
-      cap_keys = off;
+      k_bulk_heads<<<grid, 256, 0, b->stream>>>(b->d_insts, J, kin, vin);
+      k_bulk_tails<<<grid, 256, 0, b->stream>>>(b->d_insts, J, kin, vin);
+      k_bulk_finish<<<(unsigned)nj, 32, 0, b->stream>>>(b->d_insts, J);
     }
-    if (hoff > cap_hist) {
-      dev_free(dh);
-      if (dev_alloc(&dh, 4 * (size_t)hoff)) { set_err(err, errlen, "allocation failed"); rc = ECONO_ECUDA; break; }
-      cap_hist = hoff;
-    }
-    const int32_t nj = (int32_t)(g1 - g0);
-    dev_free(dj);
-    if (dev_alloc(&dj, sizeof(BulkJob) * (size_t)nj)) { set_err(err, errlen, "allocation failed"); rc = ECONO_ECUDA; break; }
-    dev_h2d(dj, jobs.data() + g0, sizeof(BulkJob) * (size_t)nj);
-    const dim3 grid((unsigned)tmax, (unsigned)nj);
-    BulkJob* J = (BulkJob*)dj;
-    uint32_t *kin = (uint32_t*)k0, *kout = (uint32_t*)k1, *vin = (uint32_t*)v0, *vout = (uint32_t*)v1;
-    k_bulk_keys<<<grid, 256, 0, b->stream>>>(b->d_insts, J, kin, vin);
-    for (int pass = 0; pass < passes; ++pass) {
-      k_radix_hist<<<grid, 256, 0, b->stream>>>(J, kin, 8 * pass, (uint32_t*)dh);
-      k_radix_scan<<<(unsigned)nj, 1024, 0, b->stream>>>(J, (uint32_t*)dh);
-      k_radix_scatter<<<grid, 256, 0, b->stream>>>(J, kin, vin, kout, vout, 8 * pass, (const uint32_t*)dh);
-      std::swap(kin, kout);
-      std::swap(vin, vout);
-    }
-    k_bulk_heads<<<grid, 256, 0, b->stream>>>(b->d_insts, J, kin, vin);
-    k_bulk_tails<<<grid, 256, 0, b->stream>>>(b->d_insts, J, kin, vin);
-    k_bulk_finish<<<(unsigned)nj, 32, 0, b->stream>>>(b->d_insts, J);
     rc = sync_batch(b, err, errlen);
     if (!rc) rc = cuda_check(err, errlen, "bulk ingest");
-    g0 = g1;
   }
   for (void* q : {k0, k1, v0, v1, dh, dj}) dev_free(q);
   return rc;

@@ -14,6 +14,37 @@ LLAMA2_13B_TOKENS = 14648
 
 BURST_RATE = 1e9          # "1M queued": every arrival lands inside the first idle tick
 
+MIXED_PARTS = (ALPACA, SHAREGPT, BOOKCORPUS)
+
+
+def mixed_trace(gen, n, rate, seed, out=None):
+    """configs[3]'s trace (SURVEY.md §8(d) cfg 4): three traces of the cfg 1-3
+    shapes (seeds seed, seed+1, seed+2; n/3 each, the remainder to the last)
+    merged by arrival time, stably, into one trace (load_trace_csv requires
+    nondecreasing arrivals, workload.hpp:181-183). gen(n, rate, prompt, rl,
+    seed) is generate_synthetic (workload.hpp:104-125)."""
+    import numpy as np
+    sizes = [n // 3, n // 3, n - 2 * (n // 3)]
+    parts = [gen(m, rate, sh["prompt"], sh["rl"], seed + i) for i, (m, sh) in enumerate(zip(sizes, MIXED_PARTS)) if m]
+    cat = np.concatenate(parts)
+    order = np.argsort(cat["arrival_time"], kind="stable")
+    if out is None:
+        return cat[order]
+    out[:] = cat[order]
+    return out
+
+
+def make_trace(name, gen, n=None, seed=None, out=None):
+    """The synthetic trace of CONFIGS[name] (n and seed overridable)."""
+    c = CONFIGS[name]
+    n = c["n"] if n is None else n
+    seed = c["seed"] if seed is None else seed
+    if c["shape"] == "mixed":
+        return mixed_trace(gen, n, c["rate"], seed, out=out)
+    kw = {} if out is None else {"out": out}
+    return gen(n, c["rate"], c["shape"]["prompt"], c["shape"]["rl"], seed, **kw)
+
+
 # name -> (trace shape, n, arrival rate, trace seed, option overrides)
 CONFIGS = {
     # configs[0]: the reference's own CPU-runnable case

@@ -45,4 +45,12 @@ def catalogue(gen):
     cases.append(("bookcorpus-cfg3-shape-burst", bk, abi.default_options(**b["opts"])))
     cases.append(("bookcorpus-cfg3-shape-burst-sd", bk, abi.default_options(
         **dict(b["opts"], policy="econoserve-sd"))))
+    m = W.CONFIGS["cfg4_mixed_1m"]  # configs[3]: mixed trace, predictor error sweep (SURVEY §8(d) cfg 4)
+    mx = W.make_trace("cfg4_mixed_1m", gen, n=600, seed=7)
+    for tag, extra in [("lognormal0.1", dict(pred_sigma=0.1)),
+                       ("lognormal0.6-pad0.25", dict(pred_sigma=0.6, pred_padding_ratio=0.25)),
+                       ("bucket0.732-pad0.15", dict(pred_model="bucket", pred_accuracy=0.732, pred_tolerance=0.15,
+                                                    pred_padding_ratio=0.15)),
+                       ("sd-lognormal0.3", dict(policy="econoserve-sd", pred_sigma=0.3))]:
+        cases.append((f"mixed-cfg4-{tag}", mx, abi.default_options(**dict(m["opts"], **extra))))
     return cases
