@@ -13,6 +13,11 @@ iterations (Engine::step(), engine.hpp:104-116) with 1M requests queued.
 value = PT admissions (pt_dispatch, engine.hpp:380) per second over all GPUs;
 us_per_iter = per-instance wall time of one scheduler iteration.
 
+`--workload` selects another BASELINE.json config (cfg4_mixed_1m: the mixed
+Alpaca/ShareGPT/BookCorpus 1M burst with the lognormal predictor, i.e. the
+preemption path; cfg2_sharegpt_100k, cfg1_alpaca_10k); the default is the
+metric's own 1M-queued case.
+
 `--impl reference` times the unmodified reference simulator (oracle/_ref,
 compiled from /root/reference by oracle/Makefile) on the host cores on the
 same config: one engine per thread, each step a bounded window of iterations.
@@ -50,10 +55,9 @@ def options(record=False):
 
 
 def make_traces(gen, n, seeds, threads=32, pinned=False):
-    """One synthetic trace per seed. pinned=True generates straight into one
-    page-locked host buffer (the e2e contract: inputs copied from pinned host
-    memory), returned as per-instance views."""
-    c = W.CONFIGS[WORKLOAD]
+    """One synthetic trace of the workload per seed (workloads.make_trace).
+    pinned=True generates straight into one page-locked host buffer (the e2e
+    contract: inputs copied from pinned host memory), returned as views."""
     outs = [None] * len(seeds)
     if pinned:
         import torch
@@ -61,9 +65,7 @@ def make_traces(gen, n, seeds, threads=32, pinned=False):
         buf = torch.empty(len(seeds) * n * rec, dtype=torch.uint8, pin_memory=True).numpy()
         outs = [buf[i * n * rec:(i + 1) * n * rec].view(abi.TRACE_DTYPE) for i in range(len(seeds))]
     with ThreadPoolExecutor(threads) as ex:
-        return list(ex.map(lambda a: gen(n, c["rate"], c["shape"]["prompt"], c["shape"]["rl"], a[0],
-                                         **({"out": a[1]} if pinned else {})),
-                           zip(seeds, outs)))
+        return list(ex.map(lambda a: W.make_trace(WORKLOAD, gen, n=n, seed=a[0], out=a[1]), zip(seeds, outs)))
 
 
 class ClockSampler:
@@ -195,7 +197,7 @@ def run_reference(args):
         "ms_per_step": 1e3 * secs / len(wins), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "requests_per_instance": args.n, "instances": threads,
-                   "iters_per_step": args.ref_iters, "policy": "econoserve-full",
+                   "iters_per_step": args.ref_iters, "policy": W.CONFIGS[WORKLOAD]["opts"]["policy"],
                    "window": window_str(args, args.ref_iters)},
         "us_per_iter": us_iter,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
@@ -333,7 +335,7 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "requests_per_instance": args.n,
                    "instances_per_gpu": I, "iters_per_step": args.iters,
-                   "policy": "econoserve-full",
+                   "policy": W.CONFIGS[WORKLOAD]["opts"]["policy"],
                    "l2": f"inputs larger than L2: {I} x ~184 MB of instance state per GPU vs 126 MB L2, no flush",
                    "window": window_str(args)},
         "us_per_iter": us_iter,
@@ -404,7 +406,10 @@ def main():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default=WORKLOAD, choices=sorted(W.CONFIGS),
+                    help="BASELINE.json config (default: configs[2], the 1M-queued case the metric is quoted on)")
     args = ap.parse_args()
+    globals()["WORKLOAD"] = args.workload
     if args.impl == "reference":
         run_reference(args)
     else:
