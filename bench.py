@@ -256,6 +256,7 @@ def run_ours(args):
         dist.barrier()
     t0 = time.perf_counter()
     b = Batch(traces, options(), device=local)
+    t_created = time.perf_counter()
     b.launch(1, stream.cuda_stream)  # idle tick up to the burst (engine.hpp:930-949)
     stream.synchronize()
     b.ingest()                       # the 1M burst, grid-wide (engine.hpp:216-235)
@@ -263,6 +264,7 @@ def run_ours(args):
     stream.synchronize()
     b.sync()
     t_create_ingest = time.perf_counter() - t0
+    t_ingest = time.perf_counter() - t_created
     sc_a = b.scalars()
     for _ in range(args.warmup):
         b.launch(args.iters, stream.cuda_stream)
@@ -346,6 +348,7 @@ def run_ours(args):
         "quiet_step_frac": (sum(a.quiet_steps - z.quiet_steps for a, z in zip(sc1, sc0)) /
                             max(1, sum(a.steps - z.steps for a, z in zip(sc1, sc0)))),
         "ingest_and_create_s": t_create_ingest,
+        "ingest_s": t_ingest,
         "tracegen_s": t_gen,
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -1090,6 +1090,9 @@ struct econo_batch {
   // JCT keys for the percentile radix select (econo_batch_jct_prepare)
   uint64_t* d_keys = nullptr;
   int64_t* d_koff = nullptr;
+  // bulk-ingest scratch (kept: a synchronous cudaFree of these GBs costs ~0.1 s)
+  void* bulk_buf = nullptr;
+  size_t bulk_bytes = 0;
   int64_t keys_total = 0;
   std::vector<uint64_t> h_keys;  // host build
 #ifndef ECONO_HOSTSIM
@@ -1430,6 +1433,7 @@ void econo_batch_destroy(econo_batch* b) {
   dev_free(b->d_insts);
   dev_free(b->d_keys);
   dev_free(b->d_koff);
+  dev_free(b->bulk_buf);
   for (auto* v : b->views) delete v;
 #ifndef ECONO_HOSTSIM
   if (b->stream) cudaStreamDestroy(b->stream);
@@ -1764,6 +1768,10 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
   return ECONO_OK;  // the host build ingests inside step()
 #else
   const int32_t ni = (int32_t)b->inst.size();
+  const bool verbose = getenv("ECONO_VERBOSE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b2) { return std::chrono::duration<double, std::milli>(b2 - a).count(); };
+  const auto t0 = now();
   void* dplan;
   if (dev_alloc(&dplan, sizeof(int64_t) * 2 * (size_t)ni)) return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
   k_bulk_plan<<<(unsigned)ni, 32, 0, b->stream>>>(b->d_insts, (int64_t*)dplan);
@@ -1813,13 +1821,24 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
     g0 = g1;
   }
   gstart.push_back(jobs.size());
-  void *k0 = nullptr, *k1 = nullptr, *v0 = nullptr, *v1 = nullptr, *dh = nullptr, *dj = nullptr;
-  auto raw = [](void** q, size_t bytes) { return cudaMalloc(q, bytes ? bytes : 8) != cudaSuccess; };
-  if (raw(&k0, 4 * (size_t)max_off) || raw(&k1, 4 * (size_t)max_off) || raw(&v0, 4 * (size_t)max_off) ||
-      raw(&v1, 4 * (size_t)max_off) || raw(&dh, 4 * (size_t)max_hoff) || raw(&dj, sizeof(BulkJob) * jobs.size())) {
+  // one cached scratch block: keys, values (ping-pong), histograms, jobs
+  const size_t kb = ((4 * (size_t)max_off + 255) & ~(size_t)255);
+  const size_t hb = ((4 * (size_t)max_hoff + 255) & ~(size_t)255);
+  const size_t need = 4 * kb + hb + sizeof(BulkJob) * jobs.size();
+  if (need > b->bulk_bytes) {
+    dev_free(b->bulk_buf);
+    b->bulk_buf = nullptr;
+    b->bulk_bytes = 0;
+    if (cudaMalloc(&b->bulk_buf, need) == cudaSuccess) b->bulk_bytes = need;
+  }
+  char* base = (char*)b->bulk_buf;
+  void *k0 = base, *k1 = base + kb, *v0 = base + 2 * kb, *v1 = base + 3 * kb, *dh = base + 4 * kb,
+       *dj = base + 4 * kb + hb;
+  if (!b->bulk_buf) {
     set_err(err, errlen, "bulk ingest allocation failed");
     rc = ECONO_ECUDA;
   } else {
+    const auto t1 = now();
     dev_h2d(dj, jobs.data(), sizeof(BulkJob) * jobs.size());
     for (size_t g = 0; g + 1 < gstart.size(); ++g) {  // stream-ordered; one sync at the end
       const int32_t nj = (int32_t)(gstart[g + 1] - gstart[g]);
@@ -1842,8 +1861,11 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
     }
     rc = sync_batch(b, err, errlen);
     if (!rc) rc = cuda_check(err, errlen, "bulk ingest");
+    if (verbose)
+      fprintf(stderr, "[econo] bulk ingest: plan+alloc %.1f ms, kernels %.1f ms (%zu jobs, %zu groups)\n", ms(t0, t1),
+              ms(t1, now()), jobs.size(), gstart.size() - 1);
   }
-  for (void* q : {k0, k1, v0, v1, dh, dj}) dev_free(q);
+  if (verbose) fprintf(stderr, "[econo] bulk ingest: total %.1f ms\n", ms(t0, now()));
   return rc;
 #endif
 }
