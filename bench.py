@@ -389,9 +389,49 @@ def run_ours(args):
         except Exception as ex:  # the reference build is missing on this box
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {ex}"}
+    if world == 1 and not args.no_full_runs:
+        b.close()  # free the 136 GB batch before the single-engine runs
+        line["full_runs"] = full_runs(args)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def full_runs(args):
+    """SURVEY §8(d) primary metric 2: completed requests/s over whole runs of
+    configs[0] and configs[1], one engine each through the single-engine
+    public API (Engine(trace, opts).run(), engine.hpp:1039-1042) from host
+    trace buffers, wall clock; the reference's own full run is timed beside
+    it on one host core for configs[0] (configs[1] takes ~155 s on the CPU,
+    SURVEY §6, and is not repeated here)."""
+    from paper_2411_06364_b200.engine import Engine, generate_trace
+    out = {}
+    for name in ("cfg1_alpaca_10k", "cfg2_sharegpt_100k"):
+        c = W.CONFIGS[name]
+        t = W.make_trace(name, generate_trace)
+        o = abi.default_options(**c["opts"])
+        o.record_events = 0
+        o.record_samples = 0
+        t0 = time.perf_counter()
+        recs, rep = Engine(t, o, device=0).run()
+        secs = time.perf_counter() - t0
+        r = {"requests": len(t), "iterations": int(rep.iterations), "wall_s": secs,
+             "completed_per_s": len(t) / secs, "mean_jct": rep.mean_jct, "ssr": rep.ssr,
+             "hosted_slots": int(rep.hosted_slots)}
+        if name == "cfg1_alpaca_10k" and not args.no_cpu_baseline:
+            try:
+                from oracle import ref
+                o2 = abi.default_options(**c["opts"])  # the reference's default EngineOptions record events
+                rt = ref.generate_trace(len(t), c["rate"], c["shape"]["prompt"], c["shape"]["rl"], c["seed"])
+                e = ref.RefEngine(rt, o2)
+                t1 = time.perf_counter()
+                e.run()
+                r["reference_wall_s"] = time.perf_counter() - t1
+                r["reference_completed_per_s"] = len(rt) / r["reference_wall_s"]
+            except Exception as ex:  # noqa: BLE001
+                r["reference"] = f"unavailable: {ex}"
+        out[name] = r
+    return out
 
 
 def main():
@@ -409,6 +449,8 @@ def main():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full-runs", action="store_true",
+                    help="skip the whole-run completed-req/s measurements of configs[0] and configs[1]")
     ap.add_argument("--workload", default=WORKLOAD, choices=sorted(W.CONFIGS),
                     help="BASELINE.json config (default: configs[2], the 1M-queued case the metric is quoted on)")
     args = ap.parse_args()
