@@ -136,6 +136,7 @@ struct Inst {
   int32_t reg_free_top, grp_free_top, n_sel, n_selg, n_hosts_members;
   int32_t error, err_id, status, mt_i, pmt_i, _pad0;
   int64_t err_val, ev_n, ev_cap, sm_n, sm_cap, ev_total;
+  double wbuf[W];      // quiet-span replay: one chunk of per-step written fractions
   int64_t pt_min_lb;   // lower bound on the smallest queued prompt (only grows between arrivals)
   int32_t bcnt[ECONO_MAX_BOUNDS + 2];  // queued PTs per deadline bucket (ordered mode)
   int64_t quiet_steps, quiet_spans, bcast;
@@ -1911,22 +1912,25 @@ EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double c
   double clock = I.clock, aw = I.agg_written, aa = I.agg_allocated;
   int64_t j = 0;
   if (!has_arr) {
+    // The fractions of a chunk go to shared memory; the unrolled chain then
+    // reads them with loads the compiler can issue ahead of the adds (a
+    // shuffle per step would put its latency on the aw chain).
     for (int64_t base = 0; base < k; base += W) {
       const int64_t jj = base + LANE;
-      const double wf = jj < k ? (double)(wt0 + (jj + 1) * fs) / cap : 0.0;
+      I.wbuf[LANE] = jj < k ? (double)(wt0 + (jj + 1) * fs) / cap : 0.0;
+      WSYNC();
       const int lim = k - base < W ? (int)(k - base) : W;
       if (lim == W) {
 #pragma unroll
         for (int l = 0; l < W; ++l) {
-          const double w = shfl(wf, l);
-          clock += dt; aw += w; aa += af; e += dt;
+          clock += dt; aw += I.wbuf[l]; aa += af; e += dt;
         }
       } else {
         for (int l = 0; l < lim; ++l) {
-          const double w = shfl(wf, l);
-          clock += dt; aw += w; aa += af; e += dt;
+          clock += dt; aw += I.wbuf[l]; aa += af; e += dt;
         }
       }
+      WSYNC();
     }
     j = k;
   } else {  // the arrival cut-off is re-checked before every replayed step

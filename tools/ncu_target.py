@@ -29,7 +29,10 @@ def main():
     a = ap.parse_args()
     traces = bench.make_traces(generate_trace, a.n, [1000 + i for i in range(a.instances)])
     b = Batch(traces, bench.options(), device=0)
-    b.launch(2)
+    b.launch(1)
+    b.sync()
+    b.ingest()
+    b.launch(1)
     b.sync()
     for _ in range(a.warmup + a.launches):
         b.launch(a.iters)
