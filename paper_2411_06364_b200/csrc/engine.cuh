@@ -32,7 +32,9 @@
 
 #ifdef __CUDACC__
 #define EDEV __device__ __forceinline__
-#define EDEVNI __device__ __noinline__
+// Every engine function inlines into k_engine_steps: measured 15% faster than
+// separate device functions (no call/stack traffic, scheduling across calls).
+#define EDEVNI __device__ __forceinline__
 #define EHD __host__ __device__ __forceinline__
 #define W 32
 #define LANE ((int)(threadIdx.x & 31))
