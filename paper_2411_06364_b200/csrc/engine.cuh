@@ -114,6 +114,35 @@ enum {
 };
 enum { STATUS_RUN = 0, STATUS_DRAIN = 1 };
 
+// Device pointer held in the shared-memory Inst. Every use carries
+// __isGlobal, so accesses compile to global loads/stores (LDG/STG); generic
+// ones could alias the shared-memory Inst, forcing its fields to be reloaded
+// after every store.
+#ifdef __CUDACC__
+#define EMEM __host__ __device__ __forceinline__
+#else
+#define EMEM inline
+#endif
+template <class T>
+struct GP {
+  T* p;
+  EMEM T* get() const {
+#ifdef __CUDA_ARCH__
+    T* q = p;
+    __builtin_assume(__isGlobal(q));
+    return q;
+#else
+    return p;
+#endif
+  }
+  EMEM operator T*() const { return get(); }
+  EMEM T& operator[](int64_t i) const { return get()[i]; }
+  EMEM GP& operator=(T* q) {
+    p = q;
+    return *this;
+  }
+};
+
 // Per-instance scalar block + SoA pointers. Kept in shared memory while a
 // launch runs (one warp per instance), written back on exit.
 struct Inst {
@@ -152,40 +181,40 @@ struct Inst {
   double agg_written, agg_allocated;
   int64_t agg_fs, agg_tfs_hits, agg_pt_iters;
   // ---- per-request SoA (n entries) ----
-  const double* arrival;
-  const int32_t* prompt;
-  const int32_t* true_rl;
-  int32_t *predicted, *padded, *generated, *occupied, *allowance, *gen_epoch, *prefill_done;
-  int32_t *preempt_count, *reserve_draws, *held, *reg_head, *reg_tail, *reg_cnt, *reserved, *written;
-  int32_t *slot_host, *slot_off, *slot_len, *slot_abs, *pt_next, *gt_next, *dem;
-  uint8_t *state, *flags;
-  double *slo, *waiting, *preempt_t, *exec_t, *dispatch_t, *first_tok, *compl_clock, *last_enq;
-  double *penalty, *sched_share;
+  GP<const double> arrival;
+  GP<const int32_t> prompt;
+  GP<const int32_t> true_rl;
+  GP<int32_t> predicted, padded, generated, occupied, allowance, gen_epoch, prefill_done;
+  GP<int32_t> preempt_count, reserve_draws, held, reg_head, reg_tail, reg_cnt, reserved, written;
+  GP<int32_t> slot_host, slot_off, slot_len, slot_abs, pt_next, gt_next, dem;
+  GP<uint8_t> state, flags;
+  GP<double> slo, waiting, preempt_t, exec_t, dispatch_t, first_tok, compl_clock, last_enq;
+  GP<double> penalty, sched_share;
   // ---- KVC region pool (reg_cap) ----
-  int32_t *rg_start, *rg_len, *rg_owner, *rg_next, *reg_free, *addr;
+  GP<int32_t> rg_start, rg_len, rg_owner, rg_next, reg_free, addr;
   // ---- PT queue ----
-  int32_t *cls_head, *cls_tail, *cls_cnt;
-  uint64_t *bm1, *bm2;
-  int32_t* tree;
+  GP<int32_t> cls_head, cls_tail, cls_cnt;
+  GP<uint64_t> bm1, bm2;
+  GP<int32_t> tree;
   // ---- GT groups (grp_cap) ----
-  uint64_t *gr_id, *gr_seq;
-  int32_t *gr_rl, *gr_head, *gr_tail, *gr_cnt, *gr_db, *gr_kb, *gr_maxocc, *grp_free, *gq, *rl_map;
-  double *gr_formed, *gr_mindl;
-  int64_t* gr_dem;
+  GP<uint64_t> gr_id, gr_seq;
+  GP<int32_t> gr_rl, gr_head, gr_tail, gr_cnt, gr_db, gr_kb, gr_maxocc, grp_free, gq, rl_map;
+  GP<double> gr_formed, gr_mindl;
+  GP<int64_t> gr_dem;
   // ---- ordered lists ----
-  int32_t *run, *slots, *ptiter_id, *ptiter_tok, *adm;
+  GP<int32_t> run, slots, ptiter_id, ptiter_tok, adm;
   // ---- scratch ----
-  int32_t *sel_ids, *selg_start, *selg_rl;            // GT selection output
-  int32_t *wa_w, *wa_b, *wa_l, *wa_u, *wb_w, *wb_b, *wb_l, *wb_u;  // planner regions
-  int32_t *cd_ri, *cd_abs, *cd_use, *cd_len, *assigned;   // planner candidates
-  int32_t *os_host, *os_hosted, *os_off, *os_len, *os_abs;  // planner output slots
-  int32_t *tmp_a, *tmp_b, *tmp_c;
+  GP<int32_t> sel_ids, selg_start, selg_rl;            // GT selection output
+  GP<int32_t> wa_w, wa_b, wa_l, wa_u, wb_w, wb_b, wb_l, wb_u;  // planner regions
+  GP<int32_t> cd_ri, cd_abs, cd_use, cd_len, assigned;   // planner candidates
+  GP<int32_t> os_host, os_hosted, os_off, os_len, os_abs;  // planner output slots
+  GP<int32_t> tmp_a, tmp_b, tmp_c;
   // ---- RNG (mt19937_64 x2) ----
-  uint64_t *mt, *pmt;
+  GP<uint64_t> mt, pmt;
   // ---- outputs ----
-  EconoEvent* ev;
-  EconoSample* sm;
-  int64_t* hist;
+  GP<EconoEvent> ev;
+  GP<EconoSample> sm;
+  GP<int64_t> hist;
 };
 
 // ------------------------------------------------------------------------
@@ -255,6 +284,14 @@ EDEV void arr_erase(T* a, int32_t n, int32_t pos, int32_t k) {
     if (ok) a[i] = x;
     WSYNC();
   }
+}
+template <class T>
+EDEV void arr_insert(GP<T> a, int32_t n, int32_t pos, T v) {
+  arr_insert(a.get(), n, pos, v);
+}
+template <class T>
+EDEV void arr_erase(GP<T> a, int32_t n, int32_t pos, int32_t k) {
+  arr_erase(a.get(), n, pos, k);
 }
 // Position of the first element equal to v (or -1), warp ballot scan.
 EDEV int32_t arr_find(const int32_t* a, int32_t n, int32_t v) {

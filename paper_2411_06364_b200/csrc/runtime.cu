@@ -43,9 +43,9 @@ namespace econo {
 // pred_rng_ stream for non-oracle predictors, scalar calibration) run per
 // instance. Phase 1: trace AoS -> SoA, arrival-order check, prompt sum.
 EDEV void init_soa_one(Inst& I, const EconoTraceRecord* tr, int64_t i, bool* order_bad, int64_t* prompt) {
-  double* arr = const_cast<double*>(I.arrival);
-  int32_t* pr = const_cast<int32_t*>(I.prompt);
-  int32_t* rl = const_cast<int32_t*>(I.true_rl);
+  double* arr = const_cast<double*>(I.arrival.get());
+  int32_t* pr = const_cast<int32_t*>(I.prompt.get());
+  int32_t* rl = const_cast<int32_t*>(I.true_rl.get());
   arr[i] = tr[i].arrival_time;
   pr[i] = (int32_t)tr[i].prompt_len;
   rl[i] = (int32_t)tr[i].true_rl;
@@ -818,14 +818,14 @@ void layout(Inst& I, char* base, size_t* bytes) {
   I.arrival = a.take<double>(n);
   I.prompt = a.take<int32_t>(n);
   I.true_rl = a.take<int32_t>(n);
-  int32_t** i32s[] = {&I.predicted, &I.padded, &I.generated, &I.occupied, &I.allowance, &I.gen_epoch,
+  GP<int32_t>* i32s[] = {&I.predicted, &I.padded, &I.generated, &I.occupied, &I.allowance, &I.gen_epoch,
                       &I.prefill_done, &I.preempt_count, &I.reserve_draws, &I.held, &I.reg_head,
                       &I.reg_tail, &I.reg_cnt, &I.reserved, &I.written, &I.slot_host, &I.slot_off,
                       &I.slot_len, &I.slot_abs, &I.pt_next, &I.gt_next, &I.dem};
   for (auto p : i32s) *p = a.take<int32_t>(n);
   I.state = a.take<uint8_t>(n);
   I.flags = a.take<uint8_t>(n);
-  double** f64s[] = {&I.slo, &I.waiting, &I.preempt_t, &I.exec_t, &I.dispatch_t, &I.first_tok,
+  GP<double>* f64s[] = {&I.slo, &I.waiting, &I.preempt_t, &I.exec_t, &I.dispatch_t, &I.first_tok,
                      &I.compl_clock, &I.last_enq, &I.penalty, &I.sched_share};
   for (auto p : f64s) *p = a.take<double>(n);
   const int64_t rc = I.reg_cap;
@@ -848,7 +848,7 @@ void layout(Inst& I, char* base, size_t* bytes) {
   const int64_t gc = I.grp_cap;
   I.gr_id = a.take<uint64_t>(gc);
   I.gr_seq = a.take<uint64_t>(gc);
-  int32_t** g32[] = {&I.gr_rl, &I.gr_head, &I.gr_tail, &I.gr_cnt, &I.gr_db, &I.gr_kb, &I.gr_maxocc, &I.grp_free};
+  GP<int32_t>* g32[] = {&I.gr_rl, &I.gr_head, &I.gr_tail, &I.gr_cnt, &I.gr_db, &I.gr_kb, &I.gr_maxocc, &I.grp_free};
   for (auto p : g32) *p = a.take<int32_t>(gc);
   I.gq = a.take<int32_t>(gc + W);
   I.rl_map = a.take<int32_t>(I.rl_cap);
@@ -864,7 +864,7 @@ void layout(Inst& I, char* base, size_t* bytes) {
   I.selg_start = a.take<int32_t>(I.sel_cap + 1);
   I.selg_rl = a.take<int32_t>(I.sel_cap + 1);
   const int64_t pc = 2 * (int64_t)I.scr_cap + W;
-  int32_t** pl[] = {&I.wa_w, &I.wa_b, &I.wa_l, &I.wa_u, &I.wb_w, &I.wb_b, &I.wb_l, &I.wb_u,
+  GP<int32_t>* pl[] = {&I.wa_w, &I.wa_b, &I.wa_l, &I.wa_u, &I.wb_w, &I.wb_b, &I.wb_l, &I.wb_u,
                     &I.cd_ri, &I.cd_abs, &I.cd_use, &I.cd_len, &I.assigned,
                     &I.os_host, &I.os_hosted, &I.os_off, &I.os_len, &I.os_abs, &I.tmp_a, &I.tmp_b, &I.tmp_c};
   for (auto p : pl) *p = a.take<int32_t>(pc);
@@ -1545,9 +1545,9 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
 #ifdef ECONO_HOSTSIM
   for (int32_t i = 0; i < n_inst; ++i) {
     Inst& I = b->inst[(size_t)i].desc;
-    double* arr = const_cast<double*>(I.arrival);
-    int32_t* pr = const_cast<int32_t*>(I.prompt);
-    int32_t* rl = const_cast<int32_t*>(I.true_rl);
+    double* arr = const_cast<double*>(I.arrival.get());
+    int32_t* pr = const_cast<int32_t*>(I.prompt.get());
+    int32_t* rl = const_cast<int32_t*>(I.true_rl.get());
     for (int64_t k = 0; k < I.n; ++k) {
       arr[k] = traces[i][k].arrival_time;
       pr[k] = (int32_t)traces[i][k].prompt_len;
