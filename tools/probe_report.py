@@ -16,7 +16,10 @@ from paper_2411_06364_b200.engine import Batch, generate_trace  # noqa: E402
 I = int(os.environ.get("INST", "740"))
 traces = bench.make_traces(generate_trace, 1_000_000, [1000 + i for i in range(I)], pinned=True)
 b = Batch(traces, bench.options(), device=0)
-b.launch(2)
+b.launch(1)
+b.sync()
+b.ingest()
+b.launch(1)
 b.launch(1000)
 b.sync()
 for rep in range(3):
