@@ -83,12 +83,6 @@ static inline uint64_t umulhi64(uint64_t a, uint64_t b) {
 #else
 #define PROF_NOW() ((int64_t)0)
 #endif
-// L1 prefetch hint (no semantic effect; a no-op in the host build).
-#ifdef __CUDA_ARCH__
-#define PREFETCH_L1(p) asm volatile("prefetch.global.L1 [%0];" ::"l"((const void*)(p)))
-#else
-#define PREFETCH_L1(p) ((void)(p))
-#endif
 // Per-phase cycle counters (prof[3], [6..10], [13..15]) cost ~10 instructions
 // each; they are compiled in only with -DECONO_PROF_PHASES (tools/probe_scale).
 #ifdef ECONO_PROF_PHASES
@@ -1956,38 +1950,11 @@ EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double c
   double e = my >= 0 ? I.exec_t[my] : 0.0;
   double clock = I.clock, aw = I.agg_written, aa = I.agg_allocated;
   int64_t j = 0;
-  // Speculative prefetch of what the event steps after this span touch (the
-  // replay's DADD chain hides the latency; nothing here changes any state):
-  // stage 1 now, stage 2 after the first chunk, stage 3 at the end.
-  //   lane 0: the GT queue head group -> its first member's fields;
-  //   lane j < n_regions: the region order addr[j] -> rg_start/rg_len;
-  //   running lanes: the request's regions (its release at completion).
-  int32_t pf_g = -1, pf_r = -1, pf_h = -1, pf_m = -1;
-  if (!I.record_samples) {
-    if (LANE == 0 && I.G > 0) pf_g = I.gq[0];
-    if (LANE < I.n_regions) pf_r = I.addr[LANE];
-    if (my >= 0) pf_h = I.reg_head[my];
-  }
   if (!has_arr) {
     // The fractions of a chunk go to shared memory; the unrolled chain then
     // reads them with loads the compiler can issue ahead of the adds (a
     // shuffle per step would put its latency on the aw chain).
     for (int64_t base = 0; base < k; base += W) {
-      if (base == W) {  // stage 2
-        if (pf_g >= 0) {
-          pf_m = I.gr_head[pf_g];
-          PREFETCH_L1(&I.gr_dem[pf_g]);
-          PREFETCH_L1(&I.gr_cnt[pf_g]);
-        }
-        if (pf_r >= 0) {
-          PREFETCH_L1(&I.rg_start[pf_r]);
-          PREFETCH_L1(&I.rg_len[pf_r]);
-        }
-        if (pf_h >= 0) {
-          PREFETCH_L1(&I.rg_start[pf_h]);
-          PREFETCH_L1(&I.rg_next[pf_h]);
-        }
-      }
       const int64_t jj = base + LANE;
       I.wbuf[LANE] = jj < k ? (double)(wt0 + (jj + 1) * fs) / cap : 0.0;
       WSYNC();
@@ -2020,18 +1987,6 @@ EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double c
     }
   }
   k = j;
-  if (pf_m >= 0) {  // stage 3: the GT head member's fields (schedule_gt_member)
-    PREFETCH_L1(&I.prompt[pf_m]);
-    PREFETCH_L1(&I.generated[pf_m]);
-    PREFETCH_L1(&I.padded[pf_m]);
-    PREFETCH_L1(&I.held[pf_m]);
-    PREFETCH_L1(&I.flags[pf_m]);
-    PREFETCH_L1(&I.reserved[pf_m]);
-    PREFETCH_L1(&I.written[pf_m]);
-    PREFETCH_L1(&I.last_enq[pf_m]);
-    PREFETCH_L1(&I.waiting[pf_m]);
-    PREFETCH_L1(&I.preempt_t[pf_m]);
-  }
   if (my >= 0) quiet_request(I, my, e, k, clk1);
   for (int32_t i = W + LANE; i < R; i += W) {
     const int32_t id = I.run[i];
