@@ -988,16 +988,28 @@ EDEV void begin_gt_run(Inst& I, int32_t id, bool hosted) {
 }
 
 // ingest_arrivals (engine.hpp:216-235) for every arrival with t <= clock+1e-12.
-EDEVNI void ingest(Inst& I) {
-  const int64_t first = I.arrival_cursor;
-  const double lim = I.clock + 1e-12;
-  if (first >= I.n || !(I.arrival[first] <= lim)) return;
-  int64_t lo = first + 1, hi = I.n;  // first index with arrival > lim (arrivals nondecreasing)
+// First index >= first whose arrival is > lim (arrivals are nondecreasing,
+// so the due ones are a prefix): one warp probe of the next W arrivals
+// answers the usual few-arrivals case in one load; a larger batch continues
+// with a binary search.
+EDEV int64_t due_end(const Inst& I, int64_t first, double lim) {
+  const int64_t pos = first + LANE;
+  const unsigned m = BALLOT(pos < I.n && I.arrival[pos < I.n ? pos : 0] <= lim);
+  if (m != (W == 32 ? 0xffffffffu : 1u)) return first + POPC(m);  // prefix of due lanes
+  int64_t lo = first + W, hi = I.n;
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
     if (I.arrival[mid] <= lim) lo = mid + 1; else hi = mid;
   }
-  const int64_t last = lo;
+  return lo;
+}
+
+EDEVNI void ingest(Inst& I) {
+  const int64_t first = I.arrival_cursor;
+  const double lim = I.clock + 1e-12;
+  if (first >= I.n) return;
+  const int64_t last = due_end(I, first, lim);
+  if (last == first) return;
   const int64_t k = last - first;
   if (I.record_events) {
     for (int64_t i = LANE; i < k; i += W) {
@@ -1844,15 +1856,7 @@ EDEVNI void handle_idle(Inst& I) {  // engine.hpp:930-961
 // a launch stops and lets the host drain before a step could overflow.
 EDEV int64_t step_event_bound(const Inst& I) {
   int64_t arrivals = 0;
-  if (I.arrival_cursor < I.n) {
-    const double lim = I.clock + 1e-12;
-    int64_t lo = I.arrival_cursor, hi = I.n;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (I.arrival[mid] <= lim) lo = mid + 1; else hi = mid;
-    }
-    arrivals = lo - I.arrival_cursor;
-  }
+  if (I.arrival_cursor < I.n) arrivals = due_end(I, I.arrival_cursor, I.clock + 1e-12) - I.arrival_cursor;
   return arrivals + 2 * I.tfs + 4 * (I.arrival_cursor - I.completed - I.pt_count) + 2 * (int64_t)I.n_slots + 64;
 }
 

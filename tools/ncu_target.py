@@ -26,7 +26,9 @@ def main():
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--launches", type=int, default=2)
+    ap.add_argument("--workload", default=bench.WORKLOAD)
     a = ap.parse_args()
+    bench.WORKLOAD = a.workload
     traces = bench.make_traces(generate_trace, a.n, [1000 + i for i in range(a.instances)])
     b = Batch(traces, bench.options(), device=0)
     b.launch(1)
