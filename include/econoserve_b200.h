@@ -333,9 +333,10 @@ int econo_write_trace_csv(const EconoTraceRecord* trace, int64_t n, char* out, i
 uint64_t econo_trace_hash(const EconoTraceRecord* trace, int64_t n);
 /* to_json(report, with_records).dump(indent) (metrics.hpp:181-240), byte for
  * byte as nlohmann::ordered_json prints it; recs = NULL omits "records";
- * indent < 0 = compact. */
+ * config_json (NULL: none) is the report's "config" echo (config.hpp:236-285)
+ * already serialised for nesting depth 1; indent < 0 = compact. */
 int econo_report_to_json(const char* policy, const EconoReport* report, const EconoRecord* recs, int64_t n_recs,
-                         int32_t indent, char* out, int64_t cap, int64_t* len);
+                         const char* config_json, int32_t indent, char* out, int64_t cap, int64_t* len);
 /* nlohmann's double printer alone (Grisu2 digits + its layout rules). */
 int econo_json_double(double v, char* out, int64_t cap, int64_t* len);
 

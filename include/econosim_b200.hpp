@@ -464,9 +464,11 @@ inline std::string to_json_string(const MetricsReport& m, bool with_records = tr
   }
   const EconoRecord* rp = with_records ? recs.data() : nullptr;
   int64_t len = 0;
-  econo_report_to_json(m.policy.c_str(), &r, rp, static_cast<int64_t>(recs.size()), indent, nullptr, 0, &len);
+  econo_report_to_json(m.policy.c_str(), &r, rp, static_cast<int64_t>(recs.size()), nullptr, indent, nullptr, 0,
+                       &len);
   std::string s(static_cast<size_t>(len) + 1, '\0');
-  econo_report_to_json(m.policy.c_str(), &r, rp, static_cast<int64_t>(recs.size()), indent, &s[0], len + 1, &len);
+  econo_report_to_json(m.policy.c_str(), &r, rp, static_cast<int64_t>(recs.size()), nullptr, indent, &s[0], len + 1,
+                       &len);
   s.resize(static_cast<size_t>(len));
   return s;
 }

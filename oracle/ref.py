@@ -229,3 +229,47 @@ def write_csv(trace):
     buf = C.create_string_buffer(n + 1)
     lib().ref_write_csv(t.ctypes.data, len(t), buf, n + 1)
     return buf.value[:n].decode()
+
+
+def _str_call(fn, *args):
+    n = fn(*args, None, 0)
+    if n < 0:
+        return None
+    buf = C.create_string_buffer(n + 1)
+    fn(*args, buf, n + 1)
+    return buf.value[:n].decode()
+
+
+def _exp_types():
+    L = lib()
+    if not getattr(L, "_exp_typed", False):
+        L.ref_parse_config.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
+        L.ref_experiment_report.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_int64]
+        L.ref_experiment_report.restype = C.c_int64
+        L.ref_render_table.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int64]
+        L.ref_render_table.restype = C.c_int64
+        L.ref_sweep_csv.argtypes = [C.c_char_p, C.c_char_p, C.c_int64]
+        L.ref_sweep_csv.restype = C.c_int64
+        L._exp_typed = True
+    return L
+
+
+def parse_config_error(config_text):
+    """parse_config: None, or (code, message)."""
+    err = C.create_string_buffer(1024)
+    rc = _exp_types().ref_parse_config(config_text.encode(), err, 1024)
+    return None if rc == 0 else (rc, err.value.decode())
+
+
+def experiment_report(config_text, policy, with_records=True, indent=2):
+    """to_json(run_experiment(parse_config(text))[policy]).dump(indent)."""
+    return _str_call(_exp_types().ref_experiment_report, config_text.encode(), policy.encode(), int(with_records),
+                     indent)
+
+
+def render_table(config_text, baseline):
+    return _str_call(_exp_types().ref_render_table, config_text.encode(), baseline.encode())
+
+
+def sweep_csv(config_text):
+    return _str_call(_exp_types().ref_sweep_csv, config_text.encode())

@@ -36,6 +36,7 @@
 
 #define private public
 #include "econosim/engine.hpp"
+#include "econosim/sweep.hpp"
 #undef private
 
 #include "econoserve_b200.h"
@@ -646,6 +647,60 @@ int64_t ref_write_csv(const EconoTraceRecord* t, int64_t n, char* out, int64_t c
   const std::string s = oss.str();
   if (out && cap > 0) std::snprintf(out, static_cast<size_t>(cap), "%s", s.c_str());
   return static_cast<int64_t>(s.size());
+}
+
+// ---- experiment / sweep layer (config.hpp, sweep.hpp, metrics.hpp:243-318) ----
+static int64_t put_str(const std::string& s, char* out, int64_t cap) {
+  if (out && cap > 0) std::snprintf(out, static_cast<size_t>(cap), "%s", s.c_str());
+  return static_cast<int64_t>(s.size());
+}
+
+// parse_config(json): 0, or 2 with the ConfigError message.
+int ref_parse_config(const char* json, char* err, size_t errlen) {
+  try {
+    parse_config(Json::parse(json));
+    return ECONO_OK;
+  } catch (const ConfigError& e) {
+    set_err(err, errlen, e.what());
+    return ECONO_ECONFIG;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return 9;
+  }
+}
+
+// to_json(run_experiment(parse_config(json))[policy]).dump(indent); -1 on error.
+int64_t ref_experiment_report(const char* json, const char* policy, int with_records, int indent, char* out,
+                              int64_t cap) {
+  try {
+    auto reports = run_experiment(parse_config(Json::parse(json)));
+    return put_str(to_json(reports.at(policy), with_records != 0).dump(indent), out, cap);
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// render_table(compare(run_experiment(...), baseline)).
+int64_t ref_render_table(const char* json, const char* baseline, char* out, int64_t cap) {
+  try {
+    auto reports = run_experiment(parse_config(Json::parse(json)));
+    std::map<std::string, MetricsReport> by_name(reports.begin(), reports.end());
+    return put_str(render_table(compare(by_name, baseline)), out, cap);
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// write_sweep_csv(run_sweep(parse_config(json), 1)).
+int64_t ref_sweep_csv(const char* json, char* out, int64_t cap) {
+  try {
+    SweepResult r = run_sweep(parse_config(Json::parse(json)), 1);
+    std::ostringstream oss;
+    write_sweep_csv(oss, r);
+    return put_str(oss.str(), out, cap);
+  } catch (const std::exception&) {
+    return -1;
+  }
 }
 
 }  // extern "C"

@@ -384,7 +384,7 @@ int econo_json_double(double v, char* out, int64_t cap, int64_t* len) {
 }
 
 int econo_report_to_json(const char* policy, const EconoReport* r, const EconoRecord* recs, int64_t n_recs,
-                         int32_t indent, char* out, int64_t cap, int64_t* len) {
+                         const char* config_json, int32_t indent, char* out, int64_t cap, int64_t* len) {
   Json j(indent);
   j.open('{');
   j.key("policy");
@@ -433,6 +433,10 @@ int econo_report_to_json(const char* policy, const EconoReport* r, const EconoRe
   }
   j.close('}');
   j.close('}');
+  if (config_json) {  // the experiment's config echo, pre-serialised at depth 1 (metrics.hpp:220)
+    j.key("config");
+    j.s += config_json;
+  }
   if (recs) {
     j.key("records");
     j.open('[');

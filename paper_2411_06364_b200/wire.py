@@ -23,7 +23,7 @@ def _types(L):
     L.econo_trace_hash.argtypes = [vp, i64]
     L.econo_trace_hash.restype = C.c_uint64
     L.econo_json_double.argtypes = [C.c_double, cp, i64, C.POINTER(i64)]
-    L.econo_report_to_json.argtypes = [cp, C.POINTER(abi.Report), vp, i64, C.c_int32, cp, i64,
+    L.econo_report_to_json.argtypes = [cp, C.POINTER(abi.Report), vp, i64, cp, C.c_int32, cp, i64,
                                        C.POINTER(i64)]
     L._wire_typed = True
     return L
@@ -86,13 +86,15 @@ def json_double(v, lib=None):
     return _out_str(lambda o, c, n: L.econo_json_double(float(v), o, c, n))
 
 
-def report_json(report, records=None, policy="econoserve-full", indent=-1, lib=None, _L=None):
-    """to_json(report, with_records = records is not None).dump(indent)."""
+def report_json(report, records=None, policy="econoserve-full", indent=-1, lib=None, _L=None, config_json=None):
+    """to_json(report, with_records = records is not None).dump(indent); config_json: the
+    pre-serialised "config" echo (experiment.config_json)."""
     L = _types(_L) if _L is not None else _lib(lib)
     recs = None if records is None else np.ascontiguousarray(records, dtype=abi.RECORD_DTYPE)
     ptr = None if recs is None else recs.ctypes.data
     nrec = 0 if recs is None else len(recs)
-    return _out_str(lambda o, c, n: L.econo_report_to_json(policy.encode(), C.byref(report), ptr, nrec,
+    cfg = None if config_json is None else config_json.encode()
+    return _out_str(lambda o, c, n: L.econo_report_to_json(policy.encode(), C.byref(report), ptr, nrec, cfg,
                                                           indent, o, c, n))
 
 
