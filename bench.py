@@ -440,8 +440,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--instances", type=int, default=740,
-                    help="serving instances per GPU (5 per SM; ~184 MB of HBM each at 1M requests)")
+    ap.add_argument("--instances", type=int, default=888,
+                    help="serving instances per GPU (6 per SM; ~184 MB of HBM each at 1M requests: 163 GB of the 180 GB)")
     ap.add_argument("--iters", type=int, default=1000,
                     help="scheduler iterations per instance per step (one k_engine_steps launch)")
     ap.add_argument("--ref-iters", type=int, default=100,
