@@ -390,11 +390,62 @@ def run_ours(args):
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {ex}"}
     if world == 1 and not args.no_full_runs:
-        b.close()  # free the 136 GB batch before the single-engine runs
+        b.close()  # free the batch before the single-engine runs
         line["full_runs"] = full_runs(args)
+    if world == 1 and not args.no_other_workloads:
+        b.close()
+        line["other_workloads"] = other_workloads(args, stream)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def other_workloads(args, stream, launches=4):
+    """The same device-timed step on the other BASELINE.json shapes (north_star:
+    Alpaca-, ShareGPT- and BookCorpus-shaped traces): configs[1] (ShareGPT
+    100k, Poisson 28 rps, 888 instances) and configs[3] (the mixed 1M burst
+    with the lognormal predictor, 148 instances)."""
+    import torch
+
+    from paper_2411_06364_b200.engine import Batch, generate_trace
+    global WORKLOAD
+    keep = WORKLOAD
+    out = {}
+    peak, _ = measured_peaks()
+    for name, inst, n in (("cfg2_sharegpt_100k", 888, 100_000), ("cfg4_mixed_1m", 148, 1_000_000)):
+        WORKLOAD = name
+        traces = make_traces(generate_trace, n, [1000 + i for i in range(inst)], pinned=True)
+        b = Batch(traces, options(), device=0)
+        b.launch(1, stream.cuda_stream)
+        stream.synchronize()
+        b.ingest()
+        for _ in range(1 + args.warmup):
+            b.launch(args.iters, stream.cuda_stream)
+        stream.synchronize()
+        b.sync()
+        sc0 = b.scalars()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(launches):
+            b.launch(args.iters, stream.cuda_stream)
+        e1.record(stream)
+        e1.synchronize()
+        secs = e0.elapsed_time(e1) / 1e3
+        b.sync()
+        sc1 = b.scalars()
+        adm = sum(x.pt_dispatched - y.pt_dispatched for x, y in zip(sc1, sc0))
+        ab = algorithmic_bytes(sc0, sc1, args.iters * launches, inst)
+        out[name] = {"instances": inst, "requests_per_instance": n, "iters_per_step": args.iters, "steps": launches,
+                     "value": adm / secs, "unit": UNIT, "us_per_iter": 1e6 * secs / (args.iters * launches),
+                     "quiet_step_frac": (sum(x.quiet_steps - y.quiet_steps for x, y in zip(sc1, sc0)) /
+                                         max(1, sum(x.steps - y.steps for x, y in zip(sc1, sc0)))),
+                     "roofline": {"achieved": ab / secs / 1e9, "peak": peak, "unit": "GB/s",
+                                  "frac": ab / secs / 1e9 / peak},
+                     "errors": sum(1 for x in sc1 if x.error)}
+        b.close()
+        del traces
+    WORKLOAD = keep
+    return out
 
 
 def full_runs(args):
@@ -449,6 +500,8 @@ def main():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-workloads", action="store_true",
+                    help="skip the configs[1] / configs[3] step measurements")
     ap.add_argument("--no-full-runs", action="store_true",
                     help="skip the whole-run completed-req/s measurements of configs[0] and configs[1]")
     ap.add_argument("--workload", default=WORKLOAD, choices=sorted(W.CONFIGS),

@@ -2,7 +2,7 @@ set -x
 timeout 1500 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err; echo "rc=$?" >> gpurun_out/final_bench.err
 timeout 1200 python bench.py --impl reference > gpurun_out/final_ref.json 2> gpurun_out/final_ref.err; echo "rc=$?" >> gpurun_out/final_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/final_launches.csv \
-  python bench.py --no-cpu-baseline --no-full-runs > gpurun_out/final_launches_bench.json 2> gpurun_out/final_launches_bench.err
+  python bench.py --no-cpu-baseline --no-full-runs --no-other-workloads > gpurun_out/final_launches_bench.json 2> gpurun_out/final_launches_bench.err
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_engine_steps -s 5 -c 1 \
   -o gpurun_out/final_steps -f python tools/ncu_target.py --instances 64 --iters 1000 > gpurun_out/final_steps.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_radix_scatter|k_bulk_keys|k_partials_slices|k_jct_hist|k_init_req" -c 6 \
