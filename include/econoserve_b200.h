@@ -133,12 +133,15 @@ typedef struct EconoOptions {
 #define ECONO_EV_GT_SCHEDULE 1    /* "gt_schedule"  detail "rl=<a>"            E:347 */
 #define ECONO_EV_HOSTED 2         /* "hosted"       "host=<a> deadline=<b>"    E:294 */
 #define ECONO_EV_PT_DISPATCH 3    /* "pt_dispatch"                             E:380 */
-#define ECONO_EV_PREFILL_DONE 4   /* "prefill_done" "to-gt-queue"              E:803 */
+#define ECONO_EV_PREFILL_DONE 4   /* "prefill_done" "to-gt-queue" (a=0), "" for baselines (a=1) E:803,807 */
 #define ECONO_EV_COMPLETE 5       /* "complete"     "rl=<a>"                   E:851 */
 #define ECONO_EV_RESERVE_TOPUP 6  /* "reserve_topup"                           E:862 */
 #define ECONO_EV_PREEMPT 7        /* "preempt"  "<a?overrun:underprediction> l_new=<b>" E:915 */
 #define ECONO_EV_HOSTED_OVERRUN 8 /* "hosted_overrun"                          E:882 */
 #define ECONO_EV_IDLE 9           /* "idle"  id=-1  detail "<a>"               E:948 */
+#define ECONO_EV_ALLOC_FAIL 10    /* "alloc_fail"                              E:437,641 */
+#define ECONO_EV_PREEMPT_SWAP 11  /* "preempt_swap" "written=<a>"              E:474 */
+#define ECONO_EV_SWAP_IN 12       /* "swap_in"                                 E:517,592,613 */
 
 /* econosim::Event (engine.hpp:53-61) with the detail string kept as integers. */
 typedef struct EconoEvent {

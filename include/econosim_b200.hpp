@@ -243,12 +243,13 @@ inline EconoOptions to_c(const EngineOptions& o) {
 
 // Event::kind / Event::detail exactly as Engine::log writes them (engine.hpp:211-214).
 inline Event to_event(const EconoEvent& e) {
-  static const char* kinds[] = {"arrive", "gt_schedule", "hosted", "pt_dispatch", "prefill_done",
-                                "complete", "reserve_topup", "preempt", "hosted_overrun", "idle"};
+  static const char* kinds[] = {"arrive",  "gt_schedule",    "hosted", "pt_dispatch", "prefill_done",
+                                "complete", "reserve_topup", "preempt", "hosted_overrun", "idle",
+                                "alloc_fail", "preempt_swap", "swap_in"};
   Event out;
   out.iter = static_cast<long>(e.iter);
   out.clock = e.clock;
-  out.kind = (e.kind >= 0 && e.kind < 10) ? kinds[e.kind] : "?";
+  out.kind = (e.kind >= 0 && e.kind < 13) ? kinds[e.kind] : "?";
   out.id = e.id;
   switch (e.kind) {
     case ECONO_EV_GT_SCHEDULE:
@@ -256,7 +257,8 @@ inline Event to_event(const EconoEvent& e) {
     case ECONO_EV_HOSTED:
       out.detail = "host=" + std::to_string(e.a) + " deadline=" + std::to_string(e.b);
       break;
-    case ECONO_EV_PREFILL_DONE: out.detail = "to-gt-queue"; break;
+    case ECONO_EV_PREFILL_DONE: out.detail = e.a ? "" : "to-gt-queue"; break;
+    case ECONO_EV_PREEMPT_SWAP: out.detail = "written=" + std::to_string(e.a); break;
     case ECONO_EV_PREEMPT:
       out.detail = std::string(e.a ? "overrun" : "underprediction") + " l_new=" + std::to_string(e.b);
       break;

@@ -111,7 +111,9 @@ int kind_code(const std::string& k) {
       {"hosted", ECONO_EV_HOSTED},           {"pt_dispatch", ECONO_EV_PT_DISPATCH},
       {"prefill_done", ECONO_EV_PREFILL_DONE}, {"complete", ECONO_EV_COMPLETE},
       {"reserve_topup", ECONO_EV_RESERVE_TOPUP}, {"preempt", ECONO_EV_PREEMPT},
-      {"hosted_overrun", ECONO_EV_HOSTED_OVERRUN}, {"idle", ECONO_EV_IDLE}};
+      {"hosted_overrun", ECONO_EV_HOSTED_OVERRUN}, {"idle", ECONO_EV_IDLE},
+      {"alloc_fail", ECONO_EV_ALLOC_FAIL}, {"preempt_swap", ECONO_EV_PREEMPT_SWAP},
+      {"swap_in", ECONO_EV_SWAP_IN}};
   auto it = m.find(k);
   return it == m.end() ? -1 : it->second;
 }
@@ -141,6 +143,13 @@ void parse_detail(const Event& ev, EconoEvent* out) {
     }
     case ECONO_EV_IDLE:
       out->a = std::atoll(d.c_str());
+      break;
+    case ECONO_EV_PREFILL_DONE:
+      out->a = d.empty() ? 1 : 0;  // "" = a baseline prefill that keeps decoding
+      break;
+    case ECONO_EV_PREEMPT_SWAP:
+      std::sscanf(d.c_str(), "written=%lld", &a);
+      out->a = a;
       break;
     default:
       break;
@@ -385,12 +394,19 @@ int64_t ref_snapshot(void* hv, int64_t* out, int64_t cap) {
   w.push_back(e.hosted_overruns_);
   w.push_back(e.exam_count_);
   w.push_back(static_cast<int64_t>(e.reqs_.size()));
-  // PT queue
-  w.push_back(static_cast<int64_t>(e.pt_queue_.entries().size()));
-  for (const auto& pe : e.pt_queue_.entries()) w.push_back(pe.id);
-  // GT queue
-  w.push_back(static_cast<int64_t>(e.gt_queue_.groups().size()));
-  for (const auto& g : e.gt_queue_.groups()) {
+  // PT queue (the baselines' wait_fifo_ in its place)
+  const bool econo = is_econoserve(e.pol_.kind);
+  if (econo) {
+    w.push_back(static_cast<int64_t>(e.pt_queue_.entries().size()));
+    for (const auto& pe : e.pt_queue_.entries()) w.push_back(pe.id);
+  } else {
+    w.push_back(static_cast<int64_t>(e.wait_fifo_.size()));
+    for (RequestId id : e.wait_fifo_) w.push_back(id);
+  }
+  // GT queue (sync-coupled's waiting_groups_ in its place)
+  const GtQueue& gq = econo ? e.gt_queue_ : e.waiting_groups_;
+  w.push_back(static_cast<int64_t>(gq.groups().size()));
+  for (const auto& g : gq.groups()) {
     w.push_back(static_cast<int64_t>(g.group_id));
     w.push_back(g.padded_rl);
     w.push_back(bits(g.formed_at));
@@ -476,6 +492,17 @@ int64_t ref_snapshot(void* hv, int64_t* out, int64_t cap) {
     auto pit = e.penalty_extra_.find(r.id);
     w.push_back(bits(pit == e.penalty_extra_.end() ? 0.0 : pit->second));
     w.push_back(bits(r.slo_deadline));
+  }
+  if (!econo) {  // baseline-policy tail
+    w.push_back(0x42415345);
+    w.push_back(e.decode_pause_ ? 1 : 0);
+    w.push_back(e.admission_open_ ? 1 : 0);
+    w.push_back(bits(e.pending_stall_));
+    w.push_back(static_cast<int64_t>(e.admit_order_.size()));
+    for (RequestId id : e.admit_order_) w.push_back(id);
+    w.push_back(static_cast<int64_t>(e.ongoing_prefills_.size()));
+    for (RequestId id : e.ongoing_prefills_) w.push_back(id);
+    for (const Request& r : e.reqs_) w.push_back(r.prefill_target);
   }
   const int64_t n = static_cast<int64_t>(w.size());
   if (out) std::memcpy(out, w.data(), static_cast<size_t>(std::min(n, cap)) * 8);

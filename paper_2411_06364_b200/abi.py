@@ -19,7 +19,7 @@ POLICY_NAMES = {v: k for k, v in POLICIES.items()}
 PRED_MODELS = {"oracle": 0, "lognormal": 1, "bucket": 2}
 
 EV_KINDS = ["arrive", "gt_schedule", "hosted", "pt_dispatch", "prefill_done", "complete",
-            "reserve_topup", "preempt", "hosted_overrun", "idle"]
+            "reserve_topup", "preempt", "hosted_overrun", "idle", "alloc_fail", "preempt_swap", "swap_in"]
 MAX_BOUNDS = 8
 MAX_HIST = 256
 PARTIAL_WORDS = 32
@@ -232,11 +232,13 @@ def event_str(ev):
     elif k == 2:
         d = f"host={a} deadline={b}"
     elif k == 4:
-        d = "to-gt-queue"
+        d = "" if a == 1 else "to-gt-queue"
     elif k == 7:
         d = ("overrun" if a == 1 else "underprediction") + f" l_new={b}"
     elif k == 9:
         d = str(a)
+    elif k == 11:
+        d = f"written={a}"
     else:
         d = ""
     return name, d

@@ -110,7 +110,7 @@ enum { F_HOSTED = 1, F_WAS_PREEMPTED = 2, F_ALLOC_FAIL = 4, F_HAS_RESERVED = 8, 
 enum {
   ERR_NONE = 0, ERR_ALLOC_FAIL, ERR_RESERVED_DRAW, ERR_SLOT_OUTSIDE, ERR_STUCK,
   ERR_RELEASE_UNKNOWN, ERR_TABLE_OVERFLOW, ERR_INFEASIBLE_KVC, ERR_INFEASIBLE_RESERVE,
-  ERR_ARRIVAL_ORDER
+  ERR_ARRIVAL_ORDER, ERR_FIRST_BLOCK, ERR_ADMIT_BLOCK, ERR_EXACT_ADMIT
 };
 enum { STATUS_RUN = 0, STATUS_DRAIN = 1 };
 
@@ -180,6 +180,10 @@ struct Inst {
   int64_t prof[16];
   double agg_written, agg_allocated;
   int64_t agg_fs, agg_tfs_hits, agg_pt_iters;
+  // ---- baseline policies (engine.hpp:383-726; baselines.cuh) ----
+  int32_t base, batch_cap, recompute, decode_pause, admission_open, n_admo, n_ongo, _pad3;
+  int64_t chunk, max_out;
+  double swap_stall, pending_stall;
   // ---- per-request SoA (n entries) ----
   GP<const double> arrival;
   GP<const int32_t> prompt;
@@ -209,6 +213,9 @@ struct Inst {
   GP<int32_t> cd_ri, cd_abs, cd_use, cd_len, assigned;   // planner candidates
   GP<int32_t> os_host, os_hosted, os_off, os_len, os_abs;  // planner output slots
   GP<int32_t> tmp_a, tmp_b, tmp_c;
+  // ---- baseline policies: admit order (LIFO victims), ongoing chunked
+  // prefills, per-request prefill target (recompute preemption) ----
+  GP<int32_t> admo, ongo, ptarget;
   // ---- RNG (mt19937_64 x2) ----
   GP<uint64_t> mt, pmt;
   // ---- outputs ----
@@ -1004,6 +1011,7 @@ EDEV int64_t due_end(const Inst& I, int64_t first, double lim) {
   return lo;
 }
 
+template <bool B>
 EDEVNI void ingest(Inst& I) {
   const int64_t first = I.arrival_cursor;
   const double lim = I.clock + 1e-12;
@@ -1021,13 +1029,20 @@ EDEVNI void ingest(Inst& I) {
       }
     }
   }
-  {
+  if (B && I.policy == ECONO_POLICY_SYNC_COUPLED) {
+    // sync-coupled: arrivals join the waiting groups (engine.hpp:226-228)
+    for (int64_t id = first; id < last; ++id)
+      group_insert_gt(I, (int32_t)id, I.padded[id], I.slo[id], 0, I.clock);
+    LANE0(I.arrival_cursor = last; I.ev_total += k; if (I.record_events) I.ev_n += k);
+    return;
+  }
+  if (!B) {
     int64_t pm = INT64_MAX;
     for (int64_t id = first + LANE; id < last; id += W) pm = I.prompt[id] < pm ? I.prompt[id] : pm;
     pm = wmin(pm);
     LANE0(if (pm < I.pt_min_lb) I.pt_min_lb = pm);
   }
-  if (I.ordered) {
+  if (!B && I.ordered) {
     // class append in id order: peers of a class inside each warp chunk link
     // to each other; the lowest links to the class tail, the highest becomes it.
     for (int64_t base = first; base < last; base += W) {
@@ -1062,6 +1077,9 @@ EDEVNI void ingest(Inst& I) {
       WSYNC();
     }
   } else {
+    // FIFO PT queue, or the baselines' wait_fifo_ (engine.hpp:229-230): a
+    // sorted id set (arrivals append in id order, preemptions re-insert at
+    // lower_bound), leaves hold the forward-size demand (the prompt).
     for (int64_t id = first + LANE; id < last; id += W) I.tree[id] = I.prompt[id];
     WSYNC();
     tree_fix(I, first, last - 1);
@@ -1363,9 +1381,13 @@ EDEV bool slot_fits(const Inst& I, int32_t host, int32_t abs, int32_t len) {
   return false;
 }
 
-EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
-  // ---- select_gt_groups (queues.hpp:220-263) ----
-  [[maybe_unused]] const int64_t tp0 = PHASE_NOW();
+// select_gt_groups (queues.hpp:220-263) over the GT queue — econoserve's
+// gt_queue_ or sync-coupled's waiting_groups_ (engine.hpp:712-713): takes
+// whole groups in key order while their cached demand fits the free KVC,
+// splits the first misfit member by member and stops. Selected ids go to
+// I.sel_ids, group bounds to I.selg_start / I.selg_rl; returns the number of
+// selected groups, *nsel_out the number of members.
+EDEVNI int32_t select_gt(Inst& I, int32_t* nsel_out) {
   int32_t nsel = 0, nselg = 0, whole = 0;
   if (I.free_total > 0) {
     Tok remaining = I.free_total;
@@ -1375,7 +1397,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
       const Tok total = I.gr_dem[g];  // the group's fields load together
       const int32_t cnt = I.gr_cnt[g], head = I.gr_head[g], grl = I.gr_rl[g];
       LANE0(I.exam_count++);
-      if (nsel + cnt > I.sel_cap && total <= remaining) { set_error(I, ERR_TABLE_OVERFLOW, g, 8); return; }
+      if (nsel + cnt > I.sel_cap && total <= remaining) { set_error(I, ERR_TABLE_OVERFLOW, g, 8); return 0; }
       if (total <= remaining) {
         remaining -= total;
         if (LANE == 0) {
@@ -1431,6 +1453,16 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     }
   }
   LANE0(I.selg_start[nselg] = nsel);
+  *nsel_out = nsel;
+  return nselg;
+}
+
+EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
+  // ---- select_gt_groups (queues.hpp:220-263) ----
+  [[maybe_unused]] const int64_t tp0 = PHASE_NOW();
+  int32_t nsel = 0;
+  const int32_t nselg = select_gt(I, &nsel);
+  if (I.error) return;
   for (int32_t i = 0; i < nsel; ++i) {
     schedule_gt_member(I, I.sel_ids[i]);
     if (I.error) return;
@@ -1560,6 +1592,8 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
   PHASE_ADD(9, PHASE_NOW() - tp2);
 }
 
+#include "baselines.cuh"
+
 EDEVNI void vacate_slot(Inst& I, int32_t id, bool* rehomed) {  // engine.hpp:888-902
   const Tok in_slot = tmin((Tok)I.generated[id] - I.gen_epoch[id], (Tok)I.padded[id]);
   bool rh = false;
@@ -1574,7 +1608,9 @@ EDEVNI void vacate_slot(Inst& I, int32_t id, bool* rehomed) {  // engine.hpp:888
   *rehomed = rh;
 }
 
+template <bool B>
 EDEVNI void preempt_and_regroup(Inst& I, int32_t id, int why) {  // engine.hpp:904-928
+  if (B) list_erase(I.admo, &I.n_admo, id);
   if (LANE == 0) {
     I.preempt_count[id]++;
     I.state[id] = ST_PREEMPTED;
@@ -1587,11 +1623,16 @@ EDEVNI void preempt_and_regroup(Inst& I, int32_t id, int why) {  // engine.hpp:9
   WSYNC();
   logev(I, ECONO_EV_PREEMPT, id, why, I.padded[id]);
   LANE0(I.state[id] = ST_WAITING_GT);
+  if (B && I.policy != ECONO_POLICY_SYNC_COUPLED) {
+    wait_insert(I, id);
+    return;
+  }
   group_insert_gt(I, id, I.padded[id], I.slo[id], I.occupied[id], I.clock);
 }
 
+template <bool B>
 EDEVNI void handle_underprediction(Inst& I, int32_t id) {  // engine.hpp:856-873
-  if (kvc_draw_reserved(I, id, I.block)) {
+  if (!B && kvc_draw_reserved(I, id, I.block)) {
     LANE0(I.allowance[id] += (int32_t)I.block; I.reserve_draws[id]++;
           I.penalty[id] += I.reserve_penalty);
     logev(I, ECONO_EV_RESERVE_TOPUP, id, 0, 0);
@@ -1602,7 +1643,7 @@ EDEVNI void handle_underprediction(Inst& I, int32_t id) {  // engine.hpp:856-873
   bool rehomed = true;
   if (I.flags[id] & F_HOSTED) vacate_slot(I, id, &rehomed);
   LANE0(I.penalty[id] += rehomed ? I.pen_free : I.pen_offload);
-  preempt_and_regroup(I, id, 0);
+  preempt_and_regroup<B>(I, id, 0);
 }
 
 EDEVNI void handle_hosted_overrun(Inst& I, int32_t id) {  // engine.hpp:875-884
@@ -1613,7 +1654,7 @@ EDEVNI void handle_hosted_overrun(Inst& I, int32_t id) {  // engine.hpp:875-884
         I.alloc_failures++);
   logev(I, ECONO_EV_HOSTED_OVERRUN, id, 0, 0);
   WSYNC();
-  preempt_and_regroup(I, id, 1);
+  preempt_and_regroup<false>(I, id, 1);
 }
 
 // Stable compaction of the running list to RUNNING requests.
@@ -1632,10 +1673,12 @@ EDEV void run_compact(Inst& I) {
   LANE0(I.R = w);
 }
 
+template <bool B>
 EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   [[maybe_unused]] const int64_t tx0 = PHASE_NOW();
-  const double dt = iteration_time(I, fs) + 0.0;
-  LANE0(I.clock += dt; I.iter++);
+  const double dt = iteration_time(I, fs) + (B ? I.pending_stall : 0.0);
+  LANE0(I.clock += dt; I.iter++; if (B) I.pending_stall = 0.0);
+  const bool pause = B && I.decode_pause;
   const double sched = (double)I.exam_count * I.sched_cost;
   if (I.n_adm > 0 && sched > 0.0) {
     const double share = sched / (double)I.n_adm;
@@ -1647,7 +1690,8 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     const int32_t id = I.ptiter_id[i];
     const int32_t tk = I.ptiter_tok[i];
     const double e = I.exec_t[id];
-    const int32_t pd = I.prefill_done[id] + tk, wr = I.written[id], oc = I.occupied[id], pr = I.prompt[id];
+    const int32_t pd = I.prefill_done[id] + tk, wr = I.written[id], oc = I.occupied[id];
+    const int32_t pr = B ? I.ptarget[id] : I.prompt[id];
     const uint8_t f = I.flags[id];
     I.exec_t[id] = e + dt;
     I.prefill_done[id] = pd;
@@ -1658,7 +1702,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   }
   wsum_pt = wsum(wsum_pt);
   // every running GT writes exactly one token this iteration
-  LANE0(I.written_total += wsum_pt + I.R);
+  LANE0(I.written_total += wsum_pt + (pause ? 0 : I.R));
   EconoSample s;
   s.iter = I.iter;
   s.clock = I.clock;
@@ -1687,7 +1731,13 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     const int32_t i = base + LANE;
     const int32_t id = i < R0 ? I.run[i] : -1;
     bool fin = false, under = false;
-    if (id >= 0) {
+    if (pause && id >= 0) {  // vLLM prefill-only iteration: decodes stall (engine.hpp:744-749)
+      const double wt = I.waiting[id];
+      const int32_t g = I.generated[id], tr = I.true_rl[id], al = I.allowance[id];
+      I.waiting[id] = wt + dt;
+      fin = g >= tr;
+      under = g >= al && g < tr;
+    } else if (id >= 0) {
       const double e = I.exec_t[id];
       const int32_t g = I.generated[id] + 1;
       const int32_t oc = I.occupied[id], wr = I.written[id], tr = I.true_rl[id], al = I.allowance[id];
@@ -1713,6 +1763,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
       kvc_release(I, cid);
       if (I.error) return;
       LANE0(I.occupied[cid] = 0; I.completed++);
+      if (B) list_erase(I.admo, &I.n_admo, cid);
       logev(I, ECONO_EV_COMPLETE, cid, I.generated[cid], 0);
       WSYNC();
       completed_now++;
@@ -1733,6 +1784,13 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     WSYNC();
     LANE0(I.flags[id] = (uint8_t)(f & ~F_PREFILL_FIN));
     if (st != ST_RUNNING) continue;
+    if constexpr (B) {  // baselines keep decoding (engine.hpp:805-808)
+      list_erase(I.ongo, &I.n_ongo, id);
+      LANE0(I.gen_epoch[id] = gen; I.run[I.R++] = id);
+      logev(I, ECONO_EV_PREFILL_DONE, id, 1, 0);
+      WSYNC();
+      continue;
+    }
     LANE0(I.state[id] = ST_WAITING_GT; I.last_enq[id] = I.clock);
     // gt_member_demand (engine.hpp:238-247) from the fields loaded above
     const Tok tgt = block_round((Tok)pr + gen + pad, I.block);
@@ -1748,7 +1806,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   for (int32_t k = 0; k < npre; ++k) {
     const int32_t id = I.tmp_a[k];
     if (I.state[id] != ST_RUNNING) continue;
-    handle_underprediction(I, id);
+    handle_underprediction<B>(I, id);
     if (I.error) return;
   }
   // hosted-slot deadlines over a copy of the slot list (engine.hpp:819-828)
@@ -1799,6 +1857,10 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     I.exam_count = 0;
     I.pts_admitted_iter = 0;
     I.pt_admittable = 0;
+    if (B) {
+      I.admission_open = I.admission_open || completed_now > 0;
+      I.decode_pause = 0;
+    }
 #ifdef ECONO_PROF_PHASES
     I.prof[15] += PROF_NOW() - tx3;
 #endif
@@ -1857,6 +1919,8 @@ EDEVNI void handle_idle(Inst& I) {  // engine.hpp:930-961
 EDEV int64_t step_event_bound(const Inst& I) {
   int64_t arrivals = 0;
   if (I.arrival_cursor < I.n) arrivals = due_end(I, I.arrival_cursor, I.clock + 1e-12) - I.arrival_cursor;
+  if (I.base)  // every admitted or queued request: swap-in, dispatch, alloc_fail, preempt_swap, ...
+    return arrivals + 2 * I.tfs + 8 * (I.arrival_cursor - I.completed) + 64;
   return arrivals + 2 * I.tfs + 4 * (I.arrival_cursor - I.completed - I.pt_count) + 2 * (int64_t)I.n_slots + 64;
 }
 
@@ -2082,17 +2146,18 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
   return k;
 }
 
+template <bool B>
 EDEVNI void engine_step(Inst& I) {  // Engine::step (engine.hpp:104-116)
   [[maybe_unused]] const int64_t t0 = PHASE_NOW();
-  ingest(I);
+  ingest<B>(I);
   PHASE_ADD(6, PHASE_NOW() - t0);
-  form_econoserve(I);
+  if (B) form_baseline(I); else form_econoserve(I);
   if (I.error) return;
   [[maybe_unused]] const int64_t t1 = PHASE_NOW();
   Tok fs = 0;
   for (int32_t i = LANE; i < I.n_ptiter; i += W) fs += I.ptiter_tok[i];
-  fs = wsum(fs) + I.R;
-  if (fs == 0) handle_idle(I); else execute_iteration(I, fs);
+  fs = wsum(fs) + ((B && I.decode_pause) ? 0 : I.R);
+  if (fs == 0) handle_idle(I); else execute_iteration<B>(I, fs);
   PHASE_ADD(10, PHASE_NOW() - t1);
   LANE0(I.steps++);
 }

@@ -68,6 +68,13 @@ EDEVNI void init_predict_sequential(Inst& I) {
     for (int32_t i = 0; i < I.n; ++i) I.predicted[i] = (int32_t)predict_rl(I, I.true_rl[i], I.pmt, I.pmt_i);
   WSYNC();
 }
+// Worst-case KVC demand of request i (engine.hpp:193-197): Orca reserves the
+// maximum output length, every other policy the larger of the true and
+// padded lengths.
+EDEV Tok worst_demand(const Inst& I, int64_t i) {
+  const Tok out = I.policy == ECONO_POLICY_ORCA ? I.max_out : tmax(I.true_rl[i], I.padded[i]);
+  return block_round((Tok)I.prompt[i] + out, I.block);
+}
 // Phase 3: per-request fields + feasibility (engine.hpp:186-206).
 EDEV bool init_req_one(Inst& I, int64_t i) {
   if (I.pred_model == ECONO_PRED_ORACLE) I.predicted[i] = (int32_t)quantize_up(I.true_rl[i], I.pred_quantum);
@@ -81,8 +88,8 @@ EDEV bool init_req_one(Inst& I, int64_t i) {
   I.reg_tail[i] = -1;
   I.pt_next[i] = -1;
   I.gt_next[i] = -1;
-  const Tok worst = block_round((Tok)I.prompt[i] + tmax(I.true_rl[i], I.padded[i]), I.block);
-  return worst > I.general_cap || (Tok)I.prompt[i] > I.reserve_cap;
+  if (I.base) I.ptarget[i] = I.prompt[i];  // prefill_target = prompt_len (engine.hpp:189)
+  return worst_demand(I, i) > I.general_cap || (!I.base && (Tok)I.prompt[i] > I.reserve_cap);
 }
 // Table initialisation for index i of every table.
 EDEV void init_tables_one(Inst& I, int64_t i) {
@@ -108,7 +115,7 @@ EDEV int64_t init_table_extent(const Inst& I) {
 EDEV void init_finish(Inst& I, int64_t first_bad) {
   if (first_bad < I.n) {
     const int32_t bad = (int32_t)first_bad;
-    const Tok worst = block_round((Tok)I.prompt[bad] + tmax(I.true_rl[bad], I.padded[bad]), I.block);
+    const Tok worst = worst_demand(I, bad);
     I.error = worst > I.general_cap ? ERR_INFEASIBLE_KVC : ERR_INFEASIBLE_RESERVE;
     I.err_id = bad;
     I.err_val = worst > I.general_cap ? worst : I.reserve_cap;
@@ -125,6 +132,7 @@ EDEV void init_finish(Inst& I, int64_t first_bad) {
 // the budget), and a step after a completion finds freed KVC for the GT
 // queue head. Skipping the test is always exact — it only decides whether a
 // replay may stand in for normal steps.
+template <bool B>
 EDEVNI void engine_steps(Inst& I, int64_t max_steps) {
   LANE0(I.status = STATUS_RUN);
   bool test = true;
@@ -135,7 +143,7 @@ EDEVNI void engine_steps(Inst& I, int64_t max_steps) {
       LANE0(I.status = STATUS_DRAIN);
       break;
     }
-    if (I.skip && test) {
+    if (!B && I.skip && test) {
       const int64_t t0 = PROF_NOW();
       const int64_t k = quiet_span(I, max_steps - s);
       const int64_t t1 = PROF_NOW();
@@ -149,7 +157,7 @@ EDEVNI void engine_steps(Inst& I, int64_t max_steps) {
     }
     const int64_t t2 = PROF_NOW();
     const int64_t c0 = I.completed;
-    engine_step(I);
+    engine_step<B>(I);
     LANE0(I.prof[2] += PROF_NOW() - t2; I.prof[5]++);
     test = I.completed == c0;
     ++s;
@@ -358,11 +366,22 @@ __global__ void __launch_bounds__(32) k_init_finish(Inst* insts, const unsigned 
 }
 
 __global__ void __launch_bounds__(32) k_engine_steps(Inst* insts, int64_t max_steps) {
+  if (insts[blockIdx.x].base) return;  // a baseline-policy instance (k_baseline_steps)
   __shared__ Inst I;
   const int64_t t0 = PROF_NOW();
   inst_load(I, &insts[blockIdx.x]);
-  engine_steps(I, max_steps);
+  engine_steps<false>(I, max_steps);
   LANE0(I.prof[11] += PROF_NOW() - t0; I.prof[12]++);
+  inst_store(&insts[blockIdx.x], I);
+}
+
+// The comparison policies (orca, vllm, sarathi, multires, sync-coupled) in
+// their own kernel, so the econoserve kernel's code is not affected by them.
+__global__ void __launch_bounds__(32) k_baseline_steps(Inst* insts, int64_t max_steps) {
+  if (!insts[blockIdx.x].base) return;
+  __shared__ Inst I;
+  inst_load(I, &insts[blockIdx.x]);
+  engine_steps<true>(I, max_steps);
   inst_store(&insts[blockIdx.x], I);
 }
 
@@ -868,6 +887,10 @@ void layout(Inst& I, char* base, size_t* bytes) {
                     &I.cd_ri, &I.cd_abs, &I.cd_use, &I.cd_len, &I.assigned,
                     &I.os_host, &I.os_hosted, &I.os_off, &I.os_len, &I.os_abs, &I.tmp_a, &I.tmp_b, &I.tmp_c};
   for (auto p : pl) *p = a.take<int32_t>(pc);
+  // baseline policies only (admit order <= running + this iteration's PTs)
+  I.admo = a.take<int32_t>(I.base ? (int64_t)I.run_cap + I.ptiter_cap + W : 1);
+  I.ongo = a.take<int32_t>(I.base ? (int64_t)I.run_cap + I.ptiter_cap + W : 1);
+  I.ptarget = a.take<int32_t>(I.base ? n : 1);
   I.mt = a.take<uint64_t>(312);
   I.pmt = a.take<uint64_t>(312);
   I.hist = a.take<int64_t>(I.hist_cap);
@@ -886,12 +909,6 @@ void rebase(Inst& I, const char* from, char* to, size_t bytes) {
       memcpy(p, &v, sizeof(v));
     }
   }
-}
-
-const char* policy_name(int k) {
-  static const char* names[] = {"orca", "vllm", "sarathi", "multires", "sync-coupled",
-                                "econoserve-d", "econoserve-sd", "econoserve-sdo", "econoserve-full"};
-  return k >= 0 && k <= 8 ? names[k] : "?";
 }
 
 // Option validation in the reference constructor's order (engine.hpp:81-100).
@@ -930,11 +947,8 @@ int validate(const EconoOptions* o, int64_t n, char* err, size_t errlen) {
   if (o->pred_padding_ratio < 0.0) return set_err(err, errlen, "padding_ratio must be >= 0"), ECONO_ECONFIG;
   if (o->pred_quantum < 1) return set_err(err, errlen, "predictor quantum must be >= 1"), ECONO_ECONFIG;
   if (n <= 0) return set_err(err, errlen, "trace is empty"), ECONO_ECONFIG;
-  if (!econo)
-    return set_err(err, errlen,
-                   "policy '%s' is outside the B200 scheduling path (econoserve-d/-sd/-sdo/-full only)",
-                   policy_name(o->policy)),
-           ECONO_ECONFIG;
+  if (o->policy < ECONO_POLICY_ORCA || o->policy > ECONO_POLICY_ECONO_FULL)
+    return set_err(err, errlen, "unknown policy code %d", o->policy), ECONO_ECONFIG;
   if (o->kvc_capacity >= (int64_t)1 << 30)
     return set_err(err, errlen, "kvc capacity must be < 2^30 tokens on the device path"), ECONO_ECONFIG;
   return ECONO_OK;
@@ -958,6 +972,18 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   I.policy = o->policy;
   I.ordered = o->policy == ECONO_POLICY_ECONO_SDO || o->policy == ECONO_POLICY_ECONO_FULL;
   I.grouping = o->policy != ECONO_POLICY_ECONO_D;
+  I.base = o->policy < ECONO_POLICY_ECONO_D ? 1 : 0;
+  I.batch_cap = o->batch_size_cap;
+  I.recompute = o->vllm_recompute ? 1 : 0;
+  I.chunk = o->chunk_size;
+  I.swap_stall = o->swap_stall;
+  I.admission_open = 1;
+  {  // max_output_len <= 0 derives it from the trace (engine.hpp:178-180)
+    int64_t mt = 0;
+    if (o->max_output_len <= 0)
+      for (int64_t i = 0; i < n; ++i) mt = imax(mt, t[i].true_rl);
+    I.max_out = o->max_output_len > 0 ? o->max_output_len : mt;
+  }
   I.full = o->policy == ECONO_POLICY_ECONO_FULL;
   I.pred_model = o->pred_model;
   I.nbd = o->n_deadline_bounds;
@@ -971,7 +997,8 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   I.tfs = o->tfs;  // cost_.tfs = pol_.tfs (engine.hpp:98)
   I.capacity = o->kvc_capacity;
   I.block = o->kvc_block_size;
-  I.reserve_cap = (int64_t)llround(o->reserved_fraction * (double)o->kvc_capacity);
+  // the reserved pool exists for the econoserve family only (engine.hpp:86-87)
+  I.reserve_cap = I.base ? 0 : (int64_t)llround(o->reserved_fraction * (double)o->kvc_capacity);
   I.general_cap = I.capacity - I.reserve_cap;
   I.pred_quantum = o->pred_quantum;
   I.t_base = o->t_base;
@@ -989,7 +1016,7 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   I.buffer_ratio = o->buffer_ratio;
   I.free_total = I.general_cap;
   I.pt_min_lb = INT64_MAX;
-  I.skip = getenv("ECONO_NO_SKIP") ? 0 : 1;
+  I.skip = (getenv("ECONO_NO_SKIP") || I.base) ? 0 : 1;
   // capacities
   I.pmax = (int32_t)pmax;
   I.nbuckets = I.nbd + 1;
@@ -1017,7 +1044,8 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   I.grp_cap = (int32_t)(imin(n, cap) + 1);
   I.slot_cap = (int32_t)(imin(n, cap) + 1);
   I.run_cap = (int32_t)(imin(n, cap) + 1);
-  I.ptiter_cap = (int32_t)(imin(n, I.tfs) + 2);
+  // Orca's PTs are bounded by its batch cap and the pool, not tfs
+  I.ptiter_cap = (int32_t)(imin(n, I.base ? I.tfs + cap : I.tfs) + 2);
   I.adm_cap = (int32_t)(imin(n, cap + I.tfs) + 2);
   // Scratch bounds: selected GT members <= 2*general_cap (each
   // has a positive block demand or holds a region of >= 1 token); planner
@@ -1066,6 +1094,15 @@ std::string format_error(const Inst& I, int* code) {
       *code = ECONO_ECONFIG;
       snprintf(buf, sizeof(buf), "trace arrival times must be nondecreasing");
       break;
+    case ERR_FIRST_BLOCK:
+      snprintf(buf, sizeof(buf), "first block grant failed unexpectedly");
+      break;
+    case ERR_ADMIT_BLOCK:
+      snprintf(buf, sizeof(buf), "admission block grant failed unexpectedly");
+      break;
+    case ERR_EXACT_ADMIT:
+      snprintf(buf, sizeof(buf), "exact allocation failed for admitted request %d", I.err_id);
+      break;
     default:
       snprintf(buf, sizeof(buf), "unknown engine error %d", I.error);
   }
@@ -1103,6 +1140,7 @@ struct econo_batch {
   void* bulk_buf = nullptr;
   size_t bulk_bytes = 0;
   int64_t keys_total = 0;
+  int64_t n_base = 0;  // baseline-policy instances (k_baseline_steps)
   std::vector<uint64_t> h_keys;  // host build
 #ifndef ECONO_HOSTSIM
   cudaStream_t stream = nullptr;
@@ -1187,11 +1225,16 @@ int drain(HostInst& h) {
 void launch_steps(econo_batch* b, int64_t max_steps, void* stream) {
 #ifdef ECONO_HOSTSIM
   (void)stream;
-  for (auto& h : b->inst) engine_steps(h.desc, max_steps);
+  for (auto& h : b->inst) {
+    if (h.desc.base) engine_steps<true>(h.desc, max_steps);
+    else engine_steps<false>(h.desc, max_steps);
+  }
   push_descs(b);
 #else
   cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
-  k_engine_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps);
+  if (b->n_base < (int64_t)b->inst.size())
+    k_engine_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps);
+  if (b->n_base > 0) k_baseline_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps);
 #endif
 }
 
@@ -1501,6 +1544,7 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     h.seed = opts[i].seed;
     h.pred_seed = opts[i].pred_seed;
     h.policy = opts[i].policy;
+    b->n_base += h.desc.base;
     size_t bytes = 0;
     layout(h.desc, nullptr, &bytes);
     h.arena_bytes = (bytes + 4095) & ~size_t(4095);
@@ -2263,9 +2307,9 @@ int64_t econo_snapshot(econo_engine* e, int64_t* out, int64_t cap) {
     for (int b = 0; b < I.nbuckets; ++b)
       for (int p = I.pmax; p >= 0; --p)
         for (int32_t id = I.cls_head[b * (I.pmax + 1) + p]; id >= 0; id = I.pt_next[id]) ptq.push_back(id);
-  } else {
-    for (int64_t id = 0; id < I.arrival_cursor; ++id)
-      if (I.state[id] == ST_WAITING_PT) ptq.push_back(id);
+  } else {  // FIFO PT queue / the baselines' wait_fifo_: present tree leaves in id order
+    for (int64_t id = 0; id < I.n; ++id)
+      if (I.tree[id] != INF32) ptq.push_back(id);
   }
   w.push_back((int64_t)ptq.size());
   w.insert(w.end(), ptq.begin(), ptq.end());
@@ -2360,6 +2404,17 @@ int64_t econo_snapshot(econo_engine* e, int64_t* out, int64_t cap) {
     w.push_back(bits(I.sched_share[i]));
     w.push_back(bits(I.penalty[i]));
     w.push_back(bits(I.slo[i]));
+  }
+  if (I.base) {  // baseline-policy tail
+    w.push_back(0x42415345);
+    w.push_back(I.decode_pause);
+    w.push_back(I.admission_open);
+    w.push_back(bits(I.pending_stall));
+    w.push_back(I.n_admo);
+    for (int32_t k = 0; k < I.n_admo; ++k) w.push_back(I.admo[k]);
+    w.push_back(I.n_ongo);
+    for (int32_t k = 0; k < I.n_ongo; ++k) w.push_back(I.ongo[k]);
+    for (int32_t i = 0; i < I.n; ++i) w.push_back(I.ptarget[i]);
   }
   const int64_t nwords = (int64_t)w.size();
   if (out) memcpy(out, w.data(), sizeof(int64_t) * (size_t)imin(nwords, cap));

@@ -350,16 +350,9 @@ class Result:
         return float(getattr(self.report, name))
 
 
-def _check_runnable(policies):
-    for p in policies:
-        if not p.startswith("econoserve-"):
-            raise ConfigError(f"policy '{p}' is outside the B200 scheduling path (econoserve-d/-sd/-sdo/-full only)")
-
-
 def run_experiment(cfg, device=0, lib=None):
     """run_experiment (config.hpp:320-330): every configured policy on the
     shared trace; {policy: Result} in the reference's std::map order."""
-    _check_runnable(cfg["policies"])
     trace = materialize_trace(cfg)
     out = {}
     for name in cfg["policies"]:
@@ -411,7 +404,6 @@ def run_sweep(cfg, device=0, lib=None):
     engine per worker thread. Returns (axes, [(cell, {policy: Result})]) in
     cell order; reports are exact (finalize + aggregate per instance)."""
     from .engine import Batch
-    _check_runnable(cfg["policies"])
     axes, cells = expand_sweep(cfg)
     cell_cfgs = [apply_cell(cfg, c) for c in cells]
     traces, opts, keys = [], [], []

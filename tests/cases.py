@@ -54,3 +54,42 @@ def catalogue(gen):
                        ("sd-lognormal0.3", dict(policy="econoserve-sd", pred_sigma=0.3))]:
         cases.append((f"mixed-cfg4-{tag}", mx, abi.default_options(**dict(m["opts"], **extra))))
     return cases
+
+
+BASELINES = ["orca", "vllm", "sarathi", "multires", "sync-coupled"]
+
+
+def baseline_catalogue(gen):
+    """The comparison policies (engine.hpp:383-726) on the reference's own
+    test traces and the BASELINE config shapes; checked against the compiled
+    reference (oracle/_ref)."""
+    cases = []
+    tr = sat_trace(gen, 300, 40.0, 8, 64, 8, 96, 3)  # test_engine.cpp:110-125
+    for k in BASELINES:
+        cases.append((f"determinism-{k}", tr, base_options(
+            k, pred_model="lognormal", pred_sigma=0.3, pred_padding_ratio=0.1)))
+    tr = sat_trace(gen, 120, 200.0, 16, 64, 32, 128, 59)  # test_engine.cpp:272-283 (tight cache)
+    cases.append(("pressure-vllm", tr, base_options("vllm", kvc_capacity=2048)))
+    cases.append(("pressure-vllm-stall", tr, base_options("vllm", kvc_capacity=2560, swap_stall=0.002)))
+    cases.append(("pressure-sarathi-chunk48", tr, base_options(
+        "sarathi", kvc_capacity=2048, chunk_size=48, swap_stall=0.001)))
+    cases.append(("pressure-sarathi-recompute", tr, base_options(
+        "sarathi", kvc_capacity=2048, chunk_size=40, vllm_recompute=1)))
+    tr = sat_trace(gen, 40, 1000.0, 8, 32, 8, 32, 53)  # test_engine.cpp:254-270
+    cases.append(("orca-cap8", tr, base_options("orca", batch_size_cap=8)))
+    cases.append(("orca-cap3-maxout", tr, base_options("orca", batch_size_cap=3, max_output_len=40)))
+    tr = sat_trace(gen, 200, 40.0, 8, 40, 16, 120, 31)  # test_engine.cpp:181-206 shape
+    for k in ["multires", "sync-coupled", "orca"]:
+        cases.append((f"underprediction-{k}", tr, base_options(
+            k, pred_model="lognormal", pred_sigma=0.6, kvc_capacity=4096)))
+    tr = sat_trace(gen, 300, 80.0, 8, 48, 16, 64, 47)  # test_engine.cpp:243-252
+    cases.append(("gt-domination-sync-coupled", tr, base_options("sync-coupled")))
+    c = W.CONFIGS["cfg1_alpaca_10k"]
+    a = gen(3000, 400.0, c["shape"]["prompt"], c["shape"]["rl"], 5)
+    for pol in ["vllm", "sarathi", "multires"]:
+        cases.append((f"alpaca400-{pol}", a, abi.default_options(**dict(c["opts"], policy=pol))))
+    m = W.CONFIGS["cfg4_mixed_1m"]
+    mx = W.make_trace("cfg4_mixed_1m", gen, n=600, seed=7)
+    for pol in BASELINES:
+        cases.append((f"mixed-cfg4-{pol}", mx, abi.default_options(**dict(m["opts"], policy=pol, pred_sigma=0.3))))
+    return cases

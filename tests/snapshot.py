@@ -59,5 +59,13 @@ def decode(w):
         r = {k: (_f(v) if k in FLOAT_FIELDS else v) for k, v in zip(REQ_FIELDS, vals)}
         reqs.append(r)
     d["requests"] = reqs
+    if p < len(w):  # baseline-policy tail
+        assert take() == 0x42415345, "bad baseline tail magic"
+        d["decode_pause"], d["admission_open"], stall = take(3)
+        d["pending_stall"] = _f(stall)
+        d["admit_order"] = [take() for _ in range(take())]
+        d["ongoing_prefills"] = [take() for _ in range(take())]
+        for r in reqs:
+            r["prefill_target"] = take()
     assert p == len(w), "trailing words in snapshot"
     return d

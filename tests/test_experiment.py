@@ -102,10 +102,33 @@ def test_config_errors_match_reference(k):
     assert str(ex.value) == want[1]
 
 
-def test_baseline_policies_are_rejected():
-    cfg = X.parse_config(dict(BASE, policies=["econoserve-full", "vllm"]))
-    with pytest.raises(ConfigError, match="outside the B200 scheduling path"):
-        X.run_experiment(cfg, lib=HOSTSIM)
+ALL = ["orca", "vllm", "sarathi", "multires", "sync-coupled", "econoserve-d", "econoserve-sd",
+       "econoserve-sdo", "econoserve-full"]
+
+
+@pytest.mark.parametrize("backend", BACK)
+def test_every_policy_report_and_table_match_reference(backend):
+    """All nine policies in one run (one batch: the baselines run in their own
+    kernel), the per-policy JSON reports and the comparison table against
+    vllm, the reference's usual baseline (tests/cli_tests.cpp:61-66)."""
+    j = dict(BASE, policies=ALL)
+    text = json.dumps(j)
+    cfg = X.parse_config(json.loads(text))
+    res = X.run_experiment(cfg, lib=_lib(backend))
+    assert list(res) == sorted(ALL)
+    for pol, r in res.items():
+        want = ref.experiment_report(text, pol, True, 2)
+        assert X.report_json(cfg, r, with_records=True, indent=2, lib=_lib(backend)) == stock_nlohmann(want), pol
+    assert X.render_table(res, "vllm") == ref.render_table(text, "vllm")
+
+
+@pytest.mark.parametrize("backend", BACK)
+def test_sweep_with_baselines_matches_reference(backend):
+    j = dict(BASE, policies=["vllm", "sarathi", "econoserve-full"],
+             sweep={"padding_ratio": [0.0, 0.2], "arrival_rate": [40.0, 90.0]})
+    text = json.dumps(j)
+    axes, cells = X.run_sweep(X.parse_config(json.loads(text)), lib=_lib(backend))
+    assert X.write_sweep_csv(axes, cells) == ref.sweep_csv(text)
 
 
 def test_cli_gen_trace_and_config_error(tmp_path, capsys):

@@ -232,9 +232,11 @@ def test_arrival_order_and_empty_trace(backend):  # engine.hpp:97, 167-169
 
 
 @pytest.mark.parametrize("backend", ["hostsim", pytest.param("device", marks=pytest.mark.gpu)])
-def test_non_econoserve_policy_rejected(backend):
-    with pytest.raises(ConfigError, match="outside the B200 scheduling path"):
-        make_engine(backend, [(0.1, 10, 10)], base_options("vllm"))
+def test_unknown_policy_code_rejected(backend):
+    o = base_options("vllm")
+    o.policy = 9
+    with pytest.raises(ConfigError, match="unknown policy code 9"):
+        make_engine(backend, [(0.1, 10, 10)], o)
 
 
 @pytest.mark.parametrize("backend", BACKENDS)
