@@ -395,6 +395,9 @@ def run_ours(args):
     if world == 1 and not args.no_other_workloads:
         b.close()
         line["other_workloads"] = other_workloads(args, stream)
+    if world == 1 and not args.no_policy_sweep:
+        b.close()
+        line["policy_sweep"] = policy_sweep(args)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -445,6 +448,64 @@ def other_workloads(args, stream, launches=4):
         b.close()
         del traces
     WORKLOAD = keep
+    return out
+
+
+POLICIES = ["orca", "vllm", "sarathi", "multires", "sync-coupled", "econoserve-d", "econoserve-sd",
+            "econoserve-sdo", "econoserve-full"]
+
+
+def policy_sweep(args, inst=888):
+    """The experiment layer's use case: every policy of the reference
+    (policies.hpp:24-37, the five baselines included) run to completion on
+    `inst` configs[0] instances (Alpaca 10k at 36 rps, trace seeds 1000+i),
+    one batch per policy, wall clock around the launches. Beside it, the
+    reference runs one such instance per policy on one host core; its
+    all-cores rate assumes perfect scaling over the host's cores (run_sweep's
+    thread pool, sweep.hpp:112-149)."""
+    from paper_2411_06364_b200.engine import Batch, generate_trace
+    c = W.CONFIGS["cfg1_alpaca_10k"]
+    n = c["n"]
+    # trace seeds from 1000 up whose prompts all fit econoserve's 3% reserve
+    # (engine.hpp:198-206); the same traces for every policy
+    rsv = round(c["opts"]["reserved_fraction"] * c["opts"]["kvc_capacity"])
+    traces, seed = [], 1000
+    while len(traces) < inst:
+        t = generate_trace(n, c["rate"], c["shape"]["prompt"], c["shape"]["rl"], seed)
+        seed += 1
+        if int(t["prompt_len"].max()) <= rsv:
+            traces.append(t)
+    out_seeds = seed - 1000
+    cores = os.cpu_count() or 1
+    out = {"instances": inst, "requests_per_instance": n, "host_cores": cores,
+           "trace_seeds": f"first {inst} feasible of 1000..{1000 + out_seeds - 1}"}
+    for pol in POLICIES:
+        o = abi.default_options(**dict(c["opts"], policy=pol, record_events=0, record_samples=0))
+        b = Batch(traces, o, device=0)
+        t0 = time.perf_counter()
+        while True:
+            b.launch(1 << 22)
+            b.sync()
+            sc = b.scalars()
+            if all(x.completed >= n or x.error for x in sc):
+                break
+        secs = time.perf_counter() - t0
+        b.close()
+        r = {"device_s": secs, "completed_per_s": inst * n / secs,
+             "errors": sum(1 for x in sc if x.error), "steps_per_instance": sum(x.steps for x in sc) / inst}
+        if not args.no_cpu_baseline:
+            try:
+                from oracle import ref
+                e = ref.RefEngine(traces[0], o)
+                t1 = time.perf_counter()
+                e.run()
+                one = time.perf_counter() - t1
+                r["reference_one_instance_s"] = one
+                r["reference_all_cores_completed_per_s"] = n * cores / one
+            except Exception as ex:  # noqa: BLE001
+                r["reference"] = f"unavailable: {ex}"
+        out[pol] = r
+        log(f"policy_sweep {pol}: {secs:.3f}s")
     return out
 
 
@@ -504,6 +565,8 @@ def main():
                     help="skip the configs[1] / configs[3] step measurements")
     ap.add_argument("--no-full-runs", action="store_true",
                     help="skip the whole-run completed-req/s measurements of configs[0] and configs[1]")
+    ap.add_argument("--no-policy-sweep", action="store_true",
+                    help="skip the all-policies configs[0] sweep (888 instances per policy)")
     ap.add_argument("--workload", default=WORKLOAD, choices=sorted(W.CONFIGS),
                     help="BASELINE.json config (default: configs[2], the 1M-queued case the metric is quoted on)")
     args = ap.parse_args()
