@@ -254,6 +254,11 @@ void econo_destroy(econo_engine* e);
 /* ---- multi-instance batch (one CTA per instance, on one device) --------- */
 typedef struct econo_batch econo_batch;
 
+/* Device bytes one instance of this trace + options occupies (its HBM arena,
+ * sized exactly as econo_batch_create would): capacity planning, e.g. how
+ * many instances fit on one GPU. Returns -code (2/3) on invalid input. */
+int64_t econo_instance_bytes(const EconoTraceRecord* trace, int64_t n, const EconoOptions* opt, char* err,
+                             size_t errlen);
 int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* n, int32_t n_inst,
                        const EconoOptions* opts /* n_inst entries */, int device,
                        econo_batch** out, char* err, size_t errlen);

@@ -374,7 +374,7 @@ EDEVNI void form_sarathi(Inst& I) {
 
 // commit_exact_epoch (engine.hpp:680-699)
 EDEVNI void commit_exact_epoch(Inst& I, int32_t id) {
-  const Tok pr = I.prompt[id], gen = I.generated[id], pad = I.padded[id];
+  const Tok pr = I.prompt[id], gen = I.generated[id], pad = padded_of(I, id);
   const Tok target = block_round(pr + gen + pad, I.block);
   const Tok held = I.held[id];
   bool ok = true;

@@ -188,11 +188,13 @@ struct Inst {
   GP<const double> arrival;
   GP<const int32_t> prompt;
   GP<const int32_t> true_rl;
-  GP<int32_t> predicted, padded, generated, occupied, allowance, gen_epoch, prefill_done;
+  GP<int32_t> predicted, generated, occupied, allowance, gen_epoch, prefill_done;
   GP<int32_t> preempt_count, reserve_draws, held, reg_head, reg_tail, reg_cnt, reserved, written;
-  GP<int32_t> slot_host, slot_off, slot_len, slot_abs, pt_next, gt_next, dem;
+  // pt_next and gt_next share storage: a request is never queued as a PT and
+  // a GT at once, and each link is written when the request joins its queue
+  GP<int32_t> slot_host, slot_off, slot_len, slot_abs, pt_next, gt_next;
   GP<uint8_t> state, flags;
-  GP<double> slo, waiting, preempt_t, exec_t, dispatch_t, first_tok, compl_clock, last_enq;
+  GP<double> waiting, preempt_t, exec_t, dispatch_t, first_tok, compl_clock, last_enq;
   GP<double> penalty, sched_share;
   // ---- KVC region pool (reg_cap) ----
   GP<int32_t> rg_start, rg_len, rg_owner, rg_next, reg_free, addr;
@@ -239,7 +241,7 @@ EDEV Tok udiv(Tok a, Tok b) {
   if (((uint64_t)a | (uint64_t)b) < (1ULL << 32)) return (Tok)((uint32_t)a / (uint32_t)b);
   return a / b;
 }
-EDEV Tok ceil_tokens(double v) { return (Tok)ceil(v - 1e-9); }
+EHD Tok ceil_tokens(double v) { return (Tok)ceil(v - 1e-9); }
 EDEV double dmax(double a, double b) { return (a < b) ? b : a; }
 EDEV double dmin(double a, double b) { return (b < a) ? b : a; }
 EDEV Tok tmax(Tok a, Tok b) { return (a < b) ? b : a; }
@@ -432,7 +434,15 @@ EDEV Tok predict_rl(const Inst& I, Tok true_rl, uint64_t* x, int32_t& idx) {
   }
   return quantize_up(tmax(1, v), I.pred_quantum);
 }
-EDEV Tok apply_padding(Tok p, double ratio) { return ceil_tokens((double)p * (1.0 + ratio)); }
+EHD Tok apply_padding(Tok p, double ratio) { return ceil_tokens((double)p * (1.0 + ratio)); }
+// padded_rl (engine.hpp:188, 921): always apply_padding(predicted_rl), so it
+// is recomputed instead of stored (4 bytes less per request).
+EHD int32_t padded_of(const Inst& I, int64_t id) { return (int32_t)apply_padding(I.predicted[id], I.pred_pad); }
+// slo_deadline (engine.hpp:190-191), recomputed with the same operations
+// from the trace (8 bytes less per request).
+EHD double slo_of(const Inst& I, int64_t id) {
+  return I.arrival[id] + I.slo_scale * (I.t_p + I.t_g * (double)I.true_rl[id]);
+}
 
 // ------------------------------------------------------------------------
 // ordering keys (queues.hpp:30-69)
@@ -914,7 +924,7 @@ EDEV void gq_remove_at(Inst& I, int32_t pos) {  // drops the group from the queu
   LANE0(I.G--; rl_set(I, I.gr_rl[g], -1); I.grp_free[I.grp_free_top++] = g);
 }
 EDEV Tok member_demand(const Inst& I, int32_t id) {  // gt_member_demand (engine.hpp:238-247)
-  const Tok target = block_round((Tok)I.prompt[id] + I.generated[id] + I.padded[id], I.block);
+  const Tok target = block_round((Tok)I.prompt[id] + I.generated[id] + padded_of(I, id), I.block);
   const Tok delta = target - I.held[id];
   return delta > 0 ? block_round(delta, I.block) : 0;
 }
@@ -923,7 +933,7 @@ EDEV Tok member_demand(const Inst& I, int32_t id) {  // gt_member_demand (engine
 // cached at join time and summed per group.
 EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline, int32_t occ, double now,
                             Tok d) {
-  LANE0(I.dem[id] = (int32_t)d; I.gt_next[id] = -1);
+  LANE0(I.gt_next[id] = -1);
   if (I.grouping) {
     const int32_t g = rl_find(I, padded);
     if (g >= 0) {
@@ -981,7 +991,7 @@ EDEV void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline, 
 // memory round trip per field.
 EDEV void begin_gt_run(Inst& I, int32_t id, bool hosted) {
   const uint8_t f = I.flags[id];
-  const int32_t gen = I.generated[id], pad = I.padded[id];
+  const int32_t gen = I.generated[id], pad = padded_of(I, id);
   const double le = I.last_enq[id], wt = I.waiting[id], pt = I.preempt_t[id];
   const double wait = dmax(0.0, I.clock - le);
   uint8_t nf = hosted ? (uint8_t)(f | F_HOSTED) : (uint8_t)(f & ~F_HOSTED);
@@ -1032,7 +1042,7 @@ EDEVNI void ingest(Inst& I) {
   if (B && I.policy == ECONO_POLICY_SYNC_COUPLED) {
     // sync-coupled: arrivals join the waiting groups (engine.hpp:226-228)
     for (int64_t id = first; id < last; ++id)
-      group_insert_gt(I, (int32_t)id, I.padded[id], I.slo[id], 0, I.clock);
+      group_insert_gt(I, (int32_t)id, padded_of(I, id), slo_of(I, id), 0, I.clock);
     LANE0(I.arrival_cursor = last; I.ev_total += k; if (I.record_events) I.ev_n += k);
     return;
   }
@@ -1051,7 +1061,7 @@ EDEVNI void ingest(Inst& I) {
       int cls = -1 - LANE;
       int b = 0, p = 0;
       if (ok) {
-        b = bucket_d(I, dmax(0.0, I.slo[id] - I.clock));
+        b = bucket_d(I, dmax(0.0, slo_of(I, id) - I.clock));
         p = I.prompt[id];
         cls = cls_of(I, b, p);
       }
@@ -1169,7 +1179,7 @@ EDEVNI void dispatch_pts(Inst& I, int32_t npt) {
 // reserve release (kvc.hpp:152-159), written/occupied accounting and
 // begin_gt_run in one lane-0 block whose loads all precede its stores.
 EDEVNI void schedule_gt_member(Inst& I, int32_t id) {
-  const Tok prompt = I.prompt[id], gen = I.generated[id], pad = I.padded[id];
+  const Tok prompt = I.prompt[id], gen = I.generated[id], pad = padded_of(I, id);
   const Tok target = block_round(prompt + gen + pad, I.block);
   const Tok held = I.held[id];
   const Tok resident = prompt + gen;
@@ -1317,7 +1327,7 @@ EDEVNI int32_t plan_host_group(Inst& I, int32_t l, int32_t hs, int32_t he, int32
           I.os_len[nout + i] = I.cd_len[ci];
           I.os_abs[nout + i] = I.cd_abs[ci];
           I.assigned[ri] = m;
-          dsum += I.dem[m];
+          dsum += member_demand(I, m);
           m = I.gt_next[m];
         }
         I.gr_head[best] = m;
@@ -1417,7 +1427,7 @@ EDEVNI int32_t select_gt(Inst& I, int32_t* nsel_out) {
       Tok pd = 0;
       if (LANE == 0) {
         while (m >= 0) {
-          const Tok d = I.dem[m];
+          const Tok d = member_demand(I, m);
           const int32_t nx = I.gt_next[m];
           I.exam_count++;
           if (pd + d > remaining) break;
@@ -1595,7 +1605,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
 #include "baselines.cuh"
 
 EDEVNI void vacate_slot(Inst& I, int32_t id, bool* rehomed) {  // engine.hpp:888-902
-  const Tok in_slot = tmin((Tok)I.generated[id] - I.gen_epoch[id], (Tok)I.padded[id]);
+  const Tok in_slot = tmin((Tok)I.generated[id] - I.gen_epoch[id], (Tok)padded_of(I, id));
   bool rh = false;
   if (in_slot > 0 && kvc_draw_reserved(I, id, in_slot)) {
     rh = true;
@@ -1616,18 +1626,17 @@ EDEVNI void preempt_and_regroup(Inst& I, int32_t id, int why) {  // engine.hpp:9
     I.state[id] = ST_PREEMPTED;
     const Tok remaining = (Tok)I.true_rl[id] - I.generated[id];
     I.predicted[id] = (int32_t)predict_rl(I, remaining, I.pmt, I.pmt_i);
-    I.padded[id] = (int32_t)apply_padding(I.predicted[id], I.pred_pad);
     I.flags[id] |= F_WAS_PREEMPTED;
     I.last_enq[id] = I.clock;
   }
   WSYNC();
-  logev(I, ECONO_EV_PREEMPT, id, why, I.padded[id]);
+  logev(I, ECONO_EV_PREEMPT, id, why, padded_of(I, id));
   LANE0(I.state[id] = ST_WAITING_GT);
   if (B && I.policy != ECONO_POLICY_SYNC_COUPLED) {
     wait_insert(I, id);
     return;
   }
-  group_insert_gt(I, id, I.padded[id], I.slo[id], I.occupied[id], I.clock);
+  group_insert_gt(I, id, padded_of(I, id), slo_of(I, id), I.occupied[id], I.clock);
 }
 
 template <bool B>
@@ -1777,9 +1786,9 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     const int32_t id = I.ptiter_id[i];
     const uint8_t f = I.flags[id];
     const uint8_t st = I.state[id];
-    const int32_t pad = I.padded[id], oc = I.occupied[id], pr = I.prompt[id], gen = I.generated[id];
+    const int32_t pad = padded_of(I, id), oc = I.occupied[id], pr = I.prompt[id], gen = I.generated[id];
     const int32_t hd = I.held[id];
-    const double slo = I.slo[id];
+    const double slo = slo_of(I, id);
     if (!(f & F_PREFILL_FIN)) continue;
     WSYNC();
     LANE0(I.flags[id] = (uint8_t)(f & ~F_PREFILL_FIN));
@@ -1958,7 +1967,7 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
   }
   if (has_arr && ta <= I.clock + 1e-12) return 0;
   if (gt_check) {  // queues.hpp:220-263 would take >= 1 member
-    if (gd <= free_tok || I.dem[gh] <= free_tok) return 0;
+    if (gd <= free_tok || member_demand(I, gh) <= free_tok) return 0;
   }
   const Tok C0 = tmin(I.tfs - (Tok)R, I.reserve_cap - I.reserved_used);
   if (C0 >= 1 && I.pt_count > 0 && C0 >= I.pt_min_lb) {  // queues.hpp:279-299 would take a PT

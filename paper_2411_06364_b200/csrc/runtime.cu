@@ -72,22 +72,19 @@ EDEVNI void init_predict_sequential(Inst& I) {
 // maximum output length, every other policy the larger of the true and
 // padded lengths.
 EDEV Tok worst_demand(const Inst& I, int64_t i) {
-  const Tok out = I.policy == ECONO_POLICY_ORCA ? I.max_out : tmax(I.true_rl[i], I.padded[i]);
+  const Tok out = I.policy == ECONO_POLICY_ORCA ? I.max_out : tmax(I.true_rl[i], padded_of(I, i));
   return block_round((Tok)I.prompt[i] + out, I.block);
 }
 // Phase 3: per-request fields + feasibility (engine.hpp:186-206).
 EDEV bool init_req_one(Inst& I, int64_t i) {
   if (I.pred_model == ECONO_PRED_ORACLE) I.predicted[i] = (int32_t)quantize_up(I.true_rl[i], I.pred_quantum);
-  I.padded[i] = (int32_t)apply_padding(I.predicted[i], I.pred_pad);
-  I.slo[i] = I.arrival[i] + I.slo_scale * (I.t_p + I.t_g * (double)I.true_rl[i]);
   I.state[i] = ST_WAITING_PT;
   I.dispatch_t[i] = -1.0;
   I.first_tok[i] = -1.0;
   I.compl_clock[i] = -1.0;
   I.reg_head[i] = -1;
   I.reg_tail[i] = -1;
-  I.pt_next[i] = -1;
-  I.gt_next[i] = -1;
+  I.pt_next[i] = -1;  // also gt_next (shared storage)
   if (I.base) I.ptarget[i] = I.prompt[i];  // prefill_target = prompt_len (engine.hpp:189)
   return worst_demand(I, i) > I.general_cap || (!I.base && (Tok)I.prompt[i] > I.reserve_cap);
 }
@@ -177,10 +174,10 @@ EDEV void engine_record(const Inst& I, int32_t i, EconoRecord& rc) {
   rc.preemption_time = I.preempt_t[i] + I.penalty[i];
   rc.scheduling_time_share = I.sched_share[i];
   rc.reserve_draws = I.reserve_draws[i];
-  rc.met_slo = rc.completion_time <= I.slo[i];
+  rc.met_slo = rc.completion_time <= slo_of(I, i);
   rc.prompt_len = I.prompt[i];
   rc.true_rl = I.true_rl[i];
-  rc.slo_deadline = I.slo[i];
+  rc.slo_deadline = slo_of(I, i);
   rc.alloc_failure = (I.flags[i] & F_ALLOC_FAIL) ? 1 : 0;
   rc._pad = 0;
 }
@@ -401,10 +398,10 @@ __global__ void k_engine_records(const Inst* inst, EconoRecord* out) {
     rc.preemption_time = I.preempt_t[i] + I.penalty[i];
     rc.scheduling_time_share = I.sched_share[i];
     rc.reserve_draws = I.reserve_draws[i];
-    rc.met_slo = rc.completion_time <= I.slo[i];
+    rc.met_slo = rc.completion_time <= slo_of(I, i);
     rc.prompt_len = I.prompt[i];
     rc.true_rl = I.true_rl[i];
-    rc.slo_deadline = I.slo[i];
+    rc.slo_deadline = slo_of(I, i);
     rc.alloc_failure = (I.flags[i] & F_ALLOC_FAIL) ? 1 : 0;
     rc._pad = 0;
     out[i] = rc;
@@ -447,7 +444,7 @@ __global__ void __launch_bounds__(256) k_bulk_keys(const Inst* insts, BulkJob* j
     const int64_t i = t0 + e;
     if (i >= J.k) break;
     const int64_t id = J.first + i;
-    const int b = bucket_d(I, dmax(0.0, I.slo[id] - now));
+    const int b = bucket_d(I, dmax(0.0, slo_of(I, id) - now));
     const int32_t p = I.prompt[id];
     key[J.off + i] = (uint32_t)(b * pm1 + p);
     val[J.off + i] = (uint32_t)id;
@@ -837,14 +834,15 @@ void layout(Inst& I, char* base, size_t* bytes) {
   I.arrival = a.take<double>(n);
   I.prompt = a.take<int32_t>(n);
   I.true_rl = a.take<int32_t>(n);
-  GP<int32_t>* i32s[] = {&I.predicted, &I.padded, &I.generated, &I.occupied, &I.allowance, &I.gen_epoch,
+  GP<int32_t>* i32s[] = {&I.predicted, &I.generated, &I.occupied, &I.allowance, &I.gen_epoch,
                       &I.prefill_done, &I.preempt_count, &I.reserve_draws, &I.held, &I.reg_head,
                       &I.reg_tail, &I.reg_cnt, &I.reserved, &I.written, &I.slot_host, &I.slot_off,
-                      &I.slot_len, &I.slot_abs, &I.pt_next, &I.gt_next, &I.dem};
+                      &I.slot_len, &I.slot_abs, &I.pt_next};
   for (auto p : i32s) *p = a.take<int32_t>(n);
+  I.gt_next = I.pt_next.p;
   I.state = a.take<uint8_t>(n);
   I.flags = a.take<uint8_t>(n);
-  GP<double>* f64s[] = {&I.slo, &I.waiting, &I.preempt_t, &I.exec_t, &I.dispatch_t, &I.first_tok,
+  GP<double>* f64s[] = {&I.waiting, &I.preempt_t, &I.exec_t, &I.dispatch_t, &I.first_tok,
                      &I.compl_clock, &I.last_enq, &I.penalty, &I.sched_share};
   for (auto p : f64s) *p = a.take<double>(n);
   const int64_t rc = I.reg_cap;
@@ -1491,6 +1489,18 @@ void econo_batch_destroy(econo_batch* b) {
   if (b->stream) cudaStreamDestroy(b->stream);
 #endif
   delete b;
+}
+
+int64_t econo_instance_bytes(const EconoTraceRecord* trace, int64_t n, const EconoOptions* opt, char* err,
+                             size_t errlen) {
+  int rc = validate(opt, n, err, errlen);
+  if (rc) return -rc;
+  Inst I;
+  rc = configure(I, opt, trace, n, err, errlen);
+  if (rc) return -rc;
+  size_t bytes = 0;
+  layout(I, nullptr, &bytes);
+  return (int64_t)((bytes + 4095) & ~size_t(4095));
 }
 
 int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns, int32_t n_inst,
@@ -2384,7 +2394,7 @@ int64_t econo_snapshot(econo_engine* e, int64_t* out, int64_t cap) {
     w.push_back(I.state[i]);
     w.push_back(I.generated[i]);
     w.push_back(I.predicted[i]);
-    w.push_back(I.padded[i]);
+    w.push_back(padded_of(I, i));
     w.push_back(I.allowance[i]);
     w.push_back(I.gen_epoch[i]);
     w.push_back(I.occupied[i]);
@@ -2403,7 +2413,7 @@ int64_t econo_snapshot(econo_engine* e, int64_t* out, int64_t cap) {
     w.push_back(bits(I.last_enq[i]));
     w.push_back(bits(I.sched_share[i]));
     w.push_back(bits(I.penalty[i]));
-    w.push_back(bits(I.slo[i]));
+    w.push_back(bits(slo_of(I, i)));
   }
   if (I.base) {  // baseline-policy tail
     w.push_back(0x42415345);

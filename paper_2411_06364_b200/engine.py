@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(HERE, "_lib", "libeconoserve_b200.so")
 SYMBOLS = [
     "econo_default_options", "econo_create", "econo_step", "econo_run", "econo_records",
     "econo_report", "econo_events", "econo_samples", "econo_scalars", "econo_snapshot",
-    "econo_destroy", "econo_batch_create", "econo_batch_launch", "econo_batch_sync",
+    "econo_destroy", "econo_instance_bytes", "econo_batch_create", "econo_batch_launch", "econo_batch_sync",
     "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
     "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore", "econo_batch_debug",
     "econo_batch_reports", "econo_batch_jct_prepare", "econo_batch_jct_hist", "econo_batch_jct_percentiles",
@@ -77,6 +77,8 @@ def load(path=None):
     L.econo_snapshot.argtypes = [vp, vp, i64]
     L.econo_snapshot.restype = i64
     L.econo_destroy.argtypes = [vp]
+    L.econo_instance_bytes.argtypes = [vp, i64, C.POINTER(abi.Options), C.c_char_p, C.c_size_t]
+    L.econo_instance_bytes.restype = i64
     L.econo_batch_create.argtypes = [C.POINTER(vp), C.POINTER(i64), i32, C.POINTER(abi.Options),
                                      C.c_int, C.POINTER(vp), cp, sz]
     L.econo_batch_launch.argtypes = [vp, i64, vp]
@@ -99,6 +101,18 @@ def load(path=None):
                                        C.POINTER(abi.LengthDist), C.c_uint64, vp, cp, sz]
     _libs[path] = L
     return L
+
+
+def instance_bytes(trace, options, lib=None):
+    """HBM bytes one instance of `trace` occupies (econo_instance_bytes)."""
+    L = load(lib)
+    t = abi.trace_array(trace)
+    err = C.create_string_buffer(1024)
+    o = options
+    r = L.econo_instance_bytes(t.ctypes.data, len(t), C.byref(o), err, 1024)
+    if r < 0:
+        _raise(int(-r), err)
+    return int(r)
 
 
 def generate_trace(n, rate, prompt, rl, seed, lib=None, out=None):
