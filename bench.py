@@ -224,6 +224,27 @@ def algorithmic_bytes(sc_before, sc_after, iters, n_inst):
     return n_inst * iters * (48.0 * run + 64.0) + 40.0 * pt + 96.0 * gt
 
 
+def auto_instances(n, device, sms=148):
+    """As many instances per SM as the GPU's free HBM holds: each needs its
+    arena (econo_instance_bytes) plus, at the end of the run, 8 B of JCT key
+    per request; the burst-ingest scratch (<= 4.3 GB) is freed before the
+    keys are allocated. Sized on one configs[2] trace (the others differ by
+    kilobytes)."""
+    import torch
+
+    from paper_2411_06364_b200.engine import generate_trace, instance_bytes
+    c = W.CONFIGS[WORKLOAD]
+    t = generate_trace(n, c["rate"], c["shape"]["prompt"], c["shape"]["rl"], 1000)
+    per = instance_bytes(t, options())
+    free, _ = torch.cuda.mem_get_info(device)
+    slack = 2 << 30  # staging buffers, event logs, the CUDA context's growth
+    for k in range(16, 0, -1):
+        inst = k * sms
+        if inst * per + max(4.4e9, 8.0 * inst * n) + slack <= free:
+            return inst
+    return sms
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -237,7 +258,7 @@ def run_ours(args):
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    I = args.instances
+    I = args.instances or auto_instances(args.n, local)
     seeds = [1000 + rank * I + i for i in range(I)]
     t0 = time.time()
     # host trace generation shares the box's cores between the ranks
@@ -552,8 +573,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--instances", type=int, default=888,
-                    help="serving instances per GPU (6 per SM; ~184 MB of HBM each at 1M requests: 163 GB of the 180 GB)")
+    ap.add_argument("--instances", type=int, default=0,
+                    help="serving instances per GPU (default: as many per SM as fit in HBM; ~172 MB each at 1M "
+                         "requests, so 7 per SM = 1036 on a B200)")
     ap.add_argument("--iters", type=int, default=1000,
                     help="scheduler iterations per instance per step (one k_engine_steps launch)")
     ap.add_argument("--ref-iters", type=int, default=100,

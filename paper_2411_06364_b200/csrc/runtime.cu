@@ -1264,6 +1264,11 @@ int jct_prepare(econo_batch* b, char* err, size_t errlen) {
       b->h_keys[(size_t)(off[(size_t)i] + k)] = jct_key(b->inst[(size_t)i].desc, k);
 #else
   if (total != b->keys_total) {
+    // the burst-ingest scratch is not needed once the run reports: give its
+    // HBM to the keys (a later ingest re-allocates it)
+    dev_free(b->bulk_buf);
+    b->bulk_buf = nullptr;
+    b->bulk_bytes = 0;
     dev_free(b->d_keys);
     dev_free(b->d_koff);
     b->d_keys = nullptr;
