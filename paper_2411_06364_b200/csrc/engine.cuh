@@ -204,7 +204,9 @@ struct Inst {
   GP<int32_t> tree;
   // ---- GT groups (grp_cap) ----
   GP<uint64_t> gr_id, gr_seq;
-  GP<int32_t> gr_rl, gr_head, gr_tail, gr_cnt, gr_db, gr_kb, gr_maxocc, grp_free, gq, rl_map;
+  // gr_hd: the head member's demand, so the quiet-span test needs no
+  // dependent load through the head id
+  GP<int32_t> gr_rl, gr_head, gr_tail, gr_cnt, gr_db, gr_kb, gr_maxocc, grp_free, gq, rl_map, gr_hd;
   GP<double> gr_formed, gr_mindl;
   GP<int64_t> gr_dem;
   // ---- ordered lists ----
@@ -944,7 +946,7 @@ EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline
         const int64_t gd = I.gr_dem[g];
         const double md = I.gr_mindl[g];
         I.G--;
-        if (cnt == 0) I.gr_head[g] = id; else I.gt_next[tail] = id;
+        if (cnt == 0) { I.gr_head[g] = id; I.gr_hd[g] = (int32_t)d; } else { I.gt_next[tail] = id; }
         I.gr_tail[g] = id;
         I.gr_cnt[g] = cnt + 1;
         I.gr_dem[g] = gd + d;
@@ -969,6 +971,7 @@ EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline
   WSYNC();
   LANE0(I.grp_free_top--;
         I.gr_id[g] = I.next_group_id++; I.gr_rl[g] = padded; I.gr_head[g] = id; I.gr_tail[g] = id;
+        I.gr_hd[g] = (int32_t)d;
         I.gr_cnt[g] = 1; I.gr_dem[g] = d; I.gr_formed[g] = now; I.gr_mindl[g] = deadline;
         I.gr_maxocc[g] = occ; I.gr_seq[g] = I.gt_next_seq++;
         I.gr_db[g] = I.ordered ? bucket_d(I, dmax(0.0, deadline - now)) : 0;
@@ -1331,6 +1334,7 @@ EDEVNI int32_t plan_host_group(Inst& I, int32_t l, int32_t hs, int32_t he, int32
           m = I.gt_next[m];
         }
         I.gr_head[best] = m;
+        if (m >= 0) I.gr_hd[best] = (int32_t)member_demand(I, m);
         I.gr_cnt[best] -= take;
         I.gr_dem[best] -= dsum;
         if (I.gr_cnt[best] == 0) I.gr_tail[best] = -1;
@@ -1424,25 +1428,27 @@ EDEVNI int32_t select_gt(Inst& I, int32_t* nsel_out) {
         continue;
       }
       int32_t taken = 0, m = head;
-      Tok pd = 0;
+      Tok pd = 0, dm = 0;
       if (LANE == 0) {
+        Tok d = I.gr_hd[g];
         while (m >= 0) {
-          const Tok d = member_demand(I, m);
           const int32_t nx = I.gt_next[m];
           I.exam_count++;
-          if (pd + d > remaining) break;
+          if (pd + d > remaining) { dm = d; break; }
           pd += d;
           I.sel_ids[nsel + taken] = m;
           taken++;
           m = nx;
+          if (m >= 0) d = member_demand(I, m);
         }
       }
+      dm = shfl(dm, 0);
       taken = shfl(taken, 0);
       m = shfl(m, 0);
       pd = shfl(pd, 0);
       if (taken > 0) {
         LANE0(I.selg_start[nselg] = nsel; I.selg_rl[nselg] = I.gr_rl[g];
-              I.gr_head[g] = m; I.gr_cnt[g] -= taken; I.gr_dem[g] -= pd);
+              I.gr_head[g] = m; I.gr_hd[g] = (int32_t)dm; I.gr_cnt[g] -= taken; I.gr_dem[g] -= pd);
         nsel += taken;
         nselg++;
         remaining -= pd;
@@ -1955,10 +1961,10 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
   const int32_t g = gt_check ? I.gq[0] : 0;
   const int32_t id0 = LANE < R ? I.run[LANE] : -1;
   int64_t gd = 0;
-  int32_t gh = 0;
+  int32_t hd = 0;
   if (gt_check) {
     gd = I.gr_dem[g];
-    gh = I.gr_head[g];
+    hd = I.gr_hd[g];
   }
   int64_t kev = INT64_MAX;
   if (id0 >= 0) {
@@ -1967,7 +1973,7 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
   }
   if (has_arr && ta <= I.clock + 1e-12) return 0;
   if (gt_check) {  // queues.hpp:220-263 would take >= 1 member
-    if (gd <= free_tok || member_demand(I, gh) <= free_tok) return 0;
+    if (gd <= free_tok || hd <= free_tok) return 0;
   }
   const Tok C0 = tmin(I.tfs - (Tok)R, I.reserve_cap - I.reserved_used);
   if (C0 >= 1 && I.pt_count > 0 && C0 >= I.pt_min_lb) {  // queues.hpp:279-299 would take a PT

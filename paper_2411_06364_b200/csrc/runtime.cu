@@ -865,7 +865,8 @@ void layout(Inst& I, char* base, size_t* bytes) {
   const int64_t gc = I.grp_cap;
   I.gr_id = a.take<uint64_t>(gc);
   I.gr_seq = a.take<uint64_t>(gc);
-  GP<int32_t>* g32[] = {&I.gr_rl, &I.gr_head, &I.gr_tail, &I.gr_cnt, &I.gr_db, &I.gr_kb, &I.gr_maxocc, &I.grp_free};
+  GP<int32_t>* g32[] = {&I.gr_rl, &I.gr_head, &I.gr_tail, &I.gr_cnt, &I.gr_db, &I.gr_kb, &I.gr_maxocc, &I.grp_free,
+                        &I.gr_hd};
   for (auto p : g32) *p = a.take<int32_t>(gc);
   I.gq = a.take<int32_t>(gc + W);
   I.rl_map = a.take<int32_t>(I.rl_cap);
