@@ -226,10 +226,10 @@ def algorithmic_bytes(sc_before, sc_after, iters, n_inst):
 
 def auto_instances(n, device, sms=148):
     """As many instances per SM as the GPU's free HBM holds: each needs its
-    arena (econo_instance_bytes) plus, at the end of the run, 8 B of JCT key
-    per request; the burst-ingest scratch (<= 4.3 GB) is freed before the
-    keys are allocated. Sized on one configs[2] trace (the others differ by
-    kilobytes)."""
+    arena (econo_instance_bytes), plus the burst-ingest scratch (<= 2.2 GB).
+    The end-of-run JCT keys (8 B per request) get a buffer only if HBM is
+    left, else each histogram pass derives them from the request fields.
+    Sized on one configs[2] trace (the others differ by kilobytes)."""
     import torch
 
     from paper_2411_06364_b200.engine import generate_trace, instance_bytes
@@ -237,10 +237,10 @@ def auto_instances(n, device, sms=148):
     t = generate_trace(n, c["rate"], c["shape"]["prompt"], c["shape"]["rl"], 1000)
     per = instance_bytes(t, options())
     free, _ = torch.cuda.mem_get_info(device)
-    slack = 2 << 30  # staging buffers, event logs, the CUDA context's growth
+    slack = 1 << 30  # staging buffers, partial-sum scratch, the CUDA context's growth
     for k in range(16, 0, -1):
         inst = k * sms
-        if inst * per + max(4.4e9, 8.0 * inst * n) + slack <= free:
+        if inst * per + 2.2e9 + slack <= free:  # + the ingest scratch (128M keys x 16 B)
             return inst
     return sms
 
@@ -574,8 +574,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--instances", type=int, default=0,
-                    help="serving instances per GPU (default: as many per SM as fit in HBM; ~172 MB each at 1M "
-                         "requests, so 7 per SM = 1036 on a B200)")
+                    help="serving instances per GPU (default: as many per SM as fit in HBM; ~157 MB each at 1M "
+                         "requests, so 8 per SM = 1184 on a B200)")
     ap.add_argument("--iters", type=int, default=1000,
                     help="scheduler iterations per instance per step (one k_engine_steps launch)")
     ap.add_argument("--ref-iters", type=int, default=100,

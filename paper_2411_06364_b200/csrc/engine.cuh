@@ -164,7 +164,7 @@ struct Inst {
   int64_t hosted_total, hosted_overruns, alloc_failures, steps, executed, pt_dispatched, gt_scheduled;
   uint64_t next_group_id, gt_next_seq;
   int32_t pt_count, G, R, n_slots, n_regions, n_ptiter, n_adm, pts_admitted_iter, pt_admittable;
-  int32_t reg_free_top, grp_free_top, n_sel, n_selg, n_hosts_members;
+  int32_t reg_free_top, grp_free_top, n_sel, n_selg, n_hosts_members, sl_free_top, _pad4;
   int32_t error, err_id, status, mt_i, pmt_i, _pad0;
   int64_t err_val, ev_n, ev_cap, sm_n, sm_cap, ev_total;
   double wbuf[W];      // quiet-span replay: one chunk of per-step written fractions
@@ -189,10 +189,10 @@ struct Inst {
   GP<const int32_t> prompt;
   GP<const int32_t> true_rl;
   GP<int32_t> predicted, generated, occupied, allowance, gen_epoch, prefill_done;
-  GP<int32_t> preempt_count, reserve_draws, held, reg_head, reg_tail, reg_cnt, reserved, written;
+  GP<int32_t> preempt_count, reserve_draws, held, reg_head, reg_tail, reserved, written;
   // pt_next and gt_next share storage: a request is never queued as a PT and
   // a GT at once, and each link is written when the request joins its queue
-  GP<int32_t> slot_host, slot_off, slot_len, slot_abs, pt_next, gt_next;
+  GP<int32_t> sidx, pt_next, gt_next;  // sidx: a hosted request's slot-pool entry
   GP<uint8_t> state, flags;
   GP<double> waiting, preempt_t, exec_t, dispatch_t, first_tok, compl_clock, last_enq;
   GP<double> penalty, sched_share;
@@ -211,6 +211,10 @@ struct Inst {
   GP<int64_t> gr_dem;
   // ---- ordered lists ----
   GP<int32_t> run, slots, ptiter_id, ptiter_tok, adm;
+  // ---- hosting-slot pool (slot_cap entries; I.slots lists entries in
+  // insertion order): host, start offset (== deadline usage), length,
+  // absolute start, hosted id; free entries on a stack ----
+  GP<int32_t> sl_host, sl_off, sl_len, sl_abs, sl_hosted, sl_free;
   // ---- scratch ----
   GP<int32_t> sel_ids, selg_start, selg_rl;            // GT selection output
   GP<int32_t> wa_w, wa_b, wa_l, wa_u, wb_w, wb_b, wb_l, wb_u;  // planner regions
@@ -650,28 +654,27 @@ EDEV int32_t region_new(Inst& I, int32_t owner, Tok start, Tok len) {  // all la
   const int32_t r = I.reg_free[I.reg_free_top - 1];
   WSYNC();
   if (LANE == 0) {  // the owner's list fields are loaded before any store
-    const int32_t cnt = I.reg_cnt[owner], tail = I.reg_tail[owner], hd = I.held[owner];
+    const int32_t tail = I.reg_tail[owner], hd = I.held[owner];
     I.reg_free_top--;
     I.rg_start[r] = (int32_t)start;
     I.rg_len[r] = (int32_t)len;
     I.rg_owner[r] = owner;
     I.rg_next[r] = -1;
-    if (cnt == 0) I.reg_head[owner] = r; else I.rg_next[tail] = r;
+    if (tail < 0) I.reg_head[owner] = r; else I.rg_next[tail] = r;
     I.reg_tail[owner] = r;
-    I.reg_cnt[owner] = cnt + 1;
     I.held[owner] = hd + (int32_t)len;
   }
   WSYNC();
   return r;
 }
 
-// owner_or_slot_host (kvc.hpp:405-410), slots identified by hosted id.
-EDEV bool owner_or_slot_host(const Inst& I, int32_t hosted, int32_t owner) {
-  int32_t h = I.slot_host[hosted];
+// owner_or_slot_host (kvc.hpp:405-410) for a slot whose host is h: walks up
+// the chain of slots the hosts themselves occupy.
+EDEV bool owner_or_slot_host(const Inst& I, int32_t h, int32_t owner) {
   for (int guard = 0; guard < 64; ++guard) {
     if (h == owner) return true;
     if (!(I.flags[h] & F_HAS_SLOT)) return false;
-    h = I.slot_host[h];
+    h = I.sl_host[I.sidx[h]];
   }
   return false;
 }
@@ -697,8 +700,8 @@ EDEVNI void kvc_compact(Inst& I) {
   for (int32_t base = 0; base < I.n_slots; base += W) {
     const int32_t si = base + LANE;
     if (si < I.n_slots) {
-      const int32_t h = I.slots[si];
-      const int32_t abs = I.slot_abs[h];
+      const int32_t sp = I.slots[si];
+      const int32_t abs = I.sl_abs[sp], sh = I.sl_host[sp];
       int32_t lo = 0, hi = L;  // last position with start <= abs
       while (lo < hi) {
         const int32_t mid = (lo + hi) >> 1;
@@ -708,7 +711,7 @@ EDEVNI void kvc_compact(Inst& I) {
       if (pos >= 0) {
         const int32_t r = I.addr[pos];
         const int32_t os = I.rg_start[r];
-        if (abs < os + I.rg_len[r] && ns[pos] != os && owner_or_slot_host(I, h, I.rg_owner[r]))
+        if (abs < os + I.rg_len[r] && ns[pos] != os && owner_or_slot_host(I, sh, I.rg_owner[r]))
           I.tmp_b[si] = abs + (ns[pos] - os);
         else
           I.tmp_b[si] = abs;
@@ -718,7 +721,7 @@ EDEVNI void kvc_compact(Inst& I) {
     }
   }
   WSYNC();
-  for (int32_t si = LANE; si < I.n_slots; si += W) I.slot_abs[I.slots[si]] = I.tmp_b[si];
+  for (int32_t si = LANE; si < I.n_slots; si += W) I.sl_abs[I.slots[si]] = I.tmp_b[si];
   for (int32_t j = LANE; j < L; j += W) I.rg_start[I.addr[j]] = ns[j];
   WSYNC();
 }
@@ -782,20 +785,21 @@ EDEV void kvc_add_written(Inst& I, int32_t id, Tok d) {  // kvc.hpp:87-90 (lane 
 // remove_slot (kvc.hpp:229-243)
 EDEVNI void kvc_remove_slot(Inst& I, int32_t hosted) {
   if (!(I.flags[hosted] & F_HAS_SLOT)) return;
-  const int32_t oh = I.slot_host[hosted], oo = I.slot_off[hosted];
-  const int32_t oa = I.slot_abs[hosted], ol = I.slot_len[hosted];
+  const int32_t op = I.sidx[hosted];
+  const int32_t oh = I.sl_host[op], oo = I.sl_off[op];
+  const int32_t oa = I.sl_abs[op], ol = I.sl_len[op];
   int32_t mypos = -1;
   for (int32_t base = 0; base < I.n_slots; base += W) {
     const int32_t si = base + LANE;
-    const int32_t h = si < I.n_slots ? I.slots[si] : -1;
-    if (h >= 0 && h != hosted && I.slot_host[h] == hosted) {
-      const int32_t a = I.slot_abs[h];
-      if (a >= oa && a + I.slot_len[h] <= oa + ol) {
-        I.slot_host[h] = oh;
-        I.slot_off[h] += oo;
+    const int32_t sp = si < I.n_slots ? I.slots[si] : -1;
+    if (sp >= 0 && sp != op && I.sl_host[sp] == hosted) {
+      const int32_t a = I.sl_abs[sp];
+      if (a >= oa && a + I.sl_len[sp] <= oa + ol) {
+        I.sl_host[sp] = oh;
+        I.sl_off[sp] += oo;
       }
     }
-    const unsigned m = BALLOT(h == hosted);
+    const unsigned m = BALLOT(sp == op);
     if (m && mypos < 0) mypos = base + FFS(m);
   }
   WSYNC();
@@ -803,16 +807,16 @@ EDEVNI void kvc_remove_slot(Inst& I, int32_t hosted) {
     arr_erase(I.slots, I.n_slots, mypos, 1);
     LANE0(I.n_slots--);
   }
-  LANE0(I.flags[hosted] &= ~F_HAS_SLOT);
+  LANE0(I.flags[hosted] &= ~F_HAS_SLOT; I.sl_free[I.sl_free_top++] = op);
 }
 
 // release (kvc.hpp:165-217)
 // release (kvc.hpp:165-217). The request's own fields are loaded once up
 // front; nothing below changes them except this function's final stores.
 EDEVNI void kvc_release(Inst& I, int32_t id) {
-  const int32_t cnt = I.reg_cnt[id], head = I.reg_head[id], rsv = I.reserved[id], wr = I.written[id];
+  const int32_t head = I.reg_head[id], rsv = I.reserved[id], wr = I.written[id];
   const uint8_t f0 = I.flags[id];
-  const bool had = cnt > 0;
+  const bool had = head >= 0;
   if (!had && !(f0 & F_HAS_RESERVED) && !(f0 & F_HAS_SLOT)) {
     set_error(I, ERR_RELEASE_UNKNOWN, id, 0);
     return;
@@ -823,7 +827,7 @@ EDEVNI void kvc_release(Inst& I, int32_t id) {
     int32_t np = 0;
     for (int32_t base = 0; base < I.n_slots; base += W) {
       const int32_t si = base + LANE;
-      const bool hit = si < I.n_slots && I.slot_host[I.slots[si]] == id;
+      const bool hit = si < I.n_slots && I.sl_host[I.slots[si]] == id;
       const unsigned m = BALLOT(hit);
       if (hit) I.tmp_c[np + POPC(m & LANEMASK_LT)] = I.slots[si];
       np += POPC(m);
@@ -839,26 +843,32 @@ EDEVNI void kvc_release(Inst& I, int32_t id) {
       freed += ln;
       r = nx;
     }
-    LANE0(I.reg_cnt[id] = 0; I.reg_head[id] = -1; I.reg_tail[id] = -1; I.held[id] = 0);
+    LANE0(I.reg_head[id] = -1; I.reg_tail[id] = -1; I.held[id] = 0);
     for (int32_t k = 0; k < np; ++k) {
-      const int32_t h = I.tmp_c[k];
-      const int32_t r = region_new(I, h, I.slot_abs[h], I.slot_len[h]);
+      const int32_t sp = I.tmp_c[k];
+      const int32_t h = I.sl_hosted[sp], sl = I.sl_len[sp];
+      const int32_t r = region_new(I, h, I.sl_abs[sp], sl);
       if (r < 0) return;
       addr_insert_region(I, r);
-      freed -= I.slot_len[h];
+      freed -= sl;
     }
     if (np > 0) {  // erase promoted slots (stable)
       int32_t w = 0;
       for (int32_t base = 0; base < I.n_slots; base += W) {
         const int32_t si = base + LANE;
-        const int32_t h = si < I.n_slots ? I.slots[si] : -1;
-        const bool keep = h >= 0 && I.slot_host[h] != id;
-        const unsigned m = BALLOT(keep);
+        const int32_t sp = si < I.n_slots ? I.slots[si] : -1;
+        const bool keep = sp >= 0 && I.sl_host[sp] != id;
+        const bool drop = sp >= 0 && !keep;
+        const unsigned m = BALLOT(keep), md = BALLOT(drop);
         WSYNC();
-        if (keep) I.slots[w + POPC(m & LANEMASK_LT)] = h;
-        if (h >= 0 && !keep) I.flags[h] &= ~F_HAS_SLOT;
+        if (keep) I.slots[w + POPC(m & LANEMASK_LT)] = sp;
+        if (drop) {
+          I.flags[I.sl_hosted[sp]] &= ~F_HAS_SLOT;
+          I.sl_free[I.sl_free_top + POPC(md & LANEMASK_LT)] = sp;
+        }
         w += POPC(m);
         WSYNC();
+        LANE0(I.sl_free_top += POPC(md));
       }
       LANE0(I.n_slots = w);
     }
@@ -1389,9 +1399,10 @@ EDEVNI int32_t plan_host_group(Inst& I, int32_t l, int32_t hs, int32_t he, int32
 EDEV bool slot_fits(const Inst& I, int32_t host, int32_t abs, int32_t len) {
   for (int32_t r = I.reg_head[host]; r >= 0; r = I.rg_next[r])
     if (abs >= I.rg_start[r] && abs + len <= I.rg_start[r] + I.rg_len[r]) return true;
-  if ((I.flags[host] & F_HAS_SLOT) && abs >= I.slot_abs[host] &&
-      abs + len <= I.slot_abs[host] + I.slot_len[host])
-    return true;
+  if (I.flags[host] & F_HAS_SLOT) {
+    const int32_t sp = I.sidx[host];
+    if (abs >= I.sl_abs[sp] && abs + len <= I.sl_abs[sp] + I.sl_len[sp]) return true;
+  }
   return false;
 }
 
@@ -1494,9 +1505,10 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
         I.tmp_a[gi] = nm;
         for (int32_t i = I.selg_start[gi]; i < I.selg_start[gi + 1]; ++i) {
           const int32_t id = I.sel_ids[i];
-          if (I.generated[id] == 0 && I.reg_cnt[id] == 1) {
+          const int32_t rh = I.reg_head[id];
+          if (I.generated[id] == 0 && rh >= 0 && rh == I.reg_tail[id]) {  // exactly one region
             I.tmp_b[nm] = id;
-            I.tmp_c[nm] = I.rg_start[I.reg_head[id]] + I.prompt[id];
+            I.tmp_c[nm] = I.rg_start[rh] + I.prompt[id];
             nm++;
           }
         }
@@ -1520,12 +1532,15 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
         if (!slot_fits(I, host, abs, len)) { set_error(I, ERR_SLOT_OUTSIDE, hosted, 0); return; }
         if (I.n_slots >= I.slot_cap) { set_error(I, ERR_TABLE_OVERFLOW, hosted, 6); return; }
         if (LANE == 0) {
-          I.slot_host[hosted] = host;
-          I.slot_off[hosted] = I.os_off[i];
-          I.slot_len[hosted] = len;
-          I.slot_abs[hosted] = abs;
+          const int32_t sp = I.sl_free[--I.sl_free_top];
+          I.sl_host[sp] = host;
+          I.sl_off[sp] = I.os_off[i];
+          I.sl_len[sp] = len;
+          I.sl_abs[sp] = abs;
+          I.sl_hosted[sp] = hosted;
+          I.sidx[hosted] = sp;
           I.flags[hosted] |= F_HAS_SLOT;
-          I.slots[I.n_slots++] = hosted;
+          I.slots[I.n_slots++] = sp;
           I.hosted_total++;
           begin_gt_run(I, hosted, true);
           I.gt_scheduled++;
@@ -1831,16 +1846,17 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     bool c = false;
     int32_t h = -1;
     if (si < I.n_slots) {
-      h = I.slots[si];
-      const int32_t host = I.slot_host[h];
-      c = I.state[host] == ST_RUNNING && (I.generated[host] - I.gen_epoch[host]) >= I.slot_off[h];
+      const int32_t sp = I.slots[si];
+      const int32_t host = I.sl_host[sp], off = I.sl_off[sp];
+      h = I.sl_hosted[sp];
+      c = I.state[host] == ST_RUNNING && (I.generated[host] - I.gen_epoch[host]) >= off;
     }
     const unsigned m = BALLOT(c);
     if (c) {
       const int32_t o = ncs + POPC(m & LANEMASK_LT);
       I.tmp_b[o] = h;
-      I.tmp_c[o] = I.slot_host[h];
-      I.tmp_a[I.scr_cap + o] = I.slot_off[h];
+      I.tmp_c[o] = I.sl_host[I.slots[si]];
+      I.tmp_a[I.scr_cap + o] = I.sl_off[I.slots[si]];
     }
     ncs += POPC(m);
   }
@@ -1994,10 +2010,10 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
     kev = e < kev ? e : kev;
   }
   for (int32_t si = LANE; si < I.n_slots; si += W) {
-    const int32_t h = I.slots[si];
-    const int32_t host = I.slot_host[h];
+    const int32_t sp = I.slots[si];
+    const int32_t host = I.sl_host[sp];
     if (I.state[host] == ST_RUNNING) {
-      const int64_t e = (int64_t)I.slot_off[h] - (I.generated[host] - I.gen_epoch[host]);
+      const int64_t e = (int64_t)I.sl_off[sp] - (I.generated[host] - I.gen_epoch[host]);
       kev = e < kev ? e : kev;
     }
   }

@@ -92,6 +92,7 @@ EDEV bool init_req_one(Inst& I, int64_t i) {
 EDEV void init_tables_one(Inst& I, int64_t i) {
   if (i < I.reg_cap) I.reg_free[i] = I.reg_cap - 1 - (int32_t)i;
   if (i < I.grp_cap) I.grp_free[i] = I.grp_cap - 1 - (int32_t)i;
+  if (i < I.slot_cap) I.sl_free[i] = I.slot_cap - 1 - (int32_t)i;
   if (i < I.rl_cap) I.rl_map[i] = -1;
   if (I.ordered) {
     if (i < (int64_t)I.nbuckets * (I.pmax + 1)) { I.cls_head[i] = -1; I.cls_tail[i] = -1; }
@@ -120,6 +121,7 @@ EDEV void init_finish(Inst& I, int64_t first_bad) {
   }
   I.reg_free_top = I.reg_cap;
   I.grp_free_top = I.grp_cap;
+  I.sl_free_top = I.slot_cap;
   I.next_group_id = 1;
 }
 
@@ -739,8 +741,9 @@ __global__ void __launch_bounds__(256) k_jct_hist(const Inst* insts, const int64
   const int bins = 1 << dbits;
   for (int j = threadIdx.x; j < nt * bins; j += blockDim.x) sh[j] = 0;
   __syncthreads();
-  const int64_t n = insts[blockIdx.y].n;
-  const uint64_t* kk = keys + off[blockIdx.y];
+  const Inst& I = insts[blockIdx.y];
+  const int64_t n = I.n;
+  const uint64_t* kk = keys ? keys + off[blockIdx.y] : nullptr;
   const uint64_t* pf = prefixes + (per_instance ? (size_t)blockIdx.y * nt : 0);
   uint64_t p[8];
   for (int t = 0; t < nt; ++t) p[t] = pf[t];
@@ -752,7 +755,14 @@ __global__ void __launch_bounds__(256) k_jct_hist(const Inst* insts, const int64
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += 2 * stride) {
     const bool in0 = i < n, in1 = i + stride < n;
-    const uint64_t k0 = in0 ? __ldcs(kk + i) : 0, k1 = in1 ? __ldcs(kk + i + stride) : 0;
+    uint64_t k0 = 0, k1 = 0;
+    if (kk) {
+      k0 = in0 ? __ldcs(kk + i) : 0;
+      k1 = in1 ? __ldcs(kk + i + stride) : 0;
+    } else {  // keys derived on the fly (no key buffer)
+      k0 = in0 ? jct_key(I, i) : 0;
+      k1 = in1 ? jct_key(I, i + stride) : 0;
+    }
 #pragma unroll 2
     for (int h = 0; h < 2; ++h) {
       const uint64_t k = h ? k1 : k0;
@@ -836,8 +846,7 @@ void layout(Inst& I, char* base, size_t* bytes) {
   I.true_rl = a.take<int32_t>(n);
   GP<int32_t>* i32s[] = {&I.predicted, &I.generated, &I.occupied, &I.allowance, &I.gen_epoch,
                       &I.prefill_done, &I.preempt_count, &I.reserve_draws, &I.held, &I.reg_head,
-                      &I.reg_tail, &I.reg_cnt, &I.reserved, &I.written, &I.slot_host, &I.slot_off,
-                      &I.slot_len, &I.slot_abs, &I.pt_next};
+                      &I.reg_tail, &I.reserved, &I.written, &I.sidx, &I.pt_next};
   for (auto p : i32s) *p = a.take<int32_t>(n);
   I.gt_next = I.pt_next.p;
   I.state = a.take<uint8_t>(n);
@@ -875,6 +884,8 @@ void layout(Inst& I, char* base, size_t* bytes) {
   I.gr_dem = a.take<int64_t>(gc);
   I.run = a.take<int32_t>(I.run_cap + W);
   I.slots = a.take<int32_t>(I.slot_cap + W);
+  GP<int32_t>* sl[] = {&I.sl_host, &I.sl_off, &I.sl_len, &I.sl_abs, &I.sl_hosted, &I.sl_free};
+  for (auto p : sl) *p = a.take<int32_t>(I.slot_cap + W);
   I.ptiter_id = a.take<int32_t>(I.ptiter_cap);
   I.ptiter_tok = a.take<int32_t>(I.ptiter_cap);
   I.adm = a.take<int32_t>(I.adm_cap);
@@ -1274,11 +1285,13 @@ int jct_prepare(econo_batch* b, char* err, size_t errlen) {
     dev_free(b->d_koff);
     b->d_keys = nullptr;
     b->d_koff = nullptr;
-    void *pk, *po;
-    if (dev_alloc(&pk, sizeof(uint64_t) * (size_t)total)) return set_err(err, errlen, "key allocation failed"), ECONO_ECUDA;
-    if (dev_alloc(&po, sizeof(int64_t) * off.size())) {
-      dev_free(pk);
-      return set_err(err, errlen, "key allocation failed"), ECONO_ECUDA;
+    void *pk = nullptr, *po;
+    if (dev_alloc(&po, sizeof(int64_t) * off.size())) return set_err(err, errlen, "key allocation failed"), ECONO_ECUDA;
+    // 8 B per request when HBM allows; a batch that fills the GPU derives each
+    // key from the request's fields in every histogram pass instead
+    if (getenv("ECONO_JCT_NO_KEYS") || cudaMalloc(&pk, sizeof(uint64_t) * (size_t)total) != cudaSuccess) {
+      (void)cudaGetLastError();
+      pk = nullptr;
     }
     b->d_keys = (uint64_t*)pk;
     b->d_koff = (int64_t*)po;
@@ -1287,7 +1300,7 @@ int jct_prepare(econo_batch* b, char* err, size_t errlen) {
   int64_t nmax = 1;
   for (auto& h : b->inst) nmax = imax(nmax, h.desc.n);
   const unsigned gx = (unsigned)imax(1, imin((nmax + 255) / 256, (148 * 8 + ni - 1) / ni));
-  k_jct_keys<<<dim3(gx, (unsigned)ni), 256, 0, b->stream>>>(b->d_insts, b->d_koff, b->d_keys);
+  if (b->d_keys) k_jct_keys<<<dim3(gx, (unsigned)ni), 256, 0, b->stream>>>(b->d_insts, b->d_koff, b->d_keys);
   rc = sync_batch(b, err, errlen);
   if (rc) return rc;
 #endif
@@ -1871,7 +1884,7 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
   if (jobs.empty()) return ECONO_OK;
   const int passes = (bits + 7) / 8;
   // groups of jobs whose keys fit the temp budget; offsets are per group
-  const int64_t budget = (int64_t)256 << 20;  // keys per group (4 x 4 B of temp each)
+  const int64_t budget = (int64_t)128 << 20;  // keys per group (4 x 4 B of temp each: 2 GB)
   std::vector<size_t> gstart;
   int64_t max_off = 0, max_hoff = 0;
   for (size_t g0 = 0; g0 < jobs.size();) {
@@ -2352,23 +2365,25 @@ int64_t econo_snapshot(econo_engine* e, int64_t* out, int64_t cap) {
   // hosting slots in insertion order
   w.push_back(I.n_slots);
   for (int32_t k = 0; k < I.n_slots; ++k) {
-    const int32_t hs = I.slots[k];
-    w.push_back(I.slot_host[hs]);
-    w.push_back(hs);
-    w.push_back(I.slot_off[hs]);
-    w.push_back(I.slot_len[hs]);
-    w.push_back(I.slot_off[hs]);
-    w.push_back(I.slot_abs[hs]);
+    const int32_t sp = I.slots[k];
+    w.push_back(I.sl_host[sp]);
+    w.push_back(I.sl_hosted[sp]);
+    w.push_back(I.sl_off[sp]);
+    w.push_back(I.sl_len[sp]);
+    w.push_back(I.sl_off[sp]);
+    w.push_back(I.sl_abs[sp]);
   }
   // holdings by id
   int64_t nh = 0;
-  for (int32_t id = 0; id < I.n; ++id) nh += I.reg_cnt[id] > 0;
+  for (int32_t id = 0; id < I.n; ++id) nh += I.reg_head[id] >= 0;
   w.push_back(nh);
   for (int32_t id = 0; id < I.n; ++id) {
-    if (I.reg_cnt[id] <= 0) continue;
+    if (I.reg_head[id] < 0) continue;
     w.push_back(id);
     w.push_back(I.held[id]);
-    w.push_back(I.reg_cnt[id]);
+    int64_t nreg = 0;
+    for (int32_t r = I.reg_head[id]; r >= 0; r = I.rg_next[r]) ++nreg;
+    w.push_back(nreg);
     for (int32_t r = I.reg_head[id]; r >= 0; r = I.rg_next[r]) {
       w.push_back(I.rg_start[r]);
       w.push_back(I.rg_len[r]);

@@ -92,3 +92,19 @@ def test_global_percentiles_exact(backend):
     got = metrics.global_percentiles(b, qs)
     want = [ref_percentile(allj, q) for q in qs]
     assert got == want
+
+
+@pytest.mark.gpu
+def test_percentiles_without_key_buffer(monkeypatch):
+    """A batch that fills the GPU has no room for the 8 B/request key buffer:
+    the histogram passes then derive each key from the request's fields.
+    Same exact order statistics either way."""
+    traces = _traces([900, 1300, 250, 4000], 90)
+    o = _opts()
+    want_b = _batch("device", traces, o)
+    want = metrics.global_percentiles(want_b, [0.0, 0.05, 0.5, 0.95, 1.0])
+    want_i = want_b.jct_percentiles([0.05, 0.95])
+    monkeypatch.setenv("ECONO_JCT_NO_KEYS", "1")
+    b = _batch("device", traces, o)
+    assert metrics.global_percentiles(b, [0.0, 0.05, 0.5, 0.95, 1.0]) == want
+    assert np.array_equal(b.jct_percentiles([0.05, 0.95]), want_i)
