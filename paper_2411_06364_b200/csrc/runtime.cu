@@ -425,6 +425,7 @@ struct BulkJob {
   unsigned long long bcnt[ECONO_MAX_BOUNDS + 2];
 };
 constexpr int kBulkTile = 4096;
+constexpr int64_t kBulkBudget = (int64_t)128 << 20;  // keys per ingest group (4 x 4 B of temp each: 2 GB)
 
 __global__ void __launch_bounds__(256) k_bulk_keys(const Inst* insts, BulkJob* jobs, uint32_t* key, uint32_t* val) {
   BulkJob& J = jobs[blockIdx.y];
@@ -970,13 +971,14 @@ unordered:
 int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t n, char* err, size_t errlen) {
   memset(&I, 0, sizeof(I));
   if (n >= (int64_t)1 << 31) return set_err(err, errlen, "trace longer than 2^31 requests"), ECONO_ECONFIG;
-  int64_t pmax = 1;
+  int64_t pmax = 1, rmax = 0;
   for (int64_t i = 0; i < n; ++i) {
     if (t[i].prompt_len < 1 || t[i].prompt_len >= ((int64_t)1 << 30) || t[i].true_rl < 1 ||
         t[i].true_rl >= ((int64_t)1 << 30))
       return set_err(err, errlen, "request %lld: prompt_len and response_len must be in [1, 2^30)", (long long)i),
              ECONO_ECONFIG;
     pmax = imax(pmax, t[i].prompt_len);
+    rmax = imax(rmax, t[i].true_rl);
   }
   I.n = (int32_t)n;
   I.policy = o->policy;
@@ -988,12 +990,8 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   I.chunk = o->chunk_size;
   I.swap_stall = o->swap_stall;
   I.admission_open = 1;
-  {  // max_output_len <= 0 derives it from the trace (engine.hpp:178-180)
-    int64_t mt = 0;
-    if (o->max_output_len <= 0)
-      for (int64_t i = 0; i < n; ++i) mt = imax(mt, t[i].true_rl);
-    I.max_out = o->max_output_len > 0 ? o->max_output_len : mt;
-  }
+  // max_output_len <= 0 derives it from the trace (engine.hpp:178-180)
+  I.max_out = o->max_output_len > 0 ? o->max_output_len : rmax;
   I.full = o->policy == ECONO_POLICY_ECONO_FULL;
   I.pred_model = o->pred_model;
   I.nbd = o->n_deadline_bounds;
@@ -1580,6 +1578,26 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     seeds[2 * i] = opts[i].seed;
     seeds[2 * i + 1] = opts[i].pred_seed;
   }
+#ifndef ECONO_HOSTSIM
+  {  // reserve the burst-ingest scratch now, before the arenas fill the GPU:
+     // a late cudaMalloc next to a nearly full HBM is slow (~0.5 s measured)
+    int64_t keys = 0, kmax = 0, jobs = 0;
+    for (auto& h : b->inst)
+      if (h.desc.ordered && !h.desc.record_events && h.desc.n >= 32768) {
+        keys += h.desc.n;
+        kmax = imax(kmax, h.desc.n);
+        ++jobs;
+      }
+    if (jobs > 0) {
+      const int64_t g = imin(keys, imax((int64_t)kBulkBudget, kmax));  // keys in one group at most
+      const size_t kb = (4 * (size_t)g + 255) & ~(size_t)255;
+      const size_t hb = (4 * 256 * (size_t)(g / kBulkTile + jobs) + 255) & ~(size_t)255;
+      const size_t need = 4 * kb + hb + sizeof(BulkJob) * (size_t)jobs;
+      if (cudaMalloc(&b->bulk_buf, need) == cudaSuccess) b->bulk_bytes = need;
+      else { (void)cudaGetLastError(); b->bulk_buf = nullptr; }
+    }
+  }
+#endif
   {
     size_t total = 0;
     for (auto& h : b->inst) total += h.arena_bytes;
@@ -1884,7 +1902,7 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
   if (jobs.empty()) return ECONO_OK;
   const int passes = (bits + 7) / 8;
   // groups of jobs whose keys fit the temp budget; offsets are per group
-  const int64_t budget = (int64_t)128 << 20;  // keys per group (4 x 4 B of temp each: 2 GB)
+  const int64_t budget = kBulkBudget;
   std::vector<size_t> gstart;
   int64_t max_off = 0, max_hoff = 0;
   for (size_t g0 = 0; g0 < jobs.size();) {
