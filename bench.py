@@ -310,8 +310,11 @@ def run_ours(args):
     b.sync()
     sc1 = b.scalars()
     dbg = b.debug().sum(axis=0) - d0
+    t_steps_done = time.perf_counter()
     parts = b.partials()
     t_e2e = time.perf_counter() - t0
+    e2e_parts = {"create_s": t_created - t0, "ingest_s": t_ingest, "steps_s": t_steps_done - t0 - t_create_ingest,
+                 "partials_s": t_e2e - (t_steps_done - t0)}
     clk = clocks.stop()
     e2e_adm = sum(x.pt_dispatched - y.pt_dispatched for x, y in zip(sc1, sc_a))
     h2d = sum(t.nbytes for t in traces)
@@ -381,7 +384,7 @@ def run_ours(args):
                              "the state each simulated iteration updates (DESIGN.md §5); traffic = ncu DRAM "
                              "bytes per launch of this config (profiles/r01_traffic.json): most of it hits L2"},
         "clocks": clk,
-        "e2e": {"value": e2e_adm_all / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
+        "e2e": {"value": e2e_adm_all / e2e_t, "unit": UNIT, "breakdown": e2e_parts, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "scope": "the whole job through the public API: Batch(host traces) + burst ingest + "
                          "warm-up + timed steps + partial sums to host, wall clock; admissions counted "

@@ -42,7 +42,8 @@ namespace econo {
 // over every instance's requests and only the sequential pieces (the
 // pred_rng_ stream for non-oracle predictors, scalar calibration) run per
 // instance. Phase 1: trace AoS -> SoA, arrival-order check, prompt sum.
-EDEV void init_soa_one(Inst& I, const EconoTraceRecord* tr, int64_t i, bool* order_bad, int64_t* prompt) {
+EDEV void init_soa_one(Inst& I, const EconoTraceRecord* tr, int64_t i, bool* order_bad, int64_t* prompt,
+                       bool* len_bad) {
   double* arr = const_cast<double*>(I.arrival.get());
   int32_t* pr = const_cast<int32_t*>(I.prompt.get());
   int32_t* rl = const_cast<int32_t*>(I.true_rl.get());
@@ -51,6 +52,8 @@ EDEV void init_soa_one(Inst& I, const EconoTraceRecord* tr, int64_t i, bool* ord
   rl[i] = (int32_t)tr[i].true_rl;
   *order_bad = i > 0 && tr[i].arrival_time < tr[i - 1].arrival_time;
   *prompt = tr[i].prompt_len;
+  *len_bad = tr[i].prompt_len < 1 || tr[i].prompt_len >= ((int64_t)1 << 30) || tr[i].true_rl < 1 ||
+             tr[i].true_rl >= ((int64_t)1 << 30);
 }
 // Phase 2 (per instance): calibration t_p / t_g (engine.hpp:171-176); the
 // prompt sum is an exact integer, equal to the reference's sequential
@@ -304,22 +307,26 @@ __global__ void __launch_bounds__(256) k_init_soa(Inst* insts, const EconoTraceR
   const EconoTraceRecord* tr = traces[ii];
   unsigned long long* sc = scr + 4 * ii;
   int64_t psum = 0;
-  long long bad = LLONG_MAX;
+  long long bad = LLONG_MAX, lbad = LLONG_MAX;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I.n; i += (int64_t)gridDim.x * blockDim.x) {
-    bool ob;
+    bool ob, lb;
     int64_t p;
-    init_soa_one(I, tr, i, &ob, &p);
+    init_soa_one(I, tr, i, &ob, &p, &lb);
     psum += p;
     if (ob && i < bad) bad = i;
+    if (lb && i < lbad) lbad = i;
   }
   for (int o = 16; o > 0; o >>= 1) {
     psum += __shfl_xor_sync(0xffffffffu, psum, o);
     const long long b2 = __shfl_xor_sync(0xffffffffu, bad, o);
     bad = b2 < bad ? b2 : bad;
+    const long long l2 = __shfl_xor_sync(0xffffffffu, lbad, o);
+    lbad = l2 < lbad ? l2 : lbad;
   }
   if ((threadIdx.x & 31) == 0) {
     if (psum) atomicAdd(&sc[1], (unsigned long long)psum);
     if (bad != LLONG_MAX) atomicMin(&sc[0], (unsigned long long)bad);
+    if (lbad != LLONG_MAX) atomicMin(&sc[3], (unsigned long long)lbad);
   }
 }
 
@@ -968,11 +975,16 @@ unordered:
 }
 
 // Fills configuration fields and capacities of an Inst from options + trace.
-int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t n, char* err, size_t errlen) {
+// scan = false (the device path): the per-record length checks run in
+// k_init_soa instead of a host pass over every trace; only Orca's derived
+// max_output_len still needs the host scan.
+int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t n, char* err, size_t errlen,
+              bool scan = true) {
   memset(&I, 0, sizeof(I));
   if (n >= (int64_t)1 << 31) return set_err(err, errlen, "trace longer than 2^31 requests"), ECONO_ECONFIG;
   int64_t pmax = 1, rmax = 0;
-  for (int64_t i = 0; i < n; ++i) {
+  const int64_t nscan = (scan || (o->policy == ECONO_POLICY_ORCA && o->max_output_len <= 0)) ? n : 0;
+  for (int64_t i = 0; i < nscan; ++i) {
     if (t[i].prompt_len < 1 || t[i].prompt_len >= ((int64_t)1 << 30) || t[i].true_rl < 1 ||
         t[i].true_rl >= ((int64_t)1 << 30))
       return set_err(err, errlen, "request %lld: prompt_len and response_len must be in [1, 2^30)", (long long)i),
@@ -1026,7 +1038,10 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   I.pt_min_lb = INT64_MAX;
   I.skip = (getenv("ECONO_NO_SKIP") || I.base) ? 0 : 1;
   // capacities
-  I.pmax = (int32_t)pmax;
+  // PT class tables span prompts 1..pmax. Ordered (econoserve) policies
+  // reject any prompt above the reserved pool at init (engine.hpp:202-206),
+  // so the pool size bounds the classes without scanning the trace.
+  I.pmax = (int32_t)(I.ordered ? imax(1, I.reserve_cap) : pmax);
   I.nbuckets = I.nbd + 1;
   I.bm_words = (I.pmax >> 6) + 1;
   I.bm_l2 = (I.bm_words >> 6) + 1;
@@ -1554,7 +1569,11 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
       th.emplace_back([&, t] {
         char e2[512];
         for (int32_t i = t; i < n_inst; i += nt) {
+#ifdef ECONO_HOSTSIM
           rcs[(size_t)i] = configure(b->inst[(size_t)i].desc, &opts[i], traces[i], ns[i], e2, sizeof(e2));
+#else  // the record checks run on the device (k_init_soa)
+          rcs[(size_t)i] = configure(b->inst[(size_t)i].desc, &opts[i], traces[i], ns[i], e2, sizeof(e2), false);
+#endif
           if (rcs[(size_t)i]) msgs[(size_t)i] = e2;
         }
       });
@@ -1648,9 +1667,9 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     mt_seed(I.pmt, I.pmt_i, seeds[2 * i + 1]);
     int64_t bad_order = I.n, psum = 0;
     for (int64_t k = 0; k < I.n; ++k) {
-      bool ob;
+      bool ob, lb;
       int64_t p;
-      init_soa_one(I, traces[i], k, &ob, &p);
+      init_soa_one(I, traces[i], k, &ob, &p, &lb);
       psum += p;
       if (ob && k < bad_order) bad_order = k;
     }
@@ -1720,7 +1739,7 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     dev_h2d(dt, d_traces.data(), sizeof(void*) * (size_t)n_inst);
     dev_h2d(ds, seeds.data(), sizeof(uint64_t) * 2 * (size_t)n_inst);
     std::vector<unsigned long long> sc0(4 * (size_t)n_inst, 0);
-    for (int32_t i = 0; i < n_inst; ++i) sc0[4 * (size_t)i] = sc0[4 * (size_t)i + 2] = ~0ULL;
+    for (int32_t i = 0; i < n_inst; ++i) sc0[4 * (size_t)i] = sc0[4 * (size_t)i + 2] = sc0[4 * (size_t)i + 3] = ~0ULL;
     dev_h2d(dsc, sc0.data(), sizeof(unsigned long long) * sc0.size());
     int64_t nmax = 0, emax = 0;
     for (auto& h : b->inst) {
@@ -1749,6 +1768,26 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
       cudaEventRecord(converted[k], b->stream);
     }
     cudaStreamSynchronize(b->stream);
+    {  // per-record length checks from k_init_soa, in instance order
+      std::vector<unsigned long long> sc1(sc0.size());
+      dev_d2h(sc1.data(), dsc, sizeof(unsigned long long) * sc1.size());
+      for (int32_t i = 0; i < n_inst; ++i)
+        if (sc1[4 * (size_t)i + 3] < (unsigned long long)ns[i]) {
+          set_err(err, errlen, "request %lld: prompt_len and response_len must be in [1, 2^30)",
+                  (long long)sc1[4 * (size_t)i + 3]);
+          for (int k = 0; k < 2; ++k) {
+            cudaEventDestroy(copied[k]);
+            cudaEventDestroy(converted[k]);
+          }
+          cudaStreamDestroy(cs);
+          for (int k = 0; k < nbuf; ++k) dev_free(stage[k]);
+          dev_free(dt);
+          dev_free(ds);
+          dev_free(dsc);
+          econo_batch_destroy(b);
+          return ECONO_ECONFIG;
+        }
+    }
     const auto t1 = now();
     for (int k = 0; k < 2; ++k) {
       cudaEventDestroy(copied[k]);

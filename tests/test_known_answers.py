@@ -250,3 +250,12 @@ def test_exact_allocation_and_pipelining_safety(backend):  # acceptance C1/C2 (o
     _, rep = e.finalize()
     assert rep.allocation_failure_pct == 0.0 and rep.preemptions == 0
     assert rep.hosted_slots > 0 and rep.hosted_overruns == 0
+
+
+@pytest.mark.parametrize("backend", ["hostsim", pytest.param("device", marks=pytest.mark.gpu)])
+def test_record_length_range_checked(backend):
+    """The device path's per-record range check (k_init_soa on the device,
+    the host scan in the host build): the first offending request is named."""
+    o = base_options("econoserve-full")
+    with pytest.raises(ConfigError, match=r"request 2: prompt_len and response_len must be in \[1, 2\^30\)"):
+        make_engine(backend, [(0.1, 10, 10), (0.2, 10, 10), (0.3, 0, 10), (0.4, 10, 0)], o)
