@@ -1164,6 +1164,9 @@ struct econo_batch {
   size_t bulk_bytes = 0;
   int64_t keys_total = 0;
   int64_t n_base = 0;  // baseline-policy instances (k_baseline_steps)
+  // trace staging buffers, kept until destroy: a cudaFree right after the
+  // upload stalls for up to ~0.3 s next to a nearly full HBM (measured)
+  void* stage[2] = {nullptr, nullptr};
   std::vector<uint64_t> h_keys;  // host build
 #ifndef ECONO_HOSTSIM
   cudaStream_t stream = nullptr;
@@ -1516,6 +1519,8 @@ void econo_batch_destroy(econo_batch* b) {
   dev_free(b->d_keys);
   dev_free(b->d_koff);
   dev_free(b->bulk_buf);
+  dev_free(b->stage[0]);
+  dev_free(b->stage[1]);
   for (auto* v : b->views) delete v;
 #ifndef ECONO_HOSTSIM
   if (b->stream) cudaStreamDestroy(b->stream);
@@ -1794,7 +1799,8 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
       cudaEventDestroy(converted[k]);
     }
     cudaStreamDestroy(cs);
-    for (int k = 0; k < nbuf; ++k) dev_free(stage[k]);
+    b->stage[0] = stage[0];
+    b->stage[1] = stage[1];
     const unsigned gx2 = (unsigned)imin(imax(1, (emax + 255) / 256), 1184 / imax(1, n_inst / 8 + 1) + 1);
     k_init_scalar<<<(unsigned)n_inst, 32, 0, b->stream>>>(b->d_insts, (const uint64_t*)ds,
                                                           (const unsigned long long*)dsc);
