@@ -69,50 +69,60 @@ def make_traces(gen, n, seeds, threads=32, pinned=False):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks and clock-event (throttle) reasons sampled through NVML by a
+    thread polling every millisecond, started right before the timed steps
+    and stopped right after them (plus one sample at each end). In-process
+    NVML reads replace an `nvidia-smi -lms` subprocess, whose periodic queries
+    stalled CUDA calls of the job for up to ~0.5 s."""
+    REASONS = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4)]
 
     def __init__(self, index):
         self.index = index
         self.rows = []
-        self.proc = None
+        self.h = None
+        self.stop_ev = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 — no NVML: no clock record
+            self.h = None
+
+    def _sample(self):
+        nv = self.nv
+        try:
+            try:
+                reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except AttributeError:
+                reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+            self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), reasons))
+        except Exception:  # noqa: BLE001 — a failed read is skipped
+            pass
+
+    def _loop(self):
+        while not self.stop_ev.wait(0.001):
+            self._sample()
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except OSError:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+        if self.h is None:
+            return
+        self._sample()
+        self.thread = threading.Thread(target=self._loop, daemon=True)
+        self.thread.start()
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-            self.thread.join(timeout=2)
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for k, nm in enumerate(names):
-                if len(r) > 5 + k and r[5 + k].lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        self.stop_ev.set()
+        self.thread.join(timeout=2)
+        self._sample()
+        reasons = sorted({nm for _, r in self.rows for nm, bit in self.REASONS if r & bit})
+        return {"sm_mhz": float(np.median([c for c, _ in self.rows])) if self.rows else None,
+                "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML, 1 ms polling over the timed steps"}
 
 
 def measured_traffic(instances, iters):
@@ -270,7 +280,6 @@ def run_ours(args):
     # K device-timed steps -> partial sums back to the host [D2H]. `value` is
     # the device-timed K steps; `e2e` is the same job's wall clock end to end.
     clocks = ClockSampler(local)
-    clocks.start()
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
     if world > 1:
@@ -298,11 +307,13 @@ def run_ours(args):
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    clocks.start()
     e0.record(stream)
     for _ in range(args.steps):
         b.launch(args.iters, stream.cuda_stream)
     e1.record(stream)
     e1.synchronize()
+    clk = clocks.stop()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -315,7 +326,6 @@ def run_ours(args):
     t_e2e = time.perf_counter() - t0
     e2e_parts = {"create_s": t_created - t0, "ingest_s": t_ingest, "steps_s": t_steps_done - t0 - t_create_ingest,
                  "partials_s": t_e2e - (t_steps_done - t0)}
-    clk = clocks.stop()
     e2e_adm = sum(x.pt_dispatched - y.pt_dispatched for x, y in zip(sc1, sc_a))
     h2d = sum(t.nbytes for t in traces)
     d2h = parts.nbytes + I * 2 * 1600
