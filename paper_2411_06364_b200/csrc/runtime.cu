@@ -1167,6 +1167,11 @@ struct econo_batch {
   // trace staging buffers, kept until destroy: a cudaFree right after the
   // upload stalls for up to ~0.3 s next to a nearly full HBM (measured)
   void* stage[2] = {nullptr, nullptr};
+  // small per-call device scratch (init descriptors, ingest plan, partial
+  // sums, histogram passes), cached per slot and only ever grown: cudaFree /
+  // cudaMalloc next to a nearly full HBM stall for tens to hundreds of ms
+  void* scr[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t scr_bytes[6] = {0, 0, 0, 0, 0, 0};
   std::vector<uint64_t> h_keys;  // host build
 #ifndef ECONO_HOSTSIM
   cudaStream_t stream = nullptr;
@@ -1179,6 +1184,25 @@ struct econo_engine {
   int32_t i;
   bool owns;
 };
+
+namespace {
+enum { SCR_INIT = 0, SCR_PLAN, SCR_PART_OUT, SCR_PART_SLICES, SCR_HIST_PREFIX, SCR_HIST };
+void dev_free(void* p);
+int dev_alloc(void** p, size_t sz);
+// Cached device scratch of at least `bytes` for one purpose (see econo_batch::scr).
+void* batch_scratch(econo_batch* b, int slot, size_t bytes) {
+  if (bytes > b->scr_bytes[slot]) {
+    dev_free(b->scr[slot]);
+    b->scr[slot] = nullptr;
+    b->scr_bytes[slot] = 0;
+    void* p;
+    if (dev_alloc(&p, bytes)) return nullptr;
+    b->scr[slot] = p;
+    b->scr_bytes[slot] = bytes;
+  }
+  return b->scr[slot];
+}
+}  // namespace
 
 namespace {
 
@@ -1372,13 +1396,11 @@ int jct_hist(econo_batch* b, int per_instance, int nt, const uint64_t* prefixes,
     cudaFuncSetAttribute(k_jct_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2048 * 4);
     smem_set = true;
   }
-  void *dp, *dh;
   const size_t hbytes = sizeof(uint64_t) * (size_t)groups * nu * bins;
-  if (dev_alloc(&dp, sizeof(uint64_t) * (size_t)groups * nu)) return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
-  if (dev_alloc(&dh, hbytes)) {
-    dev_free(dp);
-    return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
-  }
+  void* dp = batch_scratch(b, SCR_HIST_PREFIX, sizeof(uint64_t) * (size_t)groups * nu);
+  void* dh = batch_scratch(b, SCR_HIST, hbytes);
+  if (!dp || !dh) return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
+  cudaMemsetAsync(dh, 0, hbytes, b->stream);  // the passes accumulate with atomics
   dev_h2d(dp, up.data(), sizeof(uint64_t) * (size_t)groups * nu);
   int64_t nmax = 1;
   for (auto& h : b->inst) nmax = imax(nmax, h.desc.n);
@@ -1398,8 +1420,6 @@ int jct_hist(econo_batch* b, int per_instance, int nt, const uint64_t* prefixes,
       for (int t = 0; t < nt; ++t)
         memcpy(hist + ((size_t)g * nt + t) * bins, hu.data() + ((size_t)g * nu + map_t[(size_t)g * nt + t]) * bins,
                sizeof(uint64_t) * bins);
-  dev_free(dp);
-  dev_free(dh);
   return rc;
 #endif
 }
@@ -1521,6 +1541,7 @@ void econo_batch_destroy(econo_batch* b) {
   dev_free(b->bulk_buf);
   dev_free(b->stage[0]);
   dev_free(b->stage[1]);
+  for (auto* p : b->scr) dev_free(p);
   for (auto* v : b->views) delete v;
 #ifndef ECONO_HOSTSIM
   if (b->stream) cudaStreamDestroy(b->stream);
@@ -1737,10 +1758,15 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
         o += sizeof(EconoTraceRecord) * (size_t)ns[i];
       }
     }
-    void *dt, *ds, *dsc;
-    dev_alloc(&dt, sizeof(void*) * (size_t)n_inst);
-    dev_alloc(&ds, sizeof(uint64_t) * 2 * (size_t)n_inst);
-    dev_alloc(&dsc, sizeof(unsigned long long) * 4 * (size_t)n_inst);
+    char* dinit = (char*)batch_scratch(b, SCR_INIT, 56 * (size_t)n_inst + 512);
+    if (!dinit) {
+      for (int k = 0; k < nbuf; ++k) dev_free(stage[k]);
+      econo_batch_destroy(b);
+      return set_err(err, errlen, "device allocation failed"), ECONO_ECUDA;
+    }
+    void* dt = dinit;
+    void* ds = dinit + ((8 * (size_t)n_inst + 255) & ~(size_t)255);
+    void* dsc = (char*)ds + ((16 * (size_t)n_inst + 255) & ~(size_t)255);
     dev_h2d(dt, d_traces.data(), sizeof(void*) * (size_t)n_inst);
     dev_h2d(ds, seeds.data(), sizeof(uint64_t) * 2 * (size_t)n_inst);
     std::vector<unsigned long long> sc0(4 * (size_t)n_inst, 0);
@@ -1786,9 +1812,6 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
           }
           cudaStreamDestroy(cs);
           for (int k = 0; k < nbuf; ++k) dev_free(stage[k]);
-          dev_free(dt);
-          dev_free(ds);
-          dev_free(dsc);
           econo_batch_destroy(b);
           return ECONO_ECONFIG;
         }
@@ -1811,9 +1834,6 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     if (verbose)
       fprintf(stderr, "[econo] create: trace upload + SoA conversion %.1f ms (%zu MB), init kernels %.1f ms\n", ms(t0, t1),
               total >> 20, ms(t1, t2));
-    dev_free(dt);
-    dev_free(ds);
-    dev_free(dsc);
     if (rc) { econo_batch_destroy(b); return rc; }
   }
 #endif
@@ -1891,18 +1911,13 @@ int econo_batch_partials(econo_batch* b, double* out, char* err, size_t errlen) 
   for (auto& h : b->inst) nmax = imax(nmax, h.desc.n);
   // enough blocks to fill the machine a few times over, no more than the work
   const int32_t slices = (int32_t)imax(1, imin((nmax + 255) / 256, (148 * 8 + ni - 1) / ni));
-  void *d, *scr;
-  if (dev_alloc(&d, bytes)) return set_err(err, errlen, "device allocation failed"), ECONO_ECUDA;
-  if (dev_alloc(&scr, sizeof(double) * 16 * (size_t)slices * (size_t)ni)) {
-    dev_free(d);
-    return set_err(err, errlen, "device allocation failed"), ECONO_ECUDA;
-  }
+  void* d = batch_scratch(b, SCR_PART_OUT, bytes);
+  void* scr = batch_scratch(b, SCR_PART_SLICES, sizeof(double) * 16 * (size_t)slices * (size_t)ni);
+  if (!d || !scr) return set_err(err, errlen, "device allocation failed"), ECONO_ECUDA;
   k_partials_slices<<<dim3((unsigned)slices, (unsigned)ni), 256, 0, b->stream>>>(b->d_insts, (double*)scr);
   k_partials_finish<<<(unsigned)ni, 32, 0, b->stream>>>(b->d_insts, (const double*)scr, slices, (double*)d);
   int rc = sync_batch(b, err, errlen);
   if (!rc && dev_d2h(out, d, bytes)) rc = ECONO_ECUDA;
-  dev_free(scr);
-  dev_free(d);
   return rc;
 #endif
 }
@@ -1917,13 +1932,12 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms = [](auto a, auto b2) { return std::chrono::duration<double, std::milli>(b2 - a).count(); };
   const auto t0 = now();
-  void* dplan;
-  if (dev_alloc(&dplan, sizeof(int64_t) * 2 * (size_t)ni)) return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
+  void* dplan = batch_scratch(b, SCR_PLAN, sizeof(int64_t) * 2 * (size_t)ni);
+  if (!dplan) return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
   k_bulk_plan<<<(unsigned)ni, 32, 0, b->stream>>>(b->d_insts, (int64_t*)dplan);
   std::vector<int64_t> plan(2 * (size_t)ni);
   int rc = sync_batch(b, err, errlen);
   if (!rc && dev_d2h(plan.data(), dplan, sizeof(int64_t) * plan.size())) rc = ECONO_ECUDA;
-  dev_free(dplan);
   if (rc) return rc;
   const char* env = getenv("ECONO_BULK_INGEST_MIN");
   const int64_t thr = env ? atoll(env) : 32768;
