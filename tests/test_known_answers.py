@@ -259,3 +259,17 @@ def test_record_length_range_checked(backend):
     o = base_options("econoserve-full")
     with pytest.raises(ConfigError, match=r"request 2: prompt_len and response_len must be in \[1, 2\^30\)"):
         make_engine(backend, [(0.1, 10, 10), (0.2, 10, 10), (0.3, 0, 10), (0.4, 10, 0)], o)
+
+
+def test_instance_bytes_sizing():
+    """econo_instance_bytes: the HBM an instance takes (capacity planning)."""
+    from paper_2411_06364_b200.engine import instance_bytes
+    from conftest import HOSTSIM
+    o = base_options("econoserve-full")
+    small = instance_bytes([(0.1 * i, 10, 10) for i in range(20000)], o, lib=HOSTSIM)
+    big = instance_bytes([(0.1 * i, 10, 10) for i in range(40000)], o, lib=HOSTSIM)
+    # beyond the KVC-capacity-sized tables, each request costs its SoA fields (DESIGN.md §3)
+    assert 0 < small < big and 140 < (big - small) / 20000 < 160
+    o.tfs = 0
+    with pytest.raises(ConfigError, match="tfs must be >= 1"):
+        instance_bytes([(0.1, 10, 10)], o, lib=HOSTSIM)
