@@ -234,7 +234,7 @@ def algorithmic_bytes(sc_before, sc_after, iters, n_inst):
     return n_inst * iters * (48.0 * run + 64.0) + 40.0 * pt + 96.0 * gt
 
 
-def auto_instances(n, device, sms=148):
+def auto_instances(n, device, sms=148, world=1):
     """As many instances per SM as the GPU's free HBM holds: each needs its
     arena (econo_instance_bytes), plus the burst-ingest scratch (<= 2.2 GB).
     The end-of-run JCT keys (8 B per request) get a buffer only if HBM is
@@ -247,7 +247,7 @@ def auto_instances(n, device, sms=148):
     t = generate_trace(n, c["rate"], c["shape"]["prompt"], c["shape"]["rl"], 1000)
     per = instance_bytes(t, options())
     free, _ = torch.cuda.mem_get_info(device)
-    slack = 1 << 30  # staging buffers, partial-sum scratch, the CUDA context's growth
+    slack = (1 << 30) if world == 1 else (4 << 30)  # staging, scratch, context growth (+ NCCL's own)
     for k in range(16, 0, -1):
         inst = k * sms
         if inst * per + 2.2e9 + slack <= free:  # + the ingest scratch (128M keys x 16 B)
@@ -268,7 +268,16 @@ def run_ours(args):
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    I = args.instances or auto_instances(args.n, local)
+    if world > 1:  # bring NCCL's buffers up before sizing the batch to the free HBM
+        x = torch.ones(1, device=dev)
+        dist.all_reduce(x)
+        dist.barrier()
+        torch.cuda.synchronize()
+    I = args.instances or auto_instances(args.n, local, world=world)
+    if world > 1:  # every rank runs the same count (the smallest fit)
+        t_i = torch.tensor([I], dtype=torch.int64, device=dev)
+        dist.all_reduce(t_i, op=dist.ReduceOp.MIN)
+        I = int(t_i.item())
     seeds = [1000 + rank * I + i for i in range(I)]
     t0 = time.time()
     # host trace generation shares the box's cores between the ranks
