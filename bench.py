@@ -125,7 +125,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": "NVML, 1 ms polling over the timed steps"}
 
 
-def measured_traffic(instances, iters):
+def measured_traffic(instances, iters, slice_us=0):
     """DRAM bytes per k_engine_steps launch from the committed ncu capture of
     this exact configuration (profiles/r01_traffic.json), else None."""
     p = os.path.join(ROOT, "profiles", "r01_traffic.json")
@@ -134,7 +134,8 @@ def measured_traffic(instances, iters):
     with open(p) as f:
         d = json.load(f)
     c = d.get("config", {})
-    if c.get("instances_per_gpu") == instances and c.get("iters_per_step") == iters:
+    if c.get("instances_per_gpu") == instances and c.get("slice_us", 0) == slice_us and \
+            (slice_us or c.get("iters_per_step") == iters):
         return d["dram_bytes_per_launch"]
     return None
 
@@ -221,7 +222,7 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------
-def algorithmic_bytes(sc_before, sc_after, iters, n_inst):
+def algorithmic_bytes(sc_before, sc_after, iters, n_inst, total_iters=None):
     """Minimal HBM bytes one step's scheduler iterations must touch with this
     design: per executed iteration 48 B per running request
     (generated/occupied/written r+w, exec_t r+w, true_rl, allowance, state)
@@ -231,7 +232,8 @@ def algorithmic_bytes(sc_before, sc_after, iters, n_inst):
     run = np.mean([s.running for s in sc_after])
     pt = sum(a.pt_dispatched - b.pt_dispatched for a, b in zip(sc_after, sc_before))
     gt = sum(a.gt_scheduled - b.gt_scheduled for a, b in zip(sc_after, sc_before))
-    return n_inst * iters * (48.0 * run + 64.0) + 40.0 * pt + 96.0 * gt
+    it = total_iters if total_iters is not None else n_inst * iters
+    return it * (48.0 * run + 64.0) + 40.0 * pt + 96.0 * gt
 
 
 def auto_instances(n, device, sms=148, world=1):
@@ -305,8 +307,10 @@ def run_ours(args):
     t_create_ingest = time.perf_counter() - t0
     t_ingest = time.perf_counter() - t_created
     sc_a = b.scalars()
+    slice_ns = int(args.slice_us * 1000)
+    step_n = (1 << 40) if slice_ns else args.iters
     for _ in range(args.warmup):
-        b.launch(args.iters, stream.cuda_stream)
+        b.launch(step_n, stream.cuda_stream, slice_ns=slice_ns)
     stream.synchronize()
     b.sync()
     sc0 = b.scalars()
@@ -319,7 +323,7 @@ def run_ours(args):
     clocks.start()
     e0.record(stream)
     for _ in range(args.steps):
-        b.launch(args.iters, stream.cuda_stream)
+        b.launch(step_n, stream.cuda_stream, slice_ns=slice_ns)
     e1.record(stream)
     e1.synchronize()
     clk = clocks.stop()
@@ -344,7 +348,9 @@ def run_ours(args):
     adm = sum(a.pt_dispatched - z.pt_dispatched for a, z in zip(sc1, sc0))
     gts = sum(a.gt_scheduled - z.gt_scheduled for a, z in zip(sc1, sc0))
     tot = float(sum(times))
-    abytes = algorithmic_bytes(sc0, sc1, args.iters * args.steps, I)
+    it_done = sum(a.steps - z.steps for a, z in zip(sc1, sc0))  # scheduler iterations, all instances
+    it_warm = sum(a.steps - z.steps for a, z in zip(sc0, sc_a))
+    abytes = algorithmic_bytes(sc0, sc1, 0, I, total_iters=it_done)
     t = torch.tensor([tot, float(adm), float(gts), float(e2e_adm), t_e2e], dtype=torch.float64,
                      device=dev)
     # end-of-run report reduction (after the e2e window): exact global p5/p95
@@ -370,8 +376,9 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     value = adm_all / tot_max
-    iters_total = args.iters * args.steps
+    iters_total = it_done / I  # per instance over the window
     us_iter = 1e6 * tot_max / iters_total
+    ips = iters_total / args.steps
     peak, peak_kind = measured_peaks()
     achieved = abytes / tot / 1e9  # GB/s, this rank's launches
     line = {
@@ -379,10 +386,17 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "requests_per_instance": args.n,
-                   "instances_per_gpu": I, "iters_per_step": args.iters,
+                   "instances_per_gpu": I, "iters_per_step": round(ips, 1),
+                   "launch": (f"time-sliced: each step is one k_engine_steps launch in which every instance "
+                              f"advances until {args.slice_us:g} us of device time have passed (econo_batch_"
+                              f"launch_slice), ~{ips:.0f} scheduler iterations per instance on average"
+                              if slice_ns else f"{args.iters} scheduler iterations per instance per launch"),
                    "policy": W.CONFIGS[WORKLOAD]["opts"]["policy"],
-                   "l2": f"inputs larger than L2: {I} x ~184 MB of instance state per GPU vs 126 MB L2, no flush",
-                   "window": window_str(args)},
+                   "l2": f"inputs larger than L2: {I} x ~157 MB of instance state per GPU vs 126 MB L2, no flush",
+                   "window": (window_str(args) if not slice_ns else
+                              f"after the 1M burst ingest: {args.warmup} warm-up and {args.steps} timed slices; "
+                              f"scheduler iterations ~{2 + (it_warm / I):.0f}..{2 + (it_warm + it_done) / I:.0f} "
+                              f"per instance on average")},
         "us_per_iter": us_iter,
         "device_cycles": {"quiet_test": int(dbg[0]), "quiet_replay": int(dbg[1]), "normal_steps": int(dbg[2]),
                           "quiet_spans": int(dbg[4]), "normal_step_count": int(dbg[5])},
@@ -396,7 +410,7 @@ def run_ours(args):
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
-                     "traffic": measured_traffic(I, args.iters),
+                     "traffic": measured_traffic(I, args.iters, args.slice_us if slice_ns else 0),
                      "per_launch_algorithmic_bytes": abytes / args.steps, "peak_kind": peak_kind,
                      "kernel": "k_engine_steps",
                      "note": "latency-bound dependency chain (one warp per instance); algorithmic bytes = "
@@ -600,6 +614,10 @@ def main():
                          "requests, so 8 per SM = 1184 on a B200)")
     ap.add_argument("--iters", type=int, default=1000,
                     help="scheduler iterations per instance per step (one k_engine_steps launch)")
+    ap.add_argument("--slice-us", type=float, default=250.0,
+                    help="time-sliced steps: each launch runs every instance until this much device time has "
+                         "passed (0 = a fixed --iters iterations per instance, every launch waiting for its "
+                         "slowest instance)")
     ap.add_argument("--ref-iters", type=int, default=100,
                     help="reference arm / cpu_baseline: step() calls per engine per step (bounded sample)")
     ap.add_argument("--n", type=int, default=1_000_000)

@@ -266,6 +266,11 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* n, 
  * max_steps steps on `stream` (a cudaStream_t, NULL = the handle's stream).
  * Asynchronous: no host synchronisation. */
 int econo_batch_launch(econo_batch* b, int64_t max_steps, void* stream);
+/* Time-sliced launch: every live instance advances by up to max_steps steps
+ * but stops at the first step boundary after slice_ns of device time, so a
+ * slow instance no longer holds every other SM idle until it finishes (the
+ * host build ignores the slice). Asynchronous like econo_batch_launch. */
+int econo_batch_launch_slice(econo_batch* b, int64_t max_steps, int64_t slice_ns, void* stream);
 /* Grid-wide ingest of the arrivals every instance would admit at the start of
  * its next step (ingest_arrivals, engine.hpp:216-235): the same class lists,
  * bitmaps and counters the in-kernel ingest builds, produced for large bursts

@@ -134,12 +134,27 @@ EDEV void init_finish(Inst& I, int64_t first_bad) {
 // the budget), and a step after a completion finds freed KVC for the GT
 // queue head. Skipping the test is always exact — it only decides whether a
 // replay may stand in for normal steps.
+// Device wall clock (ns), for time-sliced launches.
+EDEV int64_t now_ns() {
+#ifdef __CUDA_ARCH__
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (int64_t)t;
+#else
+  return 0;
+#endif
+}
+
+// deadline_ns > 0 (a time-sliced launch, econo_batch_launch_slice): stop at
+// the first step boundary past the deadline; every instance then advances as
+// far as the slice allows instead of all waiting for the slowest one.
 template <bool B>
-EDEVNI void engine_steps(Inst& I, int64_t max_steps) {
+EDEVNI void engine_steps(Inst& I, int64_t max_steps, int64_t deadline_ns = 0) {
   LANE0(I.status = STATUS_RUN);
   bool test = true;
   for (int64_t s = 0; s < max_steps;) {
     if (I.error || I.completed >= I.n) break;
+    if (deadline_ns && now_ns() >= deadline_ns) break;
     if ((I.record_events && I.ev_n + step_event_bound(I) > I.ev_cap) ||
         (I.record_samples && I.sm_n + 1 > I.sm_cap)) {
       LANE0(I.status = STATUS_DRAIN);
@@ -371,23 +386,25 @@ __global__ void __launch_bounds__(32) k_init_finish(Inst* insts, const unsigned 
   if (threadIdx.x == 0 && !I.error) init_finish(I, bad < (unsigned long long)I.n ? (int64_t)bad : I.n);
 }
 
-__global__ void __launch_bounds__(32) k_engine_steps(Inst* insts, int64_t max_steps) {
+__global__ void __launch_bounds__(32) k_engine_steps(Inst* insts, int64_t max_steps, int64_t slice_ns) {
   if (insts[blockIdx.x].base) return;  // a baseline-policy instance (k_baseline_steps)
+  const int64_t deadline = slice_ns > 0 ? now_ns() + slice_ns : 0;
   __shared__ Inst I;
   const int64_t t0 = PROF_NOW();
   inst_load(I, &insts[blockIdx.x]);
-  engine_steps<false>(I, max_steps);
+  engine_steps<false>(I, max_steps, deadline);
   LANE0(I.prof[11] += PROF_NOW() - t0; I.prof[12]++);
   inst_store(&insts[blockIdx.x], I);
 }
 
 // The comparison policies (orca, vllm, sarathi, multires, sync-coupled) in
 // their own kernel, so the econoserve kernel's code is not affected by them.
-__global__ void __launch_bounds__(32) k_baseline_steps(Inst* insts, int64_t max_steps) {
+__global__ void __launch_bounds__(32) k_baseline_steps(Inst* insts, int64_t max_steps, int64_t slice_ns) {
   if (!insts[blockIdx.x].base) return;
+  const int64_t deadline = slice_ns > 0 ? now_ns() + slice_ns : 0;
   __shared__ Inst I;
   inst_load(I, &insts[blockIdx.x]);
-  engine_steps<true>(I, max_steps);
+  engine_steps<true>(I, max_steps, deadline);
   inst_store(&insts[blockIdx.x], I);
 }
 
@@ -1272,9 +1289,10 @@ int drain(HostInst& h) {
   return 0;
 }
 
-void launch_steps(econo_batch* b, int64_t max_steps, void* stream) {
+void launch_steps(econo_batch* b, int64_t max_steps, void* stream, int64_t slice_ns = 0) {
 #ifdef ECONO_HOSTSIM
   (void)stream;
+  (void)slice_ns;  // the host build has no device clock: max_steps only
   for (auto& h : b->inst) {
     if (h.desc.base) engine_steps<true>(h.desc, max_steps);
     else engine_steps<false>(h.desc, max_steps);
@@ -1283,8 +1301,8 @@ void launch_steps(econo_batch* b, int64_t max_steps, void* stream) {
 #else
   cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
   if (b->n_base < (int64_t)b->inst.size())
-    k_engine_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps);
-  if (b->n_base > 0) k_baseline_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps);
+    k_engine_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
+  if (b->n_base > 0) k_baseline_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
 #endif
 }
 
@@ -1853,6 +1871,11 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
 
 int econo_batch_launch(econo_batch* b, int64_t max_steps, void* stream) {
   launch_steps(b, max_steps, stream);
+  return ECONO_OK;
+}
+
+int econo_batch_launch_slice(econo_batch* b, int64_t max_steps, int64_t slice_ns, void* stream) {
+  launch_steps(b, max_steps, stream, slice_ns > 0 ? slice_ns : 0);
   return ECONO_OK;
 }
 

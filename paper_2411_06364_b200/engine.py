@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(HERE, "_lib", "libeconoserve_b200.so")
 SYMBOLS = [
     "econo_default_options", "econo_create", "econo_step", "econo_run", "econo_records",
     "econo_report", "econo_events", "econo_samples", "econo_scalars", "econo_snapshot",
-    "econo_destroy", "econo_instance_bytes", "econo_batch_create", "econo_batch_launch", "econo_batch_sync",
+    "econo_destroy", "econo_instance_bytes", "econo_batch_create", "econo_batch_launch", "econo_batch_launch_slice", "econo_batch_sync",
     "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
     "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore", "econo_batch_debug",
     "econo_batch_reports", "econo_batch_jct_prepare", "econo_batch_jct_hist", "econo_batch_jct_percentiles",
@@ -82,6 +82,7 @@ def load(path=None):
     L.econo_batch_create.argtypes = [C.POINTER(vp), C.POINTER(i64), i32, C.POINTER(abi.Options),
                                      C.c_int, C.POINTER(vp), cp, sz]
     L.econo_batch_launch.argtypes = [vp, i64, vp]
+    L.econo_batch_launch_slice.argtypes = [vp, i64, i64, vp]
     L.econo_batch_sync.argtypes = [vp, cp, sz]
     L.econo_batch_scalars.argtypes = [vp, C.POINTER(abi.Scalars)]
     L.econo_batch_engine.argtypes = [vp, i32, C.POINTER(vp)]
@@ -263,8 +264,11 @@ class Batch:
 
     __del__ = close
 
-    def launch(self, max_steps, stream=None):
-        self._L.econo_batch_launch(self.h, max_steps, stream)
+    def launch(self, max_steps, stream=None, slice_ns=0):
+        if slice_ns:
+            self._L.econo_batch_launch_slice(self.h, max_steps, int(slice_ns), stream)
+        else:
+            self._L.econo_batch_launch(self.h, max_steps, stream)
 
     def sync(self):
         err = C.create_string_buffer(1024)

@@ -14,6 +14,7 @@ def main():
     ap.add_argument("--instances", type=int, required=True)
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--launches", type=int, default=10)
+    ap.add_argument("--slice-us", type=float, default=0)
     ap.add_argument("--out", default="profiles/r01_traffic.json")
     ap.add_argument("--source", default="")
     a = ap.parse_args()
@@ -32,7 +33,8 @@ def main():
     dram = [per[i].get("dram__bytes_read.sum", 0) + per[i].get("dram__bytes_write.sum", 0) for i in ids]
     ns = [per[i]["gpu__time_duration.sum"] for i in ids]
     out = {"kernel": "k_engine_steps",
-           "config": {"workload": "cfg3_bookcorpus_1m", "instances_per_gpu": a.instances, "iters_per_step": a.iters},
+           "config": {"workload": "cfg3_bookcorpus_1m", "instances_per_gpu": a.instances, "iters_per_step": a.iters,
+                      "slice_us": a.slice_us},
            "dram_bytes_per_launch": sum(dram) / len(dram), "ncu_ns_per_launch": sum(ns) / len(ns),
            "launches": len(ids), "source": a.source or a.csv}
     json.dump(out, open(a.out, "w"), indent=1)
