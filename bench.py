@@ -315,6 +315,7 @@ def run_ours(args):
     b.sync()
     sc0 = b.scalars()
     d0 = b.debug().sum(axis=0)
+    t_warm_done = time.perf_counter()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -338,6 +339,7 @@ def run_ours(args):
     parts = b.partials()
     t_e2e = time.perf_counter() - t0
     e2e_parts = {"create_s": t_created - t0, "ingest_s": t_ingest, "steps_s": t_steps_done - t0 - t_create_ingest,
+                 "warmup_s": t_warm_done - t0 - t_create_ingest,
                  "partials_s": t_e2e - (t_steps_done - t0)}
     e2e_adm = sum(x.pt_dispatched - y.pt_dispatched for x, y in zip(sc1, sc_a))
     h2d = sum(t.nbytes for t in traces)
