@@ -577,6 +577,10 @@ def full_runs(args):
     SURVEY §6, and is not repeated here)."""
     from paper_2411_06364_b200.engine import Engine, generate_trace
     out = {}
+    # untimed warm-up of the single-engine path (first-use costs of its kernels
+    # and allocations after the big batch was released)
+    c0 = W.CONFIGS["cfg1_alpaca_10k"]
+    Engine(W.make_trace("cfg1_alpaca_10k", generate_trace, n=200), abi.default_options(**c0["opts"]), device=0).run()
     for name in ("cfg1_alpaca_10k", "cfg2_sharegpt_100k"):
         c = W.CONFIGS[name]
         t = W.make_trace(name, generate_trace)
