@@ -1,7 +1,9 @@
-"""Randomised configurations of the baseline policies (capacity, block size,
-tfs, chunk size, batch cap, recompute vs swap, swap stall, predictor), each
-run in lock-step against the compiled reference for up to 3,000 steps (vLLM
-recompute under a tight cache can livelock, in the reference too)."""
+"""Randomised configurations of every policy (capacity, block size, tfs,
+chunk size, batch cap, recompute vs swap, swap stall, reserve, buffer ratio,
+predictor), each run in lock-step against the compiled reference for up to
+3,000 steps (vLLM recompute under a tight cache can livelock, in the
+reference too); configurations the reference rejects must be rejected with
+the same message."""
 import numpy as np
 import pytest
 
@@ -16,9 +18,12 @@ from test_baselines import _engine, lockstep_or_same_error
 pytestmark = pytest.mark.skipif(not ref.available(), reason="oracle/_ref (compiled reference) not built")
 
 
-def fuzz_case(seed):
+ECONO = ["econoserve-d", "econoserve-sd", "econoserve-sdo", "econoserve-full"]
+
+
+def fuzz_case(seed, policies=BASELINES):
     rng = np.random.default_rng(seed)
-    pol = BASELINES[seed % len(BASELINES)]
+    pol = policies[seed % len(policies)]
     n = int(rng.integers(40, 220))
     plo, rlo = int(rng.integers(4, 32)), int(rng.integers(4, 32))
     tr = sat_trace(port.generate_trace, n, float(rng.choice([20.0, 80.0, 400.0])), plo, plo + int(rng.integers(8, 120)),
@@ -30,15 +35,16 @@ def fuzz_case(seed):
               chunk_size=int(rng.choice([16, 64, 256, 512])), batch_size_cap=int(rng.integers(1, 17)),
               vllm_recompute=int(rng.integers(0, 2)), swap_stall=float(rng.choice([0.0, 0.002])),
               pred_model=pm, pred_sigma=0.4, pred_accuracy=0.7, pred_tolerance=0.15,
-              pred_padding_ratio=float(rng.choice([0.0, 0.1, 0.3])), sched_cost_per_exam=float(rng.choice([0.0, 2e-5])))
+              pred_padding_ratio=float(rng.choice([0.0, 0.1, 0.3])), sched_cost_per_exam=float(rng.choice([0.0, 2e-5])),
+              reserved_fraction=float(rng.choice([0.05, 0.1, 0.2])), buffer_ratio=float(rng.choice([0.0, 0.1, 0.25])))
     return pol, tr, base_options(pol, **kw)
 
 
 SEEDS = list(range(120))
 
 
-def run_case(seed, backend):
-    pol, tr, o = fuzz_case(seed)
+def run_case(seed, backend, policies=BASELINES):
+    pol, tr, o = fuzz_case(seed, policies)
     try:
         ref.RefEngine(tr, o)
     except ref.EngineError as e:  # rejected at construction: the product must reject it the same way
@@ -58,3 +64,14 @@ def test_hostsim_fuzz(seed):
 @pytest.mark.parametrize("seed", SEEDS)
 def test_device_fuzz(seed):
     run_case(seed, "device")
+
+
+@pytest.mark.parametrize("seed", SEEDS)
+def test_hostsim_fuzz_econoserve(seed):
+    run_case(seed, "hostsim", ECONO)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", SEEDS)
+def test_device_fuzz_econoserve(seed):
+    run_case(seed, "device", ECONO)
