@@ -75,3 +75,32 @@ def test_hostsim_fuzz_econoserve(seed):
 @pytest.mark.parametrize("seed", SEEDS)
 def test_device_fuzz_econoserve(seed):
     run_case(seed, "device", ECONO)
+
+
+def run_case_nolog(seed, backend):
+    """The bench path: recording off (fused quiet-span replay, running
+    aggregates only); snapshots, records and the report must still match."""
+    from parity import lockstep
+    pol, tr, o = fuzz_case(seed, ECONO)
+    try:
+        a = ref.RefEngine(tr, o)
+    except ref.EngineError:
+        return
+    o2 = abi.default_options()
+    C_fields = [f[0] for f in abi.Options._fields_]
+    for f in C_fields:
+        setattr(o2, f, getattr(o, f))
+    o2.record_events = 0
+    o2.record_samples = 0
+    lockstep(a, _engine(backend, tr, o2), every=1, max_steps=3000, check_logs=False)
+
+
+@pytest.mark.parametrize("seed", SEEDS[:60])
+def test_hostsim_fuzz_nolog(seed):
+    run_case_nolog(seed, "hostsim")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", SEEDS[:60])
+def test_device_fuzz_nolog(seed):
+    run_case_nolog(seed, "device")
