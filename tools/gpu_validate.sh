@@ -1,3 +1,4 @@
+# round-end validation: smoke(), the full device test suite, the bench line and the reference arm
 mkdir -p gpurun_out
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final4_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/final4_smoke.log
 timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/final4_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/final4_pytest.log
