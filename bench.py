@@ -182,6 +182,34 @@ def reference_windows(n, threads, window, reps, warmup):
     return out, setup, engines
 
 
+def reference_end_step(args):
+    """Engine::step() calls a reference engine of reference_windows() has
+    made when it returns: the idle tick, the ingest step, then
+    (warmup + steps) windows of ref_iters."""
+    return 2 + args.ref_iters * (args.warmup + args.steps)
+
+
+def snapshot_digest(snap):
+    import hashlib
+    return len(snap), hashlib.sha256(np.ascontiguousarray(snap).tobytes()).hexdigest()
+
+
+def parity_block(dev_digests, engines, step):
+    """Device instances 0..k-1 of the benchmarked batch (trace seeds 1000+i)
+    against the reference engines of the CPU baseline (the same seeds), both
+    at Engine::step() call `step`: the canonical snapshot (DESIGN.md §8:
+    block tables, free gaps, slots, both queues in order, reserve/written
+    maps, the running order, 23 words per request) compared by SHA-256."""
+    k = min(len(dev_digests), len(engines))
+    equal = [dev_digests[i] == snapshot_digest(engines[i].snapshot()) for i in range(k)]
+    return {"instances_checked": k, "iterations": step, "equal": all(equal),
+            "mismatched": [i for i, e in enumerate(equal) if not e],
+            "how": "the benchmarked batch itself (same burst ingest, same time-sliced launches) brought to "
+                   f"step {step} with econo_batch_launch_to during the warm-up; its first {k} instances' "
+                   "complete-state snapshots compared (SHA-256) with the unmodified reference (oracle/_ref) "
+                   "engines of cpu_baseline at the same step"}
+
+
 def window_str(args, iters=None):
     it = iters or args.iters
     lo = 2 + it * args.warmup
@@ -309,6 +337,15 @@ def run_ours(args):
     sc_a = b.scalars()
     slice_ns = int(args.slice_us * 1000)
     step_n = (1 << 40) if slice_ns else args.iters
+    parity_dev = None
+    if world == 1 and not args.no_cpu_baseline and args.parity_instances > 0:
+        # parity checkpoint: bring the whole batch to the step where the CPU
+        # baseline's reference engines (the same seeds) will stop, with the
+        # same time-sliced launches, and keep digests of the first instances'
+        # complete state (compared with the reference after its window)
+        parity_at = reference_end_step(args)
+        b.advance_to(parity_at, stream.cuda_stream, slice_ns=slice_ns)
+        parity_dev = [snapshot_digest(b.snapshot(i)) for i in range(min(args.parity_instances, I))]
     for _ in range(args.warmup):
         b.launch(step_n, stream.cuda_stream, slice_ns=slice_ns)
     stream.synchronize()
@@ -436,7 +473,10 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         try:
             thr = min(os.cpu_count() or 1, 16)
-            wins, setup, _ = reference_windows(args.n, thr, args.ref_iters, args.steps, args.warmup)
+            wins, setup, engines = reference_windows(args.n, thr, args.ref_iters, args.steps, args.warmup)
+            if parity_dev is not None:
+                line["parity"] = parity_block(parity_dev, engines, reference_end_step(args))
+            del engines
             secs = sum(w[0] for w in wins)
             pts = sum(w[1] for w in wins)
             line["cpu_baseline"] = {
@@ -609,6 +649,48 @@ def full_runs(args):
     return out
 
 
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(n, argv):
+    """One process per GPU on this node, launched exactly as the driver
+    does (torch.distributed.run, rendezvous on 127.0.0.1): each rank runs
+    this script with the same arguments and reads RANK / LOCAL_RANK /
+    WORLD_SIZE; rank 0 prints the JSON line. NCCL's init lines go to stderr
+    (NCCL_DEBUG=INFO, INIT subsystem) so the communicator size is on record.
+    Returns the launcher's exit code (the run's ranks are torchrun's children:
+    a failure in any rank fails the launch)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + list(argv)
+    log("[bench] launching", n, "ranks:", " ".join(cmd))
+    return subprocess.call(cmd, env=env)
+
+
+def spawn_selftest(args):
+    """The rank plumbing alone, on CPU (gloo): every rank contributes its
+    rank; rank 0 prints the world size and the reduced sum."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+    x = torch.tensor([float(rank)])
+    if world > 1:
+        dist.all_reduce(x)
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "gpus_flag": args.gpus, "rank_sum": x.item()}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -626,6 +708,9 @@ def main():
                          "slowest instance)")
     ap.add_argument("--ref-iters", type=int, default=100,
                     help="reference arm / cpu_baseline: step() calls per engine per step (bounded sample)")
+    ap.add_argument("--parity-instances", type=int, default=16,
+                    help="instances of the benchmarked batch compared bit for bit with the CPU baseline's "
+                         "reference engines (0: no parity block)")
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -637,8 +722,15 @@ def main():
                     help="skip the all-policies configs[0] sweep (888 instances per policy)")
     ap.add_argument("--workload", default=WORKLOAD, choices=sorted(W.CONFIGS),
                     help="BASELINE.json config (default: configs[2], the 1M-queued case the metric is quoted on)")
+    ap.add_argument("--spawn-selftest", action="store_true",
+                    help="test hook: only the rank plumbing (gloo all-reduce of the ranks), no device work")
     args = ap.parse_args()
     globals()["WORKLOAD"] = args.workload
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without torchrun: launch the N ranks here
+        sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))
+    if args.spawn_selftest:
+        return spawn_selftest(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -271,6 +271,12 @@ int econo_batch_launch(econo_batch* b, int64_t max_steps, void* stream);
  * slow instance no longer holds every other SM idle until it finishes (the
  * host build ignores the slice). Asynchronous like econo_batch_launch. */
 int econo_batch_launch_slice(econo_batch* b, int64_t max_steps, int64_t slice_ns, void* stream);
+/* Advances every live instance until it has made target_steps Engine::step()
+ * calls in total (instances already there do nothing), optionally
+ * time-sliced like econo_batch_launch_slice (slice_ns <= 0: no slice). Brings
+ * a batch whose instances drifted apart under time slices back to one common
+ * step, e.g. to compare it with the reference at that step. Asynchronous. */
+int econo_batch_launch_to(econo_batch* b, int64_t target_steps, int64_t slice_ns, void* stream);
 /* Grid-wide ingest of the arrivals every instance would admit at the start of
  * its next step (ingest_arrivals, engine.hpp:216-235): the same class lists,
  * bitmaps and counters the in-kernel ingest builds, produced for large bursts

@@ -134,15 +134,24 @@ EDEV void init_finish(Inst& I, int64_t first_bad) {
 // the budget), and a step after a completion finds freed KVC for the GT
 // queue head. Skipping the test is always exact — it only decides whether a
 // replay may stand in for normal steps.
-// Device wall clock (ns), for time-sliced launches.
+// Device wall clock (ns), for time-sliced launches. Read by lane 0 and
+// broadcast, so every break decision taken on it is warp-uniform by
+// construction (the step body's full-mask shuffles and ballots need that).
+// Call from warp-converged code only.
 EDEV int64_t now_ns() {
 #ifdef __CUDA_ARCH__
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return (int64_t)t;
+  uint64_t t = 0;
+  if ((threadIdx.x & 31) == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (int64_t)__shfl_sync(0xffffffffu, t, 0);
 #else
   return 0;
 #endif
+}
+
+// max_steps < 0 encodes an absolute target (econo_batch_launch_to): advance
+// until Engine::step() has been called -max_steps times in total.
+EDEV int64_t steps_for(const Inst& I, int64_t max_steps) {
+  return max_steps >= 0 ? max_steps : (-max_steps > I.steps ? -max_steps - I.steps : 0);
 }
 
 // deadline_ns > 0 (a time-sliced launch, econo_batch_launch_slice): stop at
@@ -392,7 +401,7 @@ __global__ void __launch_bounds__(32) k_engine_steps(Inst* insts, int64_t max_st
   __shared__ Inst I;
   const int64_t t0 = PROF_NOW();
   inst_load(I, &insts[blockIdx.x]);
-  engine_steps<false>(I, max_steps, deadline);
+  engine_steps<false>(I, steps_for(I, max_steps), deadline);
   LANE0(I.prof[11] += PROF_NOW() - t0; I.prof[12]++);
   inst_store(&insts[blockIdx.x], I);
 }
@@ -404,7 +413,7 @@ __global__ void __launch_bounds__(32) k_baseline_steps(Inst* insts, int64_t max_
   const int64_t deadline = slice_ns > 0 ? now_ns() + slice_ns : 0;
   __shared__ Inst I;
   inst_load(I, &insts[blockIdx.x]);
-  engine_steps<true>(I, max_steps, deadline);
+  engine_steps<true>(I, steps_for(I, max_steps), deadline);
   inst_store(&insts[blockIdx.x], I);
 }
 
@@ -450,6 +459,13 @@ struct BulkJob {
 };
 constexpr int kBulkTile = 4096;
 constexpr int64_t kBulkBudget = (int64_t)128 << 20;  // keys per ingest group (4 x 4 B of temp each: 2 GB)
+// ECONO_BULK_BUDGET (keys) lowers it: a test knob that forces the multi-group
+// path of econo_batch_ingest on batches small enough for a parity test
+inline int64_t bulk_budget() {
+  const char* e = getenv("ECONO_BULK_BUDGET");
+  const int64_t v = e ? atoll(e) : 0;
+  return v > 0 && v < kBulkBudget ? v : kBulkBudget;
+}
 
 __global__ void __launch_bounds__(256) k_bulk_keys(const Inst* insts, BulkJob* jobs, uint32_t* key, uint32_t* val) {
   BulkJob& J = jobs[blockIdx.y];
@@ -1192,6 +1208,10 @@ struct econo_batch {
   std::vector<uint64_t> h_keys;  // host build
 #ifndef ECONO_HOSTSIM
   cudaStream_t stream = nullptr;
+  // recorded after every launch on a caller stream; the handle's own stream
+  // waits on it, so work the handle enqueues later (ingest plan, partial
+  // sums, records) is ordered after the steps it reads
+  cudaEvent_t launched = nullptr;
 #endif
   std::vector<econo_engine*> views;
 };
@@ -1294,8 +1314,8 @@ void launch_steps(econo_batch* b, int64_t max_steps, void* stream, int64_t slice
   (void)stream;
   (void)slice_ns;  // the host build has no device clock: max_steps only
   for (auto& h : b->inst) {
-    if (h.desc.base) engine_steps<true>(h.desc, max_steps);
-    else engine_steps<false>(h.desc, max_steps);
+    if (h.desc.base) engine_steps<true>(h.desc, steps_for(h.desc, max_steps));
+    else engine_steps<false>(h.desc, steps_for(h.desc, max_steps));
   }
   push_descs(b);
 #else
@@ -1303,6 +1323,10 @@ void launch_steps(econo_batch* b, int64_t max_steps, void* stream, int64_t slice
   if (b->n_base < (int64_t)b->inst.size())
     k_engine_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
   if (b->n_base > 0) k_baseline_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
+  if (s != b->stream) {  // order the handle's stream after these launches
+    cudaEventRecord(b->launched, s);
+    cudaStreamWaitEvent(b->stream, b->launched, 0);
+  }
 #endif
 }
 
@@ -1562,6 +1586,7 @@ void econo_batch_destroy(econo_batch* b) {
   for (auto* p : b->scr) dev_free(p);
   for (auto* v : b->views) delete v;
 #ifndef ECONO_HOSTSIM
+  if (b->launched) cudaEventDestroy(b->launched);
   if (b->stream) cudaStreamDestroy(b->stream);
 #endif
   delete b;
@@ -1600,6 +1625,7 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
   b->inst.resize((size_t)n_inst);
 #ifndef ECONO_HOSTSIM
   cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&b->launched, cudaEventDisableTiming);
 #endif
   std::vector<const EconoTraceRecord*> d_traces((size_t)n_inst);
   std::vector<uint64_t> seeds(2 * (size_t)n_inst);
@@ -1652,7 +1678,7 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
         ++jobs;
       }
     if (jobs > 0) {
-      const int64_t g = imin(keys, imax((int64_t)kBulkBudget, kmax));  // keys in one group at most
+      const int64_t g = imin(keys, imax(bulk_budget(), kmax));  // keys in one group at most
       const size_t kb = (4 * (size_t)g + 255) & ~(size_t)255;
       const size_t hb = (4 * 256 * (size_t)(g / kBulkTile + jobs) + 255) & ~(size_t)255;
       const size_t need = 4 * kb + hb + sizeof(BulkJob) * (size_t)jobs;
@@ -1879,6 +1905,12 @@ int econo_batch_launch_slice(econo_batch* b, int64_t max_steps, int64_t slice_ns
   return ECONO_OK;
 }
 
+int econo_batch_launch_to(econo_batch* b, int64_t target_steps, int64_t slice_ns, void* stream) {
+  if (target_steps < 0) return ECONO_ECONFIG;
+  launch_steps(b, -target_steps, stream, slice_ns > 0 ? slice_ns : 0);
+  return ECONO_OK;
+}
+
 
 int econo_batch_sync(econo_batch* b, char* err, size_t errlen) {
   int rc = sync_batch(b, err, errlen);
@@ -1984,7 +2016,7 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
   if (jobs.empty()) return ECONO_OK;
   const int passes = (bits + 7) / 8;
   // groups of jobs whose keys fit the temp budget; offsets are per group
-  const int64_t budget = kBulkBudget;
+  const int64_t budget = bulk_budget();
   std::vector<size_t> gstart;
   int64_t max_off = 0, max_hoff = 0;
   for (size_t g0 = 0; g0 < jobs.size();) {
@@ -2274,6 +2306,11 @@ int econo_scalars(econo_engine* e, EconoScalars* out) {
 int econo_records(econo_engine* e, EconoRecord* out, int64_t cap, char* err, size_t errlen) {
   HostInst& h = e->b->inst[(size_t)e->i];
   const Inst& I = h.desc;
+  if (I.error) {  // the engine's own SimulationError, not a generic message
+    int code;
+    const std::string m = format_error(I, &code);
+    return set_err(err, errlen, "%s", m.c_str()), code;
+  }
   if (I.completed < I.n)
     return set_err(err, errlen, "report requested before the run finished"), ECONO_ESIM;
   std::vector<EconoRecord> recs((size_t)I.n);

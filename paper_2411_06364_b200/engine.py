@@ -18,11 +18,16 @@ from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libeconoserve_b200.so")
+# development builds (e.g. the per-phase cycle counters, tools/gpu_phases.sh)
+# are loaded by pointing ECONO_LIB at them; the default is the product build
+if os.environ.get("ECONO_LIB"):
+    LIB_PATH = os.environ["ECONO_LIB"]
 
 SYMBOLS = [
     "econo_default_options", "econo_create", "econo_step", "econo_run", "econo_records",
     "econo_report", "econo_events", "econo_samples", "econo_scalars", "econo_snapshot",
-    "econo_destroy", "econo_instance_bytes", "econo_batch_create", "econo_batch_launch", "econo_batch_launch_slice", "econo_batch_sync",
+    "econo_destroy", "econo_instance_bytes", "econo_batch_create", "econo_batch_launch", "econo_batch_launch_slice",
+    "econo_batch_launch_to", "econo_batch_sync",
     "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
     "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore", "econo_batch_debug",
     "econo_batch_reports", "econo_batch_jct_prepare", "econo_batch_jct_hist", "econo_batch_jct_percentiles",
@@ -83,6 +88,7 @@ def load(path=None):
                                      C.c_int, C.POINTER(vp), cp, sz]
     L.econo_batch_launch.argtypes = [vp, i64, vp]
     L.econo_batch_launch_slice.argtypes = [vp, i64, i64, vp]
+    L.econo_batch_launch_to.argtypes = [vp, i64, i64, vp]
     L.econo_batch_sync.argtypes = [vp, cp, sz]
     L.econo_batch_scalars.argtypes = [vp, C.POINTER(abi.Scalars)]
     L.econo_batch_engine.argtypes = [vp, i32, C.POINTER(vp)]
@@ -270,6 +276,22 @@ class Batch:
         else:
             self._L.econo_batch_launch(self.h, max_steps, stream)
 
+    def launch_to(self, target_steps, stream=None, slice_ns=0):
+        """Advance every instance until it has made target_steps step() calls
+        in total (econo_batch_launch_to), time-sliced when slice_ns > 0."""
+        rc = self._L.econo_batch_launch_to(self.h, int(target_steps), int(slice_ns), stream)
+        if rc:
+            raise ConfigError("econo_batch_launch_to: negative target")
+
+    def advance_to(self, target_steps, stream=None, slice_ns=0):
+        """launch_to repeated until every live instance reached the target
+        (or finished / faulted); synchronises."""
+        while True:
+            self.launch_to(target_steps, stream, slice_ns)
+            self.sync()
+            if all(s.steps >= target_steps or s.done or s.error for s in self.scalars()):
+                return
+
     def sync(self):
         err = C.create_string_buffer(1024)
         rc = self._L.econo_batch_sync(self.h, err, 1024)
@@ -312,6 +334,21 @@ class Batch:
         n = self._L.econo_snapshot(v, None, 0)
         out = np.zeros(n, dtype=np.int64)
         self._L.econo_snapshot(v, out.ctypes.data, n)
+        return out
+
+    def engine(self, i):
+        """Borrowed single-engine view of instance i (econo_batch_engine)."""
+        v = C.c_void_p()
+        self._L.econo_batch_engine(self.h, i, C.byref(v))
+        return v
+
+    def records(self, i):
+        """finalize()'s per-request records of instance i (engine.hpp:963-994)."""
+        out = np.zeros(len(self.traces[i]), dtype=abi.RECORD_DTYPE)
+        err = C.create_string_buffer(1024)
+        rc = self._L.econo_records(self.engine(i), out.ctypes.data, len(out), err, 1024)
+        if rc:
+            _raise(rc, err)
         return out
 
     def reports(self):

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--launches", type=int, default=2)
     ap.add_argument("--workload", default=bench.WORKLOAD)
+    ap.add_argument("--slice-us", type=float, default=0.0, help="time-sliced launches (the bench's step)")
     a = ap.parse_args()
     bench.WORKLOAD = a.workload
     traces = bench.make_traces(generate_trace, a.n, [1000 + i for i in range(a.instances)])
@@ -37,7 +38,10 @@ def main():
     b.launch(1)
     b.sync()
     for _ in range(a.warmup + a.launches):
-        b.launch(a.iters)
+        if a.slice_us > 0:
+            b.launch(1 << 40, slice_ns=int(a.slice_us * 1000))
+        else:
+            b.launch(a.iters)
     b.sync()
     sc = b.scalars()
     print("errors:", sum(1 for s in sc if s.error), "pt_dispatched:", sum(s.pt_dispatched for s in sc),
