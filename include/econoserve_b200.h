@@ -325,6 +325,14 @@ int econo_batch_restore(econo_batch* b, char* err, size_t errlen);
 int econo_batch_debug(econo_batch* b, int64_t* out);
 void econo_batch_destroy(econo_batch* b);
 
+/* ---- glibc 2.39 exp/log as the device computes them ---------------------- */
+/* The lognormal predictor's exp and the polar method's log (workload.hpp:
+ * 233-235, random.tcc:1811-1844) run on the device as a port of glibc's own
+ * (x86-64 FMA variant), so predictions match the reference bit for bit.
+ * Evaluates fn (0 = exp, 1 = log) over n inputs on `device`, for checking the
+ * port against the host libm. */
+int econo_libm_eval(int32_t fn, const double* in, double* out, int64_t n, int device, char* err, size_t errlen);
+
 /* ---- host-side input preparation (out of the hot path) ------------------ */
 /* econosim::generate_synthetic (workload.hpp:104-125), bit-identical to the
  * reference generator (same libstdc++/glibc algorithms). */

@@ -29,6 +29,7 @@
 #include <stdint.h>
 
 #include "econoserve_b200.h"
+#include "glibc_libm.cuh"
 
 #ifdef __CUDACC__
 #define EDEV __device__ __forceinline__
@@ -408,7 +409,7 @@ EDEV double normal_fresh(uint64_t* x, int32_t& idx, double stddev) {
     b = 2.0 * canonical(x, idx) - 1.0;
     r2 = a * a + b * b;
   } while (r2 > 1.0 || r2 == 0.0);
-  const double mult = sqrt(-2 * log(r2) / r2);
+  const double mult = sqrt(-2 * econo_libm::log(r2) / r2);  // glibc's log, bit for bit
   double ret = b * mult;
   return ret * stddev + 0.0;
 }
@@ -417,7 +418,7 @@ EDEV Tok quantize_up(Tok v, Tok q) { return q <= 1 ? v : block_round(v, q); }
 EDEV Tok predict_rl(const Inst& I, Tok true_rl, uint64_t* x, int32_t& idx) {
   if (I.pred_model == ECONO_PRED_ORACLE) return quantize_up(true_rl, I.pred_quantum);
   if (I.pred_model == ECONO_PRED_LOGNORMAL) {
-    const double v = (double)true_rl * exp(normal_fresh(x, idx, I.pred_sigma));
+    const double v = (double)true_rl * econo_libm::exp(normal_fresh(x, idx, I.pred_sigma));  // glibc's exp
     return quantize_up(tmax(1, (Tok)llround(v)), I.pred_quantum);
   }
   const double t = (double)true_rl;

@@ -2674,3 +2674,33 @@ int econo_generate_trace(int64_t n, double rate, const EconoLengthDist* p, const
 }
 
 }  // extern "C"
+
+// ---- glibc exp/log port, evaluated on the device (glibc_libm.cuh) ---------
+#ifndef ECONO_HOSTSIM
+__global__ void k_libm_eval(int fn, const double* in, double* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = fn == 0 ? econo_libm::exp(in[i]) : econo_libm::log(in[i]);
+}
+#endif
+int econo_libm_eval(int32_t fn, const double* in, double* out, int64_t n, int device, char* err, size_t errlen) {
+  if (fn != 0 && fn != 1) return set_err(err, errlen, "fn must be 0 (exp) or 1 (log)"), ECONO_ECONFIG;
+#ifdef ECONO_HOSTSIM
+  (void)device;
+  for (int64_t i = 0; i < n; ++i) out[i] = fn == 0 ? econo_libm::exp(in[i]) : econo_libm::log(in[i]);
+  return ECONO_OK;
+#else
+  if (cudaSetDevice(device) != cudaSuccess) return set_err(err, errlen, "cudaSetDevice(%d) failed", device), ECONO_ECUDA;
+  void *din = nullptr, *dout = nullptr;
+  const size_t bytes = sizeof(double) * (size_t)(n > 0 ? n : 1);
+  int rc = ECONO_OK;
+  if (dev_alloc(&din, bytes) || dev_alloc(&dout, bytes) || dev_h2d(din, in, bytes)) rc = ECONO_ECUDA;
+  if (!rc) {
+    k_libm_eval<<<1184, 256>>>(fn, (const double*)din, (double*)dout, n);
+    if (cudaDeviceSynchronize() != cudaSuccess || dev_d2h(out, dout, bytes)) rc = ECONO_ECUDA;
+  }
+  dev_free(din);
+  dev_free(dout);
+  if (rc) set_err(err, errlen, "CUDA error: %s", cudaGetErrorString(cudaGetLastError()));
+  return rc;
+#endif
+}

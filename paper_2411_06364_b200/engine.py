@@ -31,7 +31,7 @@ SYMBOLS = [
     "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
     "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore", "econo_batch_debug",
     "econo_batch_reports", "econo_batch_jct_prepare", "econo_batch_jct_hist", "econo_batch_jct_percentiles",
-    "econo_jct_key_to_double", "econo_batch_ingest",
+    "econo_jct_key_to_double", "econo_batch_ingest", "econo_libm_eval",
 ]
 
 
@@ -89,6 +89,7 @@ def load(path=None):
     L.econo_batch_launch.argtypes = [vp, i64, vp]
     L.econo_batch_launch_slice.argtypes = [vp, i64, i64, vp]
     L.econo_batch_launch_to.argtypes = [vp, i64, i64, vp]
+    L.econo_libm_eval.argtypes = [i32, vp, vp, i64, C.c_int, cp, sz]
     L.econo_batch_sync.argtypes = [vp, cp, sz]
     L.econo_batch_scalars.argtypes = [vp, C.POINTER(abi.Scalars)]
     L.econo_batch_engine.argtypes = [vp, i32, C.POINTER(vp)]
