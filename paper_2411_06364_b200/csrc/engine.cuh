@@ -25,6 +25,7 @@
 //   HostingSlot vector (kvc.hpp:17-24) -> per-hosted-request slot fields +
 //       an insertion-ordered list of hosted ids.
 #pragma once
+#include <limits.h>
 #include <math.h>
 #include <stdint.h>
 
@@ -99,6 +100,18 @@ static inline uint64_t umulhi64(uint64_t a, uint64_t b) {
     if (LANE == 0) { stmt; } \
     WSYNC();        \
   } while (0)
+// A scalar update of warp-uniform state, executed by every lane on the same
+// values (each lane loads the same words and stores the same result), so the
+// warp never diverges around it: no BSSY/BSYNC pair, no branch, and no
+// instruction-fetch stall at the reconvergence point — on this latency-bound
+// path those stalls were the largest single cause (ncu: no_instructions, 38%
+// of samples, a third of them at BSYNC). Only for statements whose operands
+// are uniform and which contain no atomics or per-lane clocks; those keep
+// LANE0.
+#define UNI(stmt) \
+  do {            \
+    stmt;         \
+  } while (0)
 
 namespace econo {
 
@@ -170,6 +183,7 @@ struct Inst {
   int64_t err_val, ev_n, ev_cap, sm_n, sm_cap, ev_total;
   double wbuf[W];      // quiet-span replay: one chunk of per-step written fractions
   int64_t pt_min_lb;   // lower bound on the smallest queued prompt (only grows between arrivals)
+  int64_t ovf_id, ovf_dem;  // first request whose prediction saturated (kRlSat) at init, its exact demand
   int32_t bcnt[ECONO_MAX_BOUNDS + 2];  // queued PTs per deadline bucket (ordered mode)
   int64_t quiet_steps, quiet_spans, bcast;
   // device cycle counters (econo_batch_debug): [0] quiet-span tests [1] quiet
@@ -286,7 +300,7 @@ EDEV void arr_insert(T* a, int32_t n, int32_t pos, T v) {
     if (ok) a[i + 1] = x;
     WSYNC();
   }
-  LANE0(a[pos] = v);
+  UNI(a[pos] = v);
 }
 // Remove a[pos..pos+k) from an n-element array.
 template <class T>
@@ -322,8 +336,10 @@ EDEV int32_t arr_find(const int32_t* a, int32_t n, int32_t v) {
 // ------------------------------------------------------------------------
 // events / errors
 // ------------------------------------------------------------------------
+// Called warp-uniformly with uniform arguments; every lane performs the same
+// stores (see UNI), so the common no-recording case costs no divergence.
 EDEV void logev(Inst& I, int kind, int32_t id, int64_t a, int64_t b) {  // engine.hpp:211-214
-  if (LANE == 0) {
+  {
     I.ev_total++;
     if (I.record_events) {
       if (I.ev_n < I.ev_cap) {
@@ -414,12 +430,19 @@ EDEV double normal_fresh(uint64_t* x, int32_t& idx, double stddev) {
   return ret * stddev + 0.0;
 }
 EDEV Tok quantize_up(Tok v, Tok q) { return q <= 1 ? v : block_round(v, q); }
+// glibc's llround on x86-64: |v| >= 2^63 (or NaN) falls through to a plain
+// (long long) conversion, i.e. cvttsd2si's "integer indefinite" LLONG_MIN
+// (s_llround.c), where the device's conversion would saturate to LLONG_MAX.
+EDEV Tok llround_glibc(double v) {
+  if (!(v > -9223372036854775808.0 && v < 9223372036854775808.0)) return (Tok)LLONG_MIN;
+  return (Tok)llround(v);
+}
 // predict_rl (workload.hpp:228-264)
 EDEV Tok predict_rl(const Inst& I, Tok true_rl, uint64_t* x, int32_t& idx) {
   if (I.pred_model == ECONO_PRED_ORACLE) return quantize_up(true_rl, I.pred_quantum);
   if (I.pred_model == ECONO_PRED_LOGNORMAL) {
     const double v = (double)true_rl * econo_libm::exp(normal_fresh(x, idx, I.pred_sigma));  // glibc's exp
-    return quantize_up(tmax(1, (Tok)llround(v)), I.pred_quantum);
+    return quantize_up(tmax(1, llround_glibc(v)), I.pred_quantum);
   }
   const double t = (double)true_rl;
   const Tok lo_in = tmax(1, ceil_tokens(t * (1.0 - I.pred_tol)));
@@ -432,10 +455,10 @@ EDEV Tok predict_rl(const Inst& I, Tok true_rl, uint64_t* x, int32_t& idx) {
   const double u = canonical(x, idx) * (bb - a) + a;
   Tok v;
   if (canonical(x, idx) < 0.5) {
-    v = (Tok)llround(t * (1.0 + u));
+    v = llround_glibc(t * (1.0 + u));
     if (v <= hi_in) v = hi_in + 1;
   } else {
-    v = (Tok)llround(t * (1.0 - u));
+    v = llround_glibc(t * (1.0 - u));
     if (v >= lo_in) v = lo_in - 1;
     if (v < 1) v = hi_in + 1;
   }
@@ -444,7 +467,13 @@ EDEV Tok predict_rl(const Inst& I, Tok true_rl, uint64_t* x, int32_t& idx) {
 EHD Tok apply_padding(Tok p, double ratio) { return ceil_tokens((double)p * (1.0 + ratio)); }
 // padded_rl (engine.hpp:188, 921): always apply_padding(predicted_rl), so it
 // is recomputed instead of stored (4 bytes less per request).
-EHD int32_t padded_of(const Inst& I, int64_t id) { return (int32_t)apply_padding(I.predicted[id], I.pred_pad); }
+// Predicted and padded RLs are stored in 32 bits, saturated at kRlSat =
+// 2^30 tokens. Capacities are validated below 2^30, so a saturated request
+// can never be scheduled — exactly like the reference's unsaturated int64
+// value; init reports its exact int64 demand (Inst::ovf_*), never a wrapped one.
+static const int32_t kRlSat = 1 << 30;
+EHD int32_t sat_rl(Tok v) { return v >= (Tok)kRlSat ? kRlSat : (int32_t)v; }
+EHD int32_t padded_of(const Inst& I, int64_t id) { return sat_rl(apply_padding(I.predicted[id], I.pred_pad)); }
 // slo_deadline (engine.hpp:190-191), recomputed with the same operations
 // from the trace (8 bytes less per request).
 EHD double slo_of(const Inst& I, int64_t id) {
@@ -643,18 +672,18 @@ EDEV void addr_insert_region(Inst& I, int32_t r) {
   const int32_t pos = addr_lower(I, I.rg_start[r]);
   if (I.n_regions >= I.reg_cap) { set_error(I, ERR_TABLE_OVERFLOW, -1, 1); return; }
   arr_insert(I.addr, I.n_regions, pos, r);
-  LANE0(I.n_regions++);
+  UNI(I.n_regions++);
 }
 EDEV void addr_remove_region(Inst& I, int32_t r) {
   const int32_t pos = addr_lower(I, I.rg_start[r]);
   arr_erase(I.addr, I.n_regions, pos, 1);
-  LANE0(I.n_regions--);
+  UNI(I.n_regions--);
 }
 EDEV int32_t region_new(Inst& I, int32_t owner, Tok start, Tok len) {  // all lanes get the id
   if (I.reg_free_top <= 0) { set_error(I, ERR_TABLE_OVERFLOW, owner, 2); return -1; }
   const int32_t r = I.reg_free[I.reg_free_top - 1];
   WSYNC();
-  if (LANE == 0) {  // the owner's list fields are loaded before any store
+  {  // warp-uniform; the owner's list fields are loaded before any store
     const int32_t tail = I.reg_tail[owner], hd = I.held[owner];
     I.reg_free_top--;
     I.rg_start[r] = (int32_t)start;
@@ -765,18 +794,18 @@ EDEVNI bool kvc_alloc_region(Inst& I, int32_t id, Tok length) {
   if (r < 0) return false;
   if (I.n_regions >= I.reg_cap) { set_error(I, ERR_TABLE_OVERFLOW, id, 3); return false; }
   arr_insert(I.addr, I.n_regions, pos, r);
-  LANE0(I.n_regions++; I.free_total -= need);
+  UNI(I.n_regions++; I.free_total -= need);
   return true;
 }
 
 EDEV bool kvc_draw_reserved(Inst& I, int32_t id, Tok tokens) {  // kvc.hpp:144-150
   if (I.reserved_used + tokens > I.reserve_cap) return false;
-  LANE0(I.reserved_used += tokens; I.reserved[id] += (int32_t)tokens; I.flags[id] |= F_HAS_RESERVED);
+  UNI(I.reserved_used += tokens; I.reserved[id] += (int32_t)tokens; I.flags[id] |= F_HAS_RESERVED);
   return true;
 }
 EDEV void kvc_release_reserved(Inst& I, int32_t id) {  // kvc.hpp:152-159
   if (!(I.flags[id] & F_HAS_RESERVED)) return;
-  LANE0(I.reserved_used -= I.reserved[id]; I.reserved[id] = 0; I.flags[id] &= ~F_HAS_RESERVED);
+  UNI(I.reserved_used -= I.reserved[id]; I.reserved[id] = 0; I.flags[id] &= ~F_HAS_RESERVED);
 }
 EDEV void kvc_add_written(Inst& I, int32_t id, Tok d) {  // kvc.hpp:87-90 (lane 0 callers)
   I.written[id] += (int32_t)d;
@@ -806,9 +835,9 @@ EDEVNI void kvc_remove_slot(Inst& I, int32_t hosted) {
   WSYNC();
   if (mypos >= 0) {
     arr_erase(I.slots, I.n_slots, mypos, 1);
-    LANE0(I.n_slots--);
+    UNI(I.n_slots--);
   }
-  LANE0(I.flags[hosted] &= ~F_HAS_SLOT; I.sl_free[I.sl_free_top++] = op);
+  UNI(I.flags[hosted] &= ~F_HAS_SLOT; I.sl_free[I.sl_free_top++] = op);
 }
 
 // release (kvc.hpp:165-217)
@@ -840,11 +869,11 @@ EDEVNI void kvc_release(Inst& I, int32_t id) {
       const int32_t st = I.rg_start[r], ln = I.rg_len[r], nx = I.rg_next[r];
       const int32_t pos = addr_lower(I, st);
       arr_erase(I.addr, I.n_regions, pos, 1);
-      LANE0(I.n_regions--; I.reg_free[I.reg_free_top++] = r);
+      UNI(I.n_regions--; I.reg_free[I.reg_free_top++] = r);
       freed += ln;
       r = nx;
     }
-    LANE0(I.reg_head[id] = -1; I.reg_tail[id] = -1; I.held[id] = 0);
+    UNI(I.reg_head[id] = -1; I.reg_tail[id] = -1; I.held[id] = 0);
     for (int32_t k = 0; k < np; ++k) {
       const int32_t sp = I.tmp_c[k];
       const int32_t h = I.sl_hosted[sp], sl = I.sl_len[sp];
@@ -869,14 +898,14 @@ EDEVNI void kvc_release(Inst& I, int32_t id) {
         }
         w += POPC(m);
         WSYNC();
-        LANE0(I.sl_free_top += POPC(md));
+        UNI(I.sl_free_top += POPC(md));
       }
-      LANE0(I.n_slots = w);
+      UNI(I.n_slots = w);
     }
-    LANE0(I.free_total += freed);
+    UNI(I.free_total += freed);
   }
   // release_reserved (kvc.hpp:152-159) and the written count (kvc.hpp:92-101)
-  LANE0(if (f0 & F_HAS_RESERVED) { I.reserved_used -= rsv; I.reserved[id] = 0; }
+  UNI(if (f0 & F_HAS_RESERVED) { I.reserved_used -= rsv; I.reserved[id] = 0; }
         I.flags[id] = (uint8_t)(f0 & ~(F_HAS_RESERVED | F_HAS_SLOT));
         I.written_total -= wr; I.written[id] = 0);
 }
@@ -934,7 +963,7 @@ EDEV void gq_remove_at(Inst& I, int32_t pos) {  // drops the group from the queu
   const int32_t g = I.gq[pos];
   WSYNC();
   arr_erase(I.gq, I.G, pos, 1);
-  LANE0(I.G--; rl_set(I, I.gr_rl[g], -1); I.grp_free[I.grp_free_top++] = g);
+  UNI(I.G--; rl_set(I, I.gr_rl[g], -1); I.grp_free[I.grp_free_top++] = g);
 }
 EDEV Tok member_demand(const Inst& I, int32_t id) {  // gt_member_demand (engine.hpp:238-247)
   const Tok target = block_round((Tok)I.prompt[id] + I.generated[id] + padded_of(I, id), I.block);
@@ -946,41 +975,52 @@ EDEV Tok member_demand(const Inst& I, int32_t id) {  // gt_member_demand (engine
 // cached at join time and summed per group.
 EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline, int32_t occ, double now,
                             Tok d) {
-  LANE0(I.gt_next[id] = -1);
+  UNI(I.gt_next[id] = -1);
   if (I.grouping) {
     const int32_t g = rl_find(I, padded);
     if (g >= 0) {
-      const int32_t pos = gq_pos(I, g);
-      arr_erase(I.gq, I.G, pos, 1);
-      if (LANE == 0) {
-        const int32_t cnt = I.gr_cnt[g], tail = I.gr_tail[g], mo = I.gr_maxocc[g];
-        const int64_t gd = I.gr_dem[g];
-        const double md = I.gr_mindl[g];
-        I.G--;
+      // place() (queues.hpp:187-193) re-keys the group and re-inserts it at
+      // upper_bound: keys are unique (the group's original seq), so when the
+      // deadline and KVC buckets come out unchanged — always with ordering
+      // off, where the key is the seq alone — the group stays where it is
+      // and the queue is not touched.
+      const int32_t cnt = I.gr_cnt[g], tail = I.gr_tail[g], mo = I.gr_maxocc[g];
+      const int32_t odb = I.gr_db[g], okb = I.gr_kb[g];
+      const int64_t gd = I.gr_dem[g];
+      const double md = I.gr_mindl[g];
+      const double nmd = dmin(md, deadline);
+      const int32_t nmo = (int32_t)tmax(mo, occ);
+      const int32_t ndb = I.ordered ? bucket_d(I, dmax(0.0, nmd - now)) : odb;
+      const int32_t nkb = I.ordered ? bucket_k(I, nmo) : okb;
+      const bool moved = ndb != odb || nkb != okb;
+      if (moved) {  // the old key still locates the group
+        const int32_t pos = gq_pos(I, g);
+        arr_erase(I.gq, I.G, pos, 1);
+        UNI(I.G--);
+      }
+      {  // warp-uniform (every lane, same values)
         if (cnt == 0) { I.gr_head[g] = id; I.gr_hd[g] = (int32_t)d; } else { I.gt_next[tail] = id; }
         I.gr_tail[g] = id;
         I.gr_cnt[g] = cnt + 1;
         I.gr_dem[g] = gd + d;
-        const double nmd = dmin(md, deadline);
-        const int32_t nmo = (int32_t)tmax(mo, occ);
         I.gr_mindl[g] = nmd;
         I.gr_maxocc[g] = nmo;
-        if (I.ordered) {  // place(): make_key (queues.hpp:187-193)
-          I.gr_db[g] = bucket_d(I, dmax(0.0, nmd - now));
-          I.gr_kb[g] = bucket_k(I, nmo);
-        }
+        I.gr_db[g] = ndb;
+        I.gr_kb[g] = nkb;
       }
       WSYNC();
-      const int32_t p2 = gq_upper(I, g);
-      arr_insert(I.gq, I.G, p2, g);
-      LANE0(I.G++);
+      if (moved) {
+        const int32_t p2 = gq_upper(I, g);
+        arr_insert(I.gq, I.G, p2, g);
+        UNI(I.G++);
+      }
       return;
     }
   }
   if (I.grp_free_top <= 0 || I.G >= I.grp_cap) { set_error(I, ERR_TABLE_OVERFLOW, id, 4); return; }
   const int32_t g = I.grp_free[I.grp_free_top - 1];
   WSYNC();
-  LANE0(I.grp_free_top--;
+  UNI(I.grp_free_top--;
         I.gr_id[g] = I.next_group_id++; I.gr_rl[g] = padded; I.gr_head[g] = id; I.gr_tail[g] = id;
         I.gr_hd[g] = (int32_t)d;
         I.gr_cnt[g] = 1; I.gr_dem[g] = d; I.gr_formed[g] = now; I.gr_mindl[g] = deadline;
@@ -990,7 +1030,7 @@ EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline
         rl_set(I, padded, g));
   const int32_t p2 = gq_upper(I, g);
   arr_insert(I.gq, I.G, p2, g);
-  LANE0(I.G++);
+  UNI(I.G++);
 }
 EDEV void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline, int32_t occ, double now) {
   group_insert_gt(I, id, padded, deadline, occ, now, member_demand(I, id));
@@ -1057,14 +1097,14 @@ EDEVNI void ingest(Inst& I) {
     // sync-coupled: arrivals join the waiting groups (engine.hpp:226-228)
     for (int64_t id = first; id < last; ++id)
       group_insert_gt(I, (int32_t)id, padded_of(I, id), slo_of(I, id), 0, I.clock);
-    LANE0(I.arrival_cursor = last; I.ev_total += k; if (I.record_events) I.ev_n += k);
+    UNI(I.arrival_cursor = last; I.ev_total += k; if (I.record_events) I.ev_n += k);
     return;
   }
   if (!B) {
     int64_t pm = INT64_MAX;
     for (int64_t id = first + LANE; id < last; id += W) pm = I.prompt[id] < pm ? I.prompt[id] : pm;
     pm = wmin(pm);
-    LANE0(if (pm < I.pt_min_lb) I.pt_min_lb = pm);
+    UNI(if (pm < I.pt_min_lb) I.pt_min_lb = pm);
   }
   if (!B && I.ordered) {
     // class append in id order: peers of a class inside each warp chunk link
@@ -1108,14 +1148,14 @@ EDEVNI void ingest(Inst& I) {
     WSYNC();
     tree_fix(I, first, last - 1);
   }
-  LANE0(I.arrival_cursor = last; I.pt_count += (int32_t)k; I.ev_total += k;
+  UNI(I.arrival_cursor = last; I.pt_count += (int32_t)k; I.ev_total += k;
         if (I.record_events) I.ev_n += k);
 }
 
 // Takes up to k entries from the head of class (b,p); appends ids to out.
 EDEV int32_t cls_take(Inst& I, int b, int p, int32_t k, int32_t* out, int32_t nout) {
   const int32_t c = cls_of(I, b, p);
-  if (LANE == 0) {
+  {  // warp-uniform (every lane, same values)
     int32_t h = I.cls_head[c];
     for (int32_t i = 0; i < k; ++i) {
       out[nout + i] = h;
@@ -1182,7 +1222,7 @@ EDEVNI void dispatch_pts(Inst& I, int32_t npt) {
     const Tok took = shfl(incl, cnt > 0 ? cnt - 1 : 0);
     const int32_t bad_id = shfl(id, cnt < W ? cnt : 0);
     WSYNC();
-    LANE0(I.reserved_used = used0 + (cnt > 0 ? took : 0); I.n_ptiter += cnt; I.n_adm += cnt;
+    UNI(I.reserved_used = used0 + (cnt > 0 ? took : 0); I.n_ptiter += cnt; I.n_adm += cnt;
           I.pts_admitted_iter += cnt; I.pt_dispatched += cnt; I.ev_total += cnt;
           if (I.record_events) I.ev_n += cnt);
     if (bad) { set_error(I, ERR_RESERVED_DRAW, bad_id, 0); return; }
@@ -1202,7 +1242,7 @@ EDEVNI void schedule_gt_member(Inst& I, int32_t id) {
   else if (held < target) ok = kvc_alloc_region(I, id, target - held);
   if (I.error) return;
   if (!ok) { set_error(I, ERR_ALLOC_FAIL, id, 0); return; }
-  if (LANE == 0) {
+  {  // warp-uniform (every lane, same values)
     const uint8_t f = I.flags[id];
     const int32_t rsv = I.reserved[id], cur = I.written[id];
     const double le = I.last_enq[id], wt = I.waiting[id], pt = I.preempt_t[id];
@@ -1422,11 +1462,11 @@ EDEVNI int32_t select_gt(Inst& I, int32_t* nsel_out) {
       const int32_t g = I.gq[gi];
       const Tok total = I.gr_dem[g];  // the group's fields load together
       const int32_t cnt = I.gr_cnt[g], head = I.gr_head[g], grl = I.gr_rl[g];
-      LANE0(I.exam_count++);
+      UNI(I.exam_count++);
       if (nsel + cnt > I.sel_cap && total <= remaining) { set_error(I, ERR_TABLE_OVERFLOW, g, 8); return 0; }
       if (total <= remaining) {
         remaining -= total;
-        if (LANE == 0) {
+        {  // warp-uniform (every lane, same values)
           I.selg_start[nselg] = nsel;
           I.selg_rl[nselg] = grl;
           int32_t m = head;
@@ -1441,7 +1481,7 @@ EDEVNI int32_t select_gt(Inst& I, int32_t* nsel_out) {
       }
       int32_t taken = 0, m = head;
       Tok pd = 0, dm = 0;
-      if (LANE == 0) {
+      {  // warp-uniform (every lane, same values)
         Tok d = I.gr_hd[g];
         while (m >= 0) {
           const int32_t nx = I.gt_next[m];
@@ -1459,7 +1499,7 @@ EDEVNI int32_t select_gt(Inst& I, int32_t* nsel_out) {
       m = shfl(m, 0);
       pd = shfl(pd, 0);
       if (taken > 0) {
-        LANE0(I.selg_start[nselg] = nsel; I.selg_rl[nselg] = I.gr_rl[g];
+        UNI(I.selg_start[nselg] = nsel; I.selg_rl[nselg] = I.gr_rl[g];
               I.gr_head[g] = m; I.gr_hd[g] = (int32_t)dm; I.gr_cnt[g] -= taken; I.gr_dem[g] -= pd);
         nsel += taken;
         nselg++;
@@ -1473,14 +1513,14 @@ EDEVNI int32_t select_gt(Inst& I, int32_t* nsel_out) {
         rl_set(I, I.gr_rl[g], -1);
       }
       WSYNC();
-      if (LANE == 0)
+      /* warp-uniform */
         for (int32_t i = 0; i < whole; ++i) I.grp_free[I.grp_free_top++] = I.gq[i];
       WSYNC();
       arr_erase(I.gq, I.G, 0, whole);
-      LANE0(I.G -= whole);
+      UNI(I.G -= whole);
     }
   }
-  LANE0(I.selg_start[nselg] = nsel);
+  UNI(I.selg_start[nselg] = nsel);
   *nsel_out = nsel;
   return nselg;
 }
@@ -1502,7 +1542,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
   if (I.full && nselg > 0) {
     int32_t nm = 0;  // host members flattened into tmp_b/tmp_c, group bounds in tmp_a
     for (int32_t gi = 0; gi < nselg; ++gi) {
-      if (LANE == 0) {
+      {  // warp-uniform (every lane, same values)
         I.tmp_a[gi] = nm;
         for (int32_t i = I.selg_start[gi]; i < I.selg_start[gi + 1]; ++i) {
           const int32_t id = I.sel_ids[i];
@@ -1517,7 +1557,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
       nm = shfl(nm, 0);
       WSYNC();
     }
-    LANE0(I.tmp_a[nselg] = nm);
+    UNI(I.tmp_a[nselg] = nm);
     if (nm > 0 && I.G > 0) {
       int64_t exams = 0;
       int32_t nout = 0;
@@ -1526,13 +1566,13 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
         nout = plan_host_group(I, I.selg_rl[gi], hs, he, nout, &exams);
         if (I.error) return;
       }
-      LANE0(I.exam_count += exams);
+      UNI(I.exam_count += exams);
       for (int32_t i = 0; i < nout; ++i) {
         const int32_t host = I.os_host[i], hosted = I.os_hosted[i];
         const int32_t abs = I.os_abs[i], len = I.os_len[i];
         if (!slot_fits(I, host, abs, len)) { set_error(I, ERR_SLOT_OUTSIDE, hosted, 0); return; }
         if (I.n_slots >= I.slot_cap) { set_error(I, ERR_TABLE_OVERFLOW, hosted, 6); return; }
-        if (LANE == 0) {
+        {  // warp-uniform (every lane, same values)
           const int32_t sp = I.sl_free[--I.sl_free_top];
           I.sl_host[sp] = host;
           I.sl_off[sp] = I.os_off[i];
@@ -1568,11 +1608,11 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
       } else {
         adm = I.tree[I.tree_off[I.tree_levels - 1]] <= C0;
       }
-      if (!adm) LANE0(I.pt_min_lb = C0 + 1);
+      if (!adm) UNI(I.pt_min_lb = C0 + 1);
     }
-    if (adm) LANE0(I.pt_admittable = 1);
+    if (adm) UNI(I.pt_admittable = 1);
     if (tfs_rem > 0 && rfree > 0) {
-      LANE0(I.exam_count += I.pt_count);
+      UNI(I.exam_count += I.pt_count);
       Tok C = C0;  // both budgets drop by p: take iff p <= min(budgets)
       if (!adm) {
         // nothing fits (the admittable probe above used the same bound)
@@ -1596,7 +1636,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
         while (C > 0) {
           const int32_t id = tree_first(I, pos, C);
           if (id < 0) break;
-          LANE0(I.tmp_a[npt] = id; I.pt_count--);
+          UNI(I.tmp_a[npt] = id; I.pt_count--);
           npt++;
           C -= I.prompt[id];
           tree_set(I, id, INF32);
@@ -1613,7 +1653,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
       } else {
         const int32_t id = tree_first(I, 0, rfree);
         if (id >= 0) {
-          LANE0(I.tmp_a[0] = id; I.pt_count--);
+          UNI(I.tmp_a[0] = id; I.pt_count--);
           npt = 1;
           tree_set(I, id, INF32);
         }
@@ -1632,11 +1672,11 @@ EDEVNI void vacate_slot(Inst& I, int32_t id, bool* rehomed) {  // engine.hpp:888
   if (in_slot > 0 && kvc_draw_reserved(I, id, in_slot)) {
     rh = true;
   } else if (in_slot > 0) {
-    LANE0(const Tok w = I.written[id]; const Tok d = tmin(in_slot, w);
+    UNI(const Tok w = I.written[id]; const Tok d = tmin(in_slot, w);
           I.written[id] -= (int32_t)d; I.written_total -= d; I.occupied[id] -= (int32_t)in_slot);
   }
   kvc_remove_slot(I, id);
-  LANE0(I.flags[id] &= ~F_HOSTED);
+  UNI(I.flags[id] &= ~F_HOSTED);
   *rehomed = rh;
 }
 
@@ -1647,13 +1687,13 @@ EDEVNI void preempt_and_regroup(Inst& I, int32_t id, int why) {  // engine.hpp:9
     I.preempt_count[id]++;
     I.state[id] = ST_PREEMPTED;
     const Tok remaining = (Tok)I.true_rl[id] - I.generated[id];
-    I.predicted[id] = (int32_t)predict_rl(I, remaining, I.pmt, I.pmt_i);
+    I.predicted[id] = sat_rl(predict_rl(I, remaining, I.pmt, I.pmt_i));
     I.flags[id] |= F_WAS_PREEMPTED;
     I.last_enq[id] = I.clock;
   }
   WSYNC();
   logev(I, ECONO_EV_PREEMPT, id, why, padded_of(I, id));
-  LANE0(I.state[id] = ST_WAITING_GT);
+  UNI(I.state[id] = ST_WAITING_GT);
   if (B && I.policy != ECONO_POLICY_SYNC_COUPLED) {
     wait_insert(I, id);
     return;
@@ -1664,24 +1704,24 @@ EDEVNI void preempt_and_regroup(Inst& I, int32_t id, int why) {  // engine.hpp:9
 template <bool B>
 EDEVNI void handle_underprediction(Inst& I, int32_t id) {  // engine.hpp:856-873
   if (!B && kvc_draw_reserved(I, id, I.block)) {
-    LANE0(I.allowance[id] += (int32_t)I.block; I.reserve_draws[id]++;
+    UNI(I.allowance[id] += (int32_t)I.block; I.reserve_draws[id]++;
           I.penalty[id] += I.reserve_penalty);
     logev(I, ECONO_EV_RESERVE_TOPUP, id, 0, 0);
     WSYNC();
     return;
   }
-  LANE0(I.flags[id] |= F_ALLOC_FAIL; I.alloc_failures++);
+  UNI(I.flags[id] |= F_ALLOC_FAIL; I.alloc_failures++);
   bool rehomed = true;
   if (I.flags[id] & F_HOSTED) vacate_slot(I, id, &rehomed);
-  LANE0(I.penalty[id] += rehomed ? I.pen_free : I.pen_offload);
+  UNI(I.penalty[id] += rehomed ? I.pen_free : I.pen_offload);
   preempt_and_regroup<B>(I, id, 0);
 }
 
 EDEVNI void handle_hosted_overrun(Inst& I, int32_t id) {  // engine.hpp:875-884
-  LANE0(I.hosted_overruns++);
+  UNI(I.hosted_overruns++);
   bool rehomed = false;
   vacate_slot(I, id, &rehomed);
-  LANE0(I.penalty[id] += rehomed ? I.pen_free : I.pen_offload; I.flags[id] |= F_ALLOC_FAIL;
+  UNI(I.penalty[id] += rehomed ? I.pen_free : I.pen_offload; I.flags[id] |= F_ALLOC_FAIL;
         I.alloc_failures++);
   logev(I, ECONO_EV_HOSTED_OVERRUN, id, 0, 0);
   WSYNC();
@@ -1701,14 +1741,14 @@ EDEV void run_compact(Inst& I) {
     w += POPC(m);
     WSYNC();
   }
-  LANE0(I.R = w);
+  UNI(I.R = w);
 }
 
 template <bool B>
 EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   [[maybe_unused]] const int64_t tx0 = PHASE_NOW();
   const double dt = iteration_time(I, fs) + (B ? I.pending_stall : 0.0);
-  LANE0(I.clock += dt; I.iter++; if (B) I.pending_stall = 0.0);
+  UNI(I.clock += dt; I.iter++; if (B) I.pending_stall = 0.0);
   const bool pause = B && I.decode_pause;
   const double sched = (double)I.exam_count * I.sched_cost;
   if (I.n_adm > 0 && sched > 0.0) {
@@ -1733,7 +1773,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   }
   wsum_pt = wsum(wsum_pt);
   // every running GT writes exactly one token this iteration
-  LANE0(I.written_total += wsum_pt + (pause ? 0 : I.R));
+  UNI(I.written_total += wsum_pt + (pause ? 0 : I.R));
   EconoSample s;
   s.iter = I.iter;
   s.clock = I.clock;
@@ -1790,10 +1830,10 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
       const int l = FFS(m);
       m &= m - 1;
       const int32_t cid = shfl(id, l);
-      LANE0(I.state[cid] = ST_DONE; I.compl_clock[cid] = I.clock);
+      UNI(I.state[cid] = ST_DONE; I.compl_clock[cid] = I.clock);
       kvc_release(I, cid);
       if (I.error) return;
-      LANE0(I.occupied[cid] = 0; I.completed++);
+      UNI(I.occupied[cid] = 0; I.completed++);
       if (B) list_erase(I.admo, &I.n_admo, cid);
       logev(I, ECONO_EV_COMPLETE, cid, I.generated[cid], 0);
       WSYNC();
@@ -1813,16 +1853,16 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     const double slo = slo_of(I, id);
     if (!(f & F_PREFILL_FIN)) continue;
     WSYNC();
-    LANE0(I.flags[id] = (uint8_t)(f & ~F_PREFILL_FIN));
+    UNI(I.flags[id] = (uint8_t)(f & ~F_PREFILL_FIN));
     if (st != ST_RUNNING) continue;
     if constexpr (B) {  // baselines keep decoding (engine.hpp:805-808)
       list_erase(I.ongo, &I.n_ongo, id);
-      LANE0(I.gen_epoch[id] = gen; I.run[I.R++] = id);
+      UNI(I.gen_epoch[id] = gen; I.run[I.R++] = id);
       logev(I, ECONO_EV_PREFILL_DONE, id, 1, 0);
       WSYNC();
       continue;
     }
-    LANE0(I.state[id] = ST_WAITING_GT; I.last_enq[id] = I.clock);
+    UNI(I.state[id] = ST_WAITING_GT; I.last_enq[id] = I.clock);
     // gt_member_demand (engine.hpp:238-247) from the fields loaded above
     const Tok tgt = block_round((Tok)pr + gen + pad, I.block);
     const Tok dl = tgt - hd;
@@ -1871,7 +1911,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     if (I.error) return;
   }
   if (npre || ncs) run_compact(I);
-  if (LANE == 0) {
+  {  // warp-uniform (every lane, same values)
     s.completed = completed_now;
     if (I.record_samples) {
       if (I.sm_n < I.sm_cap) I.sm[I.sm_n] = s;
@@ -1894,7 +1934,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
       I.decode_pause = 0;
     }
 #ifdef ECONO_PROF_PHASES
-    I.prof[15] += PROF_NOW() - tx3;
+    if (LANE == 0) I.prof[15] += PROF_NOW() - tx3;
 #endif
   }
   WSYNC();
@@ -1903,7 +1943,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
 EDEVNI void handle_idle(Inst& I) {  // engine.hpp:930-961
   if (I.arrival_cursor < I.n) {
     const double next = I.arrival[I.arrival_cursor];
-    if (LANE == 0) {
+    {  // warp-uniform (every lane, same values)
       long long k = 1;
       if (next > I.clock) {
         const long long c = (long long)ceil((next - I.clock) / I.t_base);
@@ -1934,7 +1974,7 @@ EDEVNI void handle_idle(Inst& I) {  // engine.hpp:930-961
     }
     WSYNC();
     logev(I, ECONO_EV_IDLE, -1, I.err_val, 0);
-    LANE0(I.err_val = 0);
+    UNI(I.err_val = 0);
     return;
   }
   int32_t stuck = -1;  // first request not done (engine.hpp:951-960)
@@ -2001,7 +2041,7 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
       fit = I.tree[I.tree_off[I.tree_levels - 1]] <= C0;
     }
     if (fit) return 0;
-    LANE0(I.pt_min_lb = C0 + 1);
+    UNI(I.pt_min_lb = C0 + 1);
   }
   // first decode-side event: completion / under-prediction / slot deadline
   for (int32_t i = W + LANE; i < R; i += W) {
@@ -2095,7 +2135,7 @@ EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double c
     quiet_request(I, id, e2, k, clk1);
   }
   WSYNC();
-  LANE0(I.clock = clock; I.written_total = wt0 + k * fs; I.agg_written = aw; I.agg_allocated = aa;
+  UNI(I.clock = clock; I.written_total = wt0 + k * fs; I.agg_written = aw; I.agg_allocated = aa;
         I.iter += k; I.steps += k; I.executed += k; I.agg_fs += fs * k;
         if ((double)fs >= 0.95 * (double)I.tfs) I.agg_tfs_hits += k;
         I.hist[0] += k; I.quiet_steps += k; I.quiet_spans++);
@@ -2160,6 +2200,7 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
     }
   }
   WSYNC();
+  // lane 0 alone holds the recorded path's sums (aw, aa)
   LANE0(I.clock = clock; I.written_total = wt0 + k * fs; I.agg_written = aw; I.agg_allocated = aa);
   for (int32_t i = LANE; i < I.R; i += W) {
     const int32_t id = I.run[i];
@@ -2171,7 +2212,7 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
     I.occupied[id] += (int32_t)k;
     I.written[id] += (int32_t)k;
   }
-  LANE0(I.iter += k; I.steps += k; I.executed += k; I.agg_fs += fs * k;
+  UNI(I.iter += k; I.steps += k; I.executed += k; I.agg_fs += fs * k;
         if ((double)fs >= 0.95 * (double)I.tfs) I.agg_tfs_hits += k;
         I.hist[0] += k; if (I.record_samples) I.sm_n += k;
         I.quiet_steps += k; I.quiet_spans++);
@@ -2191,7 +2232,7 @@ EDEVNI void engine_step(Inst& I) {  // Engine::step (engine.hpp:104-116)
   fs = wsum(fs) + ((B && I.decode_pause) ? 0 : I.R);
   if (fs == 0) handle_idle(I); else execute_iteration<B>(I, fs);
   PHASE_ADD(10, PHASE_NOW() - t1);
-  LANE0(I.steps++);
+  UNI(I.steps++);
 }
 
 }  // namespace econo

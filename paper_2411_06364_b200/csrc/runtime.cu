@@ -68,7 +68,13 @@ EDEV void init_calibrate(Inst& I, int64_t prompt_sum) {
 EDEVNI void init_predict_sequential(Inst& I) {
   if (I.pred_model == ECONO_PRED_ORACLE) return;
   if (LANE == 0)
-    for (int32_t i = 0; i < I.n; ++i) I.predicted[i] = (int32_t)predict_rl(I, I.true_rl[i], I.pmt, I.pmt_i);
+    for (int32_t i = 0; i < I.n; ++i) {
+      const Tok p = predict_rl(I, I.true_rl[i], I.pmt, I.pmt_i);
+      I.predicted[i] = sat_rl(p);
+      const Tok pad = apply_padding(p, I.pred_pad);
+      if (I.ovf_id >= I.n && (p >= kRlSat || pad >= kRlSat))  // engine.hpp:196-202 with int64 lengths
+        I.ovf_id = i, I.ovf_dem = block_round((Tok)I.prompt[i] + tmax(I.true_rl[i], pad), I.block);
+    }
   WSYNC();
 }
 // Worst-case KVC demand of request i (engine.hpp:193-197): Orca reserves the
@@ -80,7 +86,7 @@ EDEV Tok worst_demand(const Inst& I, int64_t i) {
 }
 // Phase 3: per-request fields + feasibility (engine.hpp:186-206).
 EDEV bool init_req_one(Inst& I, int64_t i) {
-  if (I.pred_model == ECONO_PRED_ORACLE) I.predicted[i] = (int32_t)quantize_up(I.true_rl[i], I.pred_quantum);
+  if (I.pred_model == ECONO_PRED_ORACLE) I.predicted[i] = sat_rl(quantize_up(I.true_rl[i], I.pred_quantum));
   I.state[i] = ST_WAITING_PT;
   I.dispatch_t[i] = -1.0;
   I.first_tok[i] = -1.0;
@@ -116,7 +122,14 @@ EDEV int64_t init_table_extent(const Inst& I) {
 EDEV void init_finish(Inst& I, int64_t first_bad) {
   if (first_bad < I.n) {
     const int32_t bad = (int32_t)first_bad;
-    const Tok worst = worst_demand(I, bad);
+    Tok worst = worst_demand(I, bad);
+    if (I.policy != ECONO_POLICY_ORCA) {  // a saturated prediction: the exact int64 demand
+      if (I.pred_model == ECONO_PRED_ORACLE)
+        worst = block_round((Tok)I.prompt[bad] + tmax(I.true_rl[bad], apply_padding(quantize_up(I.true_rl[bad],
+                            I.pred_quantum), I.pred_pad)), I.block);
+      else if (bad == I.ovf_id)
+        worst = I.ovf_dem;
+    }
     I.error = worst > I.general_cap ? ERR_INFEASIBLE_KVC : ERR_INFEASIBLE_RESERVE;
     I.err_id = bad;
     I.err_val = worst > I.general_cap ? worst : I.reserve_cap;
@@ -1069,6 +1082,8 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   I.buffer_ratio = o->buffer_ratio;
   I.free_total = I.general_cap;
   I.pt_min_lb = INT64_MAX;
+  I.ovf_id = INT64_MAX;  // no saturated prediction
+  I.ovf_dem = 0;
   I.skip = (getenv("ECONO_NO_SKIP") || I.base) ? 0 : 1;
   // capacities
   // PT class tables span prompts 1..pmax. Ordered (econoserve) policies

@@ -273,3 +273,33 @@ def test_instance_bytes_sizing():
     o.tfs = 0
     with pytest.raises(ConfigError, match="tfs must be >= 1"):
         instance_bytes([(0.1, 10, 10)], o, lib=HOSTSIM)
+
+
+@pytest.mark.parametrize("backend", ["hostsim", pytest.param("device", marks=pytest.mark.gpu)])
+@pytest.mark.parametrize("sigma", [25.0, 60.0])
+def test_extreme_lognormal_predictions_match_reference(backend, sigma):
+    """Predictions far outside 32 bits: llround's x86 out-of-range value
+    (LLONG_MIN -> max(1, .) = 1, s_llround.c) and predicted RLs >= 2^30,
+    which the product saturates (engine.cuh kRlSat) and reports with the
+    reference's exact int64 demand (engine.hpp:196-202), or which leave the
+    run identical when no request is infeasible."""
+    from oracle import port
+    tr = sat_trace(gen, 300, 50.0, 8, 64, 8, 128, 71)
+    opts = base_options("econoserve-full", pred_model="lognormal", pred_sigma=sigma, kvc_capacity=4096)
+    try:
+        o = port.OracleEngine(tr, opts)
+        o.step(1 << 30)
+        want = ("ok", o.snapshot())
+    except Exception as ex:  # noqa: BLE001 — the reference's SimulationError
+        want = ("error", str(ex))
+    try:
+        e = make_engine(backend, tr, opts)
+        e.step(1 << 30)
+        got = ("ok", e.snapshot())
+    except Exception as ex:  # noqa: BLE001
+        got = ("error", str(ex))
+    assert got[0] == want[0], (got, want)
+    if want[0] == "ok":
+        assert np.array_equal(got[1], want[1])
+    else:
+        assert got[1] == want[1]

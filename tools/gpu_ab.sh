@@ -1,7 +1,3 @@
-# A/B of two builds of the product library on the same box (dev tool):
-# _lib/libeconoserve_b200_A.so vs _lib/libeconoserve_b200_B.so, alternating.
-for v in A B A B; do
-  cp paper_2411_06364_b200/_lib/libeconoserve_b200_$v.so paper_2411_06364_b200/_lib/libeconoserve_b200.so
-  echo "== $v" >> gpurun_out/ab.log
-  timeout 600 python tools/probe_scale.py --counts ${COUNTS:-888} --iters 1000 --lanes 0 2>&1 | grep "inst=" >> gpurun_out/ab.log
-done
+# A/B of library builds (tools/_prof/lib_<X>.so) on the bench step; LIBS overrides the list
+mkdir -p gpurun_out
+timeout 1500 python tools/ab_multi.py --libs ${LIBS:-base,uni} --rounds ${ROUNDS:-2} > gpurun_out/ab_${TAG:-x}.log 2>&1
