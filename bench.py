@@ -125,19 +125,50 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": "NVML, 1 ms polling over the timed steps"}
 
 
-def measured_traffic(instances, iters, slice_us=0):
-    """DRAM bytes per k_engine_steps launch from the committed ncu capture of
-    this exact configuration (profiles/r01_traffic.json), else None."""
-    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+def measured_traffic(instances, slice_us):
+    """ncu DRAM bytes and duration per k_engine_steps launch of this exact
+    configuration (profiles/r02_traffic.json, made by tools/make_traffic.py
+    from the committed launch list), else None."""
+    p = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
     c = d.get("config", {})
-    if c.get("instances_per_gpu") == instances and c.get("slice_us", 0) == slice_us and \
-            (slice_us or c.get("iters_per_step") == iters):
-        return d["dram_bytes_per_launch"]
+    if c.get("instances_per_gpu") == instances and c.get("slice_us") == slice_us and \
+            c.get("workload") == WORKLOAD:
+        return d
     return None
+
+
+def roofline_block(abytes, secs, launches, inst, slice_us, counts, dbg, peak, peak_kind):
+    """The dominant kernel's roofline: algorithmic bytes per launch (what the
+    executed work must touch, algorithmic_bytes) over the measured launch
+    time against the measured HBM copy bandwidth; the ncu DRAM bytes of the
+    same configuration beside it; and the latency view that actually bounds
+    a one-warp-per-instance dependency chain (cycles per event step)."""
+    achieved = abytes / secs / 1e9
+    tr = measured_traffic(inst, slice_us)
+    normal = max(1, counts["normal_steps"])
+    blk = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+           "traffic": tr["dram_bytes_per_launch"] if tr else None,
+           "per_launch_algorithmic_bytes": abytes / launches, "peak_kind": peak_kind, "kernel": "k_engine_steps",
+           "work_counts": counts,
+           "latency": {"normal_step_cycles": float(dbg[2]) / normal,
+                       "quiet_test_cycles": float(dbg[0]) / max(1, counts["spans"]),
+                       "replay_cycles_per_span": float(dbg[1]) / max(1, counts["spans"]),
+                       "l2_hit_latency_cycles": 262,
+                       "normal_step_in_l2_round_trips": float(dbg[2]) / normal / 262,
+                       "note": "one warp per instance runs a dependent chain; the bound is its latency, not "
+                               "HBM bandwidth (issue slots ~10% busy, ncu profiles/r02_*)"},
+           "note": "algorithmic bytes per executed unit (normal step, replayed span, admission, schedule, "
+                   "completion; DESIGN.md §5), not per simulated iteration: a replay keeps the span in "
+                   "registers"}
+    if tr:
+        blk["dram_achieved"] = tr["dram_bytes_per_launch"] / (tr["ncu_ns_per_launch"] * 1e-9) / 1e9
+        blk["dram_frac"] = blk["dram_achieved"] / peak
+        blk["traffic_source"] = tr.get("source")
+    return blk
 
 
 def measured_peaks():
@@ -257,18 +288,33 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------
-def algorithmic_bytes(sc_before, sc_after, iters, n_inst, total_iters=None):
-    """Minimal HBM bytes one step's scheduler iterations must touch with this
-    design: per executed iteration 48 B per running request
-    (generated/occupied/written r+w, exec_t r+w, true_rl, allowance, state)
-    + 64 B of queue/bitmap probes; per PT admission 40 B (class head/count,
-    next link, prompt, reserve draw, dispatch fields); per GT schedule 96 B
-    (allocation scan share, region record, address insert, request fields)."""
-    run = np.mean([s.running for s in sc_after])
-    pt = sum(a.pt_dispatched - b.pt_dispatched for a, b in zip(sc_after, sc_before))
-    gt = sum(a.gt_scheduled - b.gt_scheduled for a, b in zip(sc_after, sc_before))
-    it = total_iters if total_iters is not None else n_inst * iters
-    return it * (48.0 * run + 64.0) + 40.0 * pt + 96.0 * gt
+def algorithmic_bytes(counts):
+    """Minimal HBM bytes the design must move for the work a set of
+    k_engine_steps launches did — counted per EXECUTED unit,
+    not per simulated iteration: a quiet span replays its k iterations in
+    registers (quiet_steps_fused), so it touches each running request once.
+      per normal (event) step: 48 B per running request (generated, occupied,
+        written r+w, exec_t r+w, true_rl, allowance, state) + 64 B of queue /
+        bitmap / scalar probes;
+      per replayed span: the same 48 B per running request + 64 B;
+      per PT admission 40 B (class head/count, next link, prompt, reserve
+        draw, dispatch fields); per GT schedule 96 B (allocation scan share,
+        region record, address insert, request fields); per completion 64 B
+        (release, record fields).
+    `counts`: normal_steps, spans, mean_running, pt, gt, completed."""
+    c = counts
+    per_unit = 48.0 * c["mean_running"] + 64.0
+    return ((c["normal_steps"] + c["spans"]) * per_unit + 40.0 * c["pt"] + 96.0 * c["gt"] +
+            64.0 * c["completed"])
+
+
+def work_counts(sc_before, sc_after, dbg):
+    """The executed units of a window (device counters, econo_batch_debug)."""
+    return {"normal_steps": int(dbg[5]), "spans": int(dbg[4]),
+            "mean_running": float(np.mean([s.running for s in sc_after])),
+            "pt": int(sum(a.pt_dispatched - b.pt_dispatched for a, b in zip(sc_after, sc_before))),
+            "gt": int(sum(a.gt_scheduled - b.gt_scheduled for a, b in zip(sc_after, sc_before))),
+            "completed": int(sum(a.completed - b.completed for a, b in zip(sc_after, sc_before)))}
 
 
 def auto_instances(n, device, sms=148, world=1):
@@ -276,12 +322,12 @@ def auto_instances(n, device, sms=148, world=1):
     arena (econo_instance_bytes), plus the burst-ingest scratch (<= 2.2 GB).
     The end-of-run JCT keys (8 B per request) get a buffer only if HBM is
     left, else each histogram pass derives them from the request fields.
-    Sized on one configs[2] trace (the others differ by kilobytes)."""
+    Sized on the workload's own trace; at most 16 per SM (the registers of
+    16 one-warp CTAs fill an SM)."""
     import torch
 
     from paper_2411_06364_b200.engine import generate_trace, instance_bytes
-    c = W.CONFIGS[WORKLOAD]
-    t = generate_trace(n, c["rate"], c["shape"]["prompt"], c["shape"]["rl"], 1000)
+    t = W.make_trace(WORKLOAD, generate_trace, n=n, seed=1000)
     per = instance_bytes(t, options())
     free, _ = torch.cuda.mem_get_info(device)
     slack = (1 << 30) if world == 1 else (4 << 30)  # staging, scratch, context growth (+ NCCL's own)
@@ -410,7 +456,8 @@ def run_ours(args):
     tot = float(sum(times))
     it_done = sum(a.steps - z.steps for a, z in zip(sc1, sc0))  # scheduler iterations, all instances
     it_warm = sum(a.steps - z.steps for a, z in zip(sc0, sc_a))
-    abytes = algorithmic_bytes(sc0, sc1, 0, I, total_iters=it_done)
+    wcounts = work_counts(sc0, sc1, dbg)
+    abytes = algorithmic_bytes(wcounts)
     t = torch.tensor([tot, float(adm), float(gts), float(e2e_adm), t_e2e], dtype=torch.float64,
                      device=dev)
     # end-of-run report reduction (after the e2e window): exact global p5/p95
@@ -468,14 +515,8 @@ def run_ours(args):
         "ingest_s": t_ingest,
         "tracegen_s": t_gen,
         "gpu_launches": args.steps,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak,
-                     "traffic": measured_traffic(I, args.iters, args.slice_us if slice_ns else 0),
-                     "per_launch_algorithmic_bytes": abytes / args.steps, "peak_kind": peak_kind,
-                     "kernel": "k_engine_steps",
-                     "note": "latency-bound dependency chain (one warp per instance); algorithmic bytes = "
-                             "the state each simulated iteration updates (DESIGN.md §5); traffic = ncu DRAM "
-                             "bytes per launch of this config (profiles/r01_traffic.json): most of it hits L2"},
+        "roofline": roofline_block(abytes, tot, args.steps, I, args.slice_us if slice_ns else 0, wcounts, dbg, peak,
+                                   peak_kind),
         "clocks": clk,
         "e2e": {"value": e2e_adm_all / e2e_t, "unit": UNIT, "breakdown": e2e_parts, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
@@ -537,11 +578,13 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def other_workloads(args, stream, launches=4):
+def other_workloads(args, stream, launches=3, warm=2):
     """The same device-timed step on the other BASELINE.json shapes (north_star:
-    Alpaca-, ShareGPT- and BookCorpus-shaped traces): configs[1] (ShareGPT
-    100k, Poisson 28 rps, 888 instances) and configs[3] (the mixed 1M burst
-    with the lognormal predictor, 148 instances)."""
+    Alpaca-, ShareGPT- and BookCorpus-shaped traces), each sized to the GPU
+    like the headline (as many instances as HBM and the 16 resident warps per
+    SM allow): configs[1] (ShareGPT 100k, Poisson 28 rps: KVC pipelining
+    active) and configs[3] (the mixed 1M burst with the lognormal predictor:
+    preemptions, reserve top-ups, hosted slots). Time-sliced launches."""
     import torch
 
     from paper_2411_06364_b200.engine import Batch, generate_trace
@@ -549,35 +592,43 @@ def other_workloads(args, stream, launches=4):
     keep = WORKLOAD
     out = {}
     peak, _ = measured_peaks()
-    for name, inst, n in (("cfg2_sharegpt_100k", 888, 100_000), ("cfg4_mixed_1m", 148, 1_000_000)):
+    sl = int(args.slice_us * 1000)
+    for name in ("cfg2_sharegpt_100k", "cfg4_mixed_1m"):
         WORKLOAD = name
+        n = W.CONFIGS[name]["n"]
+        inst = auto_instances(n, 0)
         traces = make_traces(generate_trace, n, [1000 + i for i in range(inst)], pinned=True)
         b = Batch(traces, options(), device=0)
         b.launch(1, stream.cuda_stream)
         stream.synchronize()
         b.ingest()
-        for _ in range(1 + args.warmup):
-            b.launch(args.iters, stream.cuda_stream)
+        for _ in range(warm):
+            b.launch(1 << 40, stream.cuda_stream, slice_ns=sl)
         stream.synchronize()
         b.sync()
-        sc0 = b.scalars()
+        sc0, d0 = b.scalars(), b.debug().sum(axis=0)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(launches):
-            b.launch(args.iters, stream.cuda_stream)
+            b.launch(1 << 40, stream.cuda_stream, slice_ns=sl)
         e1.record(stream)
         e1.synchronize()
         secs = e0.elapsed_time(e1) / 1e3
         b.sync()
-        sc1 = b.scalars()
+        sc1, dbg = b.scalars(), b.debug().sum(axis=0) - d0
         adm = sum(x.pt_dispatched - y.pt_dispatched for x, y in zip(sc1, sc0))
-        ab = algorithmic_bytes(sc0, sc1, args.iters * launches, inst)
-        out[name] = {"instances": inst, "requests_per_instance": n, "iters_per_step": args.iters, "steps": launches,
-                     "value": adm / secs, "unit": UNIT, "us_per_iter": 1e6 * secs / (args.iters * launches),
-                     "quiet_step_frac": (sum(x.quiet_steps - y.quiet_steps for x, y in zip(sc1, sc0)) /
-                                         max(1, sum(x.steps - y.steps for x, y in zip(sc1, sc0)))),
+        its = sum(x.steps - y.steps for x, y in zip(sc1, sc0))
+        wc = work_counts(sc0, sc1, dbg)
+        ab = algorithmic_bytes(wc)
+        out[name] = {"instances": inst, "requests_per_instance": n, "steps": launches,
+                     "launch": f"time-sliced, {args.slice_us:g} us", "value": adm / secs, "unit": UNIT,
+                     "us_per_iter": 1e6 * secs / (its / inst),
+                     "quiet_step_frac": (sum(x.quiet_steps - y.quiet_steps for x, y in zip(sc1, sc0)) / max(1, its)),
+                     "hosted_slots_created": int(sum(x.hosted_slots_created - y.hosted_slots_created
+                                                     for x, y in zip(sc1, sc0))),
+                     "normal_step_cycles": float(dbg[2]) / max(1, dbg[5]),
                      "roofline": {"achieved": ab / secs / 1e9, "peak": peak, "unit": "GB/s",
-                                  "frac": ab / secs / 1e9 / peak},
+                                  "frac": ab / secs / 1e9 / peak, "work_counts": wc},
                      "errors": sum(1 for x in sc1 if x.error)}
         b.close()
         del traces
@@ -737,7 +788,7 @@ def main():
                          "requests, so 8 per SM = 1184 on a B200)")
     ap.add_argument("--iters", type=int, default=1000,
                     help="scheduler iterations per instance per step (one k_engine_steps launch)")
-    ap.add_argument("--slice-us", type=float, default=250.0,
+    ap.add_argument("--slice-us", type=float, default=20000.0,
                     help="time-sliced steps: each launch runs every instance until this much device time has "
                          "passed (0 = a fixed --iters iterations per instance, every launch waiting for its "
                          "slowest instance)")

@@ -1,7 +1,7 @@
-"""profiles/r01_traffic.json from an ncu launch list of the bench (dev tool):
+"""profiles/r02_traffic.json from an ncu launch list of the bench (dev tool):
 averages DRAM bytes and duration over the last `--launches` k_engine_steps
 launches (the timed ones). Usage:
-  python tools/make_traffic.py gpurun_out/final_launches.csv --instances 1184 --iters 1000"""
+  python tools/make_traffic.py gpurun_out/r2_launches.csv --instances 1184 --slice-us 20000"""
 import argparse
 import csv
 import json
@@ -15,7 +15,7 @@ def main():
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--launches", type=int, default=10)
     ap.add_argument("--slice-us", type=float, default=0)
-    ap.add_argument("--out", default="profiles/r01_traffic.json")
+    ap.add_argument("--out", default="profiles/r02_traffic.json")
     ap.add_argument("--source", default="")
     a = ap.parse_args()
     rows = list(csv.reader(open(a.csv)))
@@ -33,8 +33,7 @@ def main():
     dram = [per[i].get("dram__bytes_read.sum", 0) + per[i].get("dram__bytes_write.sum", 0) for i in ids]
     ns = [per[i]["gpu__time_duration.sum"] for i in ids]
     out = {"kernel": "k_engine_steps",
-           "config": {"workload": "cfg3_bookcorpus_1m", "instances_per_gpu": a.instances, "iters_per_step": a.iters,
-                      "slice_us": a.slice_us},
+           "config": {"workload": "cfg3_bookcorpus_1m", "instances_per_gpu": a.instances, "slice_us": a.slice_us},
            "dram_bytes_per_launch": sum(dram) / len(dram), "ncu_ns_per_launch": sum(ns) / len(ns),
            "launches": len(ids), "source": a.source or a.csv}
     json.dump(out, open(a.out, "w"), indent=1)
