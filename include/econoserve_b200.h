@@ -199,7 +199,8 @@ typedef struct EconoReport {
   int64_t preemptions, reserve_draws, hosted_slots, hosted_overruns;
   double mean_waiting, mean_execution, mean_preemption, mean_scheduling;
   uint64_t trace_hash;
-  int32_t n_hist;           /* entries in the completion histogram (<= ECONO_MAX_HIST) */
+  int32_t n_hist;           /* entries in the completion histogram (<= ECONO_MAX_HIST; a report that would
+                               need more fails with ECONO_ESIM instead of truncating) */
   int32_t _pad;
   int32_t hist_count[ECONO_MAX_HIST]; /* sorted ascending, like std::map<int,double> */
   double hist_frac[ECONO_MAX_HIST];

@@ -17,8 +17,8 @@
 //   IterationSample / RequestRecord / MetricsReport   metrics.hpp:17-76
 //   Engine::step/run/report/events/samples/clock/...  engine.hpp:79-145
 //   ConfigError / SimulationError    common.hpp:17-24
-// Only the econoserve-{d,sd,sdo,full} policies run here (the baselines are
-// outside this path); other kinds throw ConfigError.
+// Every policy kind runs on the device: the econoserve-{d,sd,sdo,full} family
+// and the five comparison baselines (k_baseline_steps).
 #pragma once
 
 #include <cstdint>

@@ -38,6 +38,10 @@
 // separate device functions (no call/stack traffic, scheduling across calls).
 #define EDEVNI __device__ __forceinline__
 #define EHD __host__ __device__ __forceinline__
+// Rare paths (compaction, the pipelining planner, preemption, overruns,
+// idle stretches) are kept out of line so the event-step code the warps
+// actually run stays dense in the instruction cache.
+#define ECOLD __device__ __noinline__
 #define W 32
 #define LANE ((int)(threadIdx.x & 31))
 #define WSYNC() __syncwarp()
@@ -62,6 +66,7 @@ EHD uint64_t umulhi64(uint64_t a, uint64_t b) {
 #define EDEV static inline
 #define EDEVNI static
 #define EHD static inline
+#define ECOLD static
 #define W 1
 #define LANE 0
 #define WSYNC() ((void)0)
@@ -710,7 +715,7 @@ EDEV bool owner_or_slot_host(const Inst& I, int32_t h, int32_t owner) {
 }
 
 // compact() (kvc.hpp:372-401): slide every region down in address order.
-EDEVNI void kvc_compact(Inst& I) {
+ECOLD void kvc_compact(Inst& I) {
   const int32_t L = I.n_regions;
   int32_t* ns = I.tmp_a;  // new start per address position
   int32_t carry = 0;
@@ -1272,7 +1277,7 @@ EDEVNI void schedule_gt_member(Inst& I, int32_t id) {
 // plan_pipeline (kvc_pipeline.hpp:29-136). Host group h's members are
 // I.tmp_b[hs..he) (ids) with write bases I.tmp_c[hs..he). Appends planned
 // slots to the os_* arrays; returns the new count.
-EDEVNI int32_t plan_host_group(Inst& I, int32_t l, int32_t hs, int32_t he, int32_t nout, int64_t* exams) {
+ECOLD int32_t plan_host_group(Inst& I, int32_t l, int32_t hs, int32_t he, int32_t nout, int64_t* exams) {
   if (l < 2 || he <= hs) return nout;
   const Tok b = ceil_tokens(I.buffer_ratio * (double)l);
   int32_t nr = he - hs;
@@ -1666,7 +1671,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
 
 #include "baselines.cuh"
 
-EDEVNI void vacate_slot(Inst& I, int32_t id, bool* rehomed) {  // engine.hpp:888-902
+ECOLD void vacate_slot(Inst& I, int32_t id, bool* rehomed) {  // engine.hpp:888-902
   const Tok in_slot = tmin((Tok)I.generated[id] - I.gen_epoch[id], (Tok)padded_of(I, id));
   bool rh = false;
   if (in_slot > 0 && kvc_draw_reserved(I, id, in_slot)) {
@@ -1681,7 +1686,7 @@ EDEVNI void vacate_slot(Inst& I, int32_t id, bool* rehomed) {  // engine.hpp:888
 }
 
 template <bool B>
-EDEVNI void preempt_and_regroup(Inst& I, int32_t id, int why) {  // engine.hpp:904-928
+ECOLD void preempt_and_regroup(Inst& I, int32_t id, int why) {  // engine.hpp:904-928
   if (B) list_erase(I.admo, &I.n_admo, id);
   if (LANE == 0) {
     I.preempt_count[id]++;
@@ -1702,7 +1707,7 @@ EDEVNI void preempt_and_regroup(Inst& I, int32_t id, int why) {  // engine.hpp:9
 }
 
 template <bool B>
-EDEVNI void handle_underprediction(Inst& I, int32_t id) {  // engine.hpp:856-873
+ECOLD void handle_underprediction(Inst& I, int32_t id) {  // engine.hpp:856-873
   if (!B && kvc_draw_reserved(I, id, I.block)) {
     UNI(I.allowance[id] += (int32_t)I.block; I.reserve_draws[id]++;
           I.penalty[id] += I.reserve_penalty);
@@ -1717,7 +1722,7 @@ EDEVNI void handle_underprediction(Inst& I, int32_t id) {  // engine.hpp:856-873
   preempt_and_regroup<B>(I, id, 0);
 }
 
-EDEVNI void handle_hosted_overrun(Inst& I, int32_t id) {  // engine.hpp:875-884
+ECOLD void handle_hosted_overrun(Inst& I, int32_t id) {  // engine.hpp:875-884
   UNI(I.hosted_overruns++);
   bool rehomed = false;
   vacate_slot(I, id, &rehomed);
@@ -1940,7 +1945,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   WSYNC();
 }
 
-EDEVNI void handle_idle(Inst& I) {  // engine.hpp:930-961
+ECOLD void handle_idle(Inst& I) {  // engine.hpp:930-961
   if (I.arrival_cursor < I.n) {
     const double next = I.arrival[I.arrival_cursor];
     {  // warp-uniform (every lane, same values)

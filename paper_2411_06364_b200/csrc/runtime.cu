@@ -704,6 +704,230 @@ __global__ void __launch_bounds__(256) k_bulk_tails(Inst* insts, const BulkJob* 
     if (in && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&I.cls_cnt[c], (int32_t)__popc(peers));
   }
 }
+// ---------------------------------------------------------------------------
+// Burst ingest without a global sort (the default path): the class lists only
+// need, for every arrival, the next arrival of the same class in id order.
+//  k_ingest_tiles: per 4096-id tile, a stable two-pass radix sort of
+//    (class, local index) in shared memory gives the in-tile successors,
+//    written to pt_next in id order (coalesced), and one segment record per
+//    class present in the tile (class, first, last, count: 8 bytes);
+//  k_ingest_stitch: one CTA per instance walks its tiles from the last to the
+//    first with a per-class table in shared memory (classes are distinct
+//    within a tile, so a tile's segments are stitched in parallel), links each
+//    segment's last id to the next tile's first of the class, then splices
+//    every class onto its list (queues.hpp:85-92 order: id ascending within a
+//    class) and updates counts, bitmaps and the ingest scalars.
+// HBM traffic per arrival: 16 B read (arrival, true_rl, prompt) + 4 B written
+// (pt_next) + the segments (<= 8 B, ~2 B at cfg3's class spread), against
+// ~94 B for sort + scatter + splice.
+// ---------------------------------------------------------------------------
+constexpr int kTileI = 4096;
+EDEV uint64_t seg_pack(uint32_t c, uint32_t f, uint32_t l, uint32_t n) {
+  return ((uint64_t)c << 37) | ((uint64_t)f << 25) | ((uint64_t)l << 13) | (uint64_t)n;
+}
+
+// One stable pass of the tile by the 8-bit digit at `shift` (warp-ordered
+// match_any ranks, exactly as k_radix_scatter's in-tile reorder).
+EDEV void tile_radix_pass(const uint32_t* in, uint32_t* out, uint32_t (*cnt)[256], uint32_t* tstart, int shift) {
+  constexpr int PER = kTileI / 256;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int d = threadIdx.x; d < 8 * 256; d += blockDim.x) (&cnt[0][0])[d] = 0;
+  uint32_t kr[PER], rank[PER];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    kr[r] = in[w * (kTileI / 8) + r * 32 + lane];
+    const int d = (int)((kr[r] >> shift) & 255);
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t base = cnt[w][d];
+    __syncwarp();
+    if ((peers & ((1u << lane) - 1u)) == 0) cnt[w][d] = base + __popc(peers);
+    __syncwarp();
+    rank[r] = base + __popc(peers & ((1u << lane) - 1u));
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;
+    uint32_t run = 0;
+    for (int ww = 0; ww < 8; ++ww) {
+      const uint32_t c = cnt[ww][d];
+      cnt[ww][d] = run;
+      run += c;
+    }
+    tstart[d] = run;
+  }
+  __syncthreads();
+  {
+    const uint32_t v = tstart[threadIdx.x];
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    __shared__ uint32_t ws[8];
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int ww = 0; ww < w; ++ww) pre += ws[ww];
+    __syncthreads();
+    tstart[threadIdx.x] = pre + x - v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const int d = (int)((kr[r] >> shift) & 255);
+    out[tstart[d] + cnt[w][d] + rank[r]] = kr[r];
+  }
+  __syncthreads();
+}
+
+// J.off: the job's first tile * kTileI in `segs`; J.hoff: its first tile in `nseg`.
+__global__ void __launch_bounds__(256) k_ingest_tiles(Inst* insts, BulkJob* jobs, uint64_t* segs, int32_t* nseg) {
+  BulkJob& J = jobs[blockIdx.y];
+  if ((int)blockIdx.x >= J.tiles) return;
+  Inst& I = insts[J.inst];
+  __shared__ uint32_t ka[kTileI], kb[kTileI];
+  __shared__ uint32_t cnt[8][256];
+  __shared__ uint32_t tstart[256];
+  __shared__ unsigned long long sb[ECONO_MAX_BOUNDS + 2];
+  __shared__ unsigned long long smin;
+  __shared__ uint32_t wsum[8];
+  if (threadIdx.x < ECONO_MAX_BOUNDS + 2) sb[threadIdx.x] = 0;
+  if (threadIdx.x == 0) smin = ~0ULL;
+  __syncthreads();
+  const int64_t t0 = (int64_t)blockIdx.x * kTileI;
+  const int n = (int)(J.k - t0 < kTileI ? J.k - t0 : kTileI);
+  const double now = I.clock;
+  const uint32_t pm1 = (uint32_t)I.pmax + 1;
+  unsigned long long mn = ~0ULL;
+  uint32_t bc[ECONO_MAX_BOUNDS + 2];
+#pragma unroll
+  for (int bb = 0; bb < ECONO_MAX_BOUNDS + 2; ++bb) bc[bb] = 0;
+  for (int e = threadIdx.x; e < kTileI; e += blockDim.x) {
+    uint32_t key = 0xFFFFFFFFu;  // padding sorts after every class (< 2^16)
+    if (e < n) {
+      const int64_t id = J.first + t0 + e;
+      const int b = bucket_d(I, dmax(0.0, slo_of(I, id) - now));
+      const int32_t p = I.prompt[id];
+      key = (((uint32_t)b * pm1 + (uint32_t)p) << 12) | (uint32_t)e;
+      mn = (unsigned long long)p < mn ? (unsigned long long)p : mn;
+#pragma unroll
+      for (int bb = 0; bb < ECONO_MAX_BOUNDS + 2; ++bb) bc[bb] += b == bb;
+    }
+    ka[e] = key;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, mn, o);
+    mn = x < mn ? x : mn;
+  }
+#pragma unroll
+  for (int bb = 0; bb < ECONO_MAX_BOUNDS + 2; ++bb) {
+    uint32_t c = bc[bb];
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&sb[bb], (unsigned long long)c);
+  }
+  if ((threadIdx.x & 31) == 0) atomicMin(&smin, mn);
+  tile_radix_pass(ka, kb, cnt, tstart, 12);  // class bits 0..7
+  tile_radix_pass(kb, ka, cnt, tstart, 20);  // class bits 8..15
+  // sorted by (class, local index): successors, segment starts
+  constexpr int PER = kTileI / 256;
+  const int j0 = threadIdx.x * PER;
+  uint32_t starts = 0;
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const int j = j0 + r;
+    if (j < n) {
+      const uint32_t k = ka[j], c = k >> 12;
+      const bool last = j + 1 >= n || (ka[j + 1] >> 12) != c;
+      // scattered within the tile's 16 KB of pt_next: merged in L2 before DRAM
+      I.pt_next[J.first + t0 + (k & 4095)] = last ? -1 : (int32_t)(J.first + t0 + (ka[j + 1] & 4095));
+      if (j == 0 || (ka[j - 1] >> 12) != c) starts |= 1u << r;
+    }
+  }
+  // exclusive prefix of segment starts over the tile (thread order = sorted order)
+  const uint32_t mine = __popc(starts);
+  uint32_t x = mine;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  uint32_t pre = 0, total = 0;
+  for (int ww = 0; ww < 8; ++ww) {
+    if (ww < w) pre += wsum[ww];
+    total += wsum[ww];
+  }
+  uint32_t s = pre + x - mine;
+  // compacted segment starts (kb is free after the second pass), then one
+  // record per segment: its end is the position before the next start
+#pragma unroll
+  for (int r = 0; r < PER; ++r)
+    if (starts & (1u << r)) kb[s++] = (uint32_t)(j0 + r);
+  __syncthreads();
+  for (uint32_t q = threadIdx.x; q < total; q += blockDim.x) {
+    const uint32_t j = kb[q], e = (q + 1 < total ? kb[q + 1] : (uint32_t)n) - 1;
+    segs[J.off + t0 + q] = seg_pack(ka[j] >> 12, ka[j] & 4095, ka[e] & 4095, e - j + 1);
+  }
+  if (threadIdx.x == 0) {
+    nseg[J.hoff + blockIdx.x] = (int32_t)total;
+    atomicMin(&J.minp, smin);
+  }
+  if (threadIdx.x < ECONO_MAX_BOUNDS + 2 && sb[threadIdx.x]) atomicAdd(&J.bcnt[threadIdx.x], sb[threadIdx.x]);
+}
+
+// One CTA per job; dynamic shared memory: 3 x ncls int32 (+ bucket sums).
+__global__ void __launch_bounds__(512) k_ingest_stitch(Inst* insts, const BulkJob* jobs, const uint64_t* segs,
+                                                       const int32_t* nseg) {
+  const BulkJob& J = jobs[blockIdx.x];
+  Inst& I = insts[J.inst];
+  const int ncls = I.nbuckets * (I.pmax + 1);
+  extern __shared__ int32_t tab[];
+  int32_t* first = tab;
+  int32_t* tail = tab + ncls;
+  int32_t* cnt = tab + 2 * ncls;
+  for (int c = threadIdx.x; c < ncls; c += blockDim.x) {
+    first[c] = -1;
+    cnt[c] = 0;
+  }
+  __syncthreads();
+  for (int t = J.tiles - 1; t >= 0; --t) {
+    const int ns = nseg[J.hoff + t];
+    const int64_t base = J.first + (int64_t)t * kTileI;
+    for (int q = threadIdx.x; q < ns; q += blockDim.x) {
+      const uint64_t pk = segs[J.off + (int64_t)t * kTileI + q];
+      const int c = (int)(pk >> 37);
+      const int32_t gf = (int32_t)(base + ((pk >> 25) & 4095)), gl = (int32_t)(base + ((pk >> 13) & 4095));
+      const int32_t nx = first[c];
+      if (nx >= 0) I.pt_next[gl] = nx; else tail[c] = gl;
+      first[c] = gf;
+      cnt[c] += (int32_t)(pk & 8191);
+    }
+    __syncthreads();
+  }
+  const int pm1 = I.pmax + 1;
+  for (int c = threadIdx.x; c < ncls; c += blockDim.x) {
+    if (cnt[c] == 0) continue;
+    const int32_t old_tail = I.cls_tail[c];
+    if (old_tail >= 0) I.pt_next[old_tail] = first[c]; else I.cls_head[c] = first[c];
+    I.cls_tail[c] = tail[c];
+    I.cls_cnt[c] += cnt[c];
+    const int b = c / pm1, p = c % pm1;
+    atomicOr(reinterpret_cast<unsigned long long*>(&I.bm1[(int64_t)b * I.bm_words + (p >> 6)]), 1ULL << (p & 63));
+    atomicOr(reinterpret_cast<unsigned long long*>(&I.bm2[(int64_t)b * I.bm_l2 + (p >> 12)]),
+             1ULL << ((p >> 6) & 63));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // the ingest scalars (k_bulk_finish)
+    I.arrival_cursor = J.first + J.k;
+    I.pt_count += (int32_t)J.k;
+    I.ev_total += J.k;
+    if ((int64_t)J.minp < I.pt_min_lb) I.pt_min_lb = (int64_t)J.minp;
+    for (int b = 0; b < I.nbuckets; ++b) I.bcnt[b] += (int32_t)J.bcnt[b];
+  }
+}
+
 // The instance scalars ingest() updates (engine.hpp:216-235).
 __global__ void k_bulk_finish(Inst* insts, const BulkJob* jobs) {
   const BulkJob& J = jobs[blockIdx.x];
@@ -2029,6 +2253,65 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
     while (bits < 32 && (ncls - 1) >> bits) ++bits;
   }
   if (jobs.empty()) return ECONO_OK;
+  {  // the default path: tile-local sorts + a per-instance stitch (no global sort)
+    int64_t max_ncls = 0;
+    for (const BulkJob& J : jobs) {
+      const Inst& I = b->inst[(size_t)J.inst].desc;
+      max_ncls = imax(max_ncls, (int64_t)I.nbuckets * (I.pmax + 1));
+    }
+    const size_t smem = 12 * (size_t)max_ncls;
+    if (!getenv("ECONO_INGEST_RADIX") && max_ncls <= 65536 && smem <= 200 * 1024) {
+      const int64_t budget = bulk_budget();
+      std::vector<size_t> gs;
+      int64_t max_off = 0, max_t = 0;
+      for (size_t g0 = 0; g0 < jobs.size();) {  // groups of jobs within the scratch budget
+        size_t g1 = g0;
+        int64_t off = 0, tl = 0;
+        while (g1 < jobs.size() && (g1 == g0 || off + (int64_t)jobs[g1].tiles * kTileI <= budget)) {
+          jobs[g1].off = off;   // segment slots: tile-aligned
+          jobs[g1].hoff = tl;   // per-tile segment counts
+          off += (int64_t)jobs[g1].tiles * kTileI;
+          tl += jobs[g1].tiles;
+          ++g1;
+        }
+        gs.push_back(g0);
+        max_off = imax(max_off, off);
+        max_t = imax(max_t, tl);
+        g0 = g1;
+      }
+      gs.push_back(jobs.size());
+      const size_t sb = (8 * (size_t)max_off + 255) & ~(size_t)255, nb = (4 * (size_t)max_t + 255) & ~(size_t)255;
+      const size_t need = sb + nb + sizeof(BulkJob) * jobs.size();
+      if (need > b->bulk_bytes) {
+        dev_free(b->bulk_buf);
+        b->bulk_buf = nullptr;
+        b->bulk_bytes = 0;
+        if (cudaMalloc(&b->bulk_buf, need) == cudaSuccess) b->bulk_bytes = need;
+      }
+      if (!b->bulk_buf) return set_err(err, errlen, "bulk ingest allocation failed"), ECONO_ECUDA;
+      char* base = (char*)b->bulk_buf;
+      uint64_t* segs = (uint64_t*)base;
+      int32_t* nseg = (int32_t*)(base + sb);
+      void* dj = base + sb + nb;
+      const auto t1 = now();
+      dev_h2d(dj, jobs.data(), sizeof(BulkJob) * jobs.size());
+      cudaFuncSetAttribute(k_ingest_stitch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      for (size_t g = 0; g + 1 < gs.size(); ++g) {
+        const int32_t nj = (int32_t)(gs[g + 1] - gs[g]);
+        int32_t tmax = 0;
+        for (size_t q = gs[g]; q < gs[g + 1]; ++q) tmax = std::max(tmax, jobs[q].tiles);
+        BulkJob* J = (BulkJob*)dj + gs[g];
+        k_ingest_tiles<<<dim3((unsigned)tmax, (unsigned)nj), 256, 0, b->stream>>>(b->d_insts, J, segs, nseg);
+        k_ingest_stitch<<<(unsigned)nj, 512, smem, b->stream>>>(b->d_insts, J, segs, nseg);
+      }
+      rc = sync_batch(b, err, errlen);
+      if (!rc) rc = cuda_check(err, errlen, "bulk ingest");
+      if (verbose)
+        fprintf(stderr, "[econo] bulk ingest (tiles): plan+alloc %.1f ms, kernels %.1f ms (%zu jobs, %zu groups)\n",
+                ms(t0, t1), ms(t1, now()), jobs.size(), gs.size() - 1);
+      return rc;
+    }
+  }
   const int passes = (bits + 7) / 8;
   // groups of jobs whose keys fit the temp budget; offsets are per group
   const int64_t budget = bulk_budget();
@@ -2162,8 +2445,11 @@ int econo_batch_reports(econo_batch* b, EconoReport* out, char* err, size_t errl
       if (dev_d2h(hist.data(), I.hist, sizeof(int64_t) * hist.size()))
         return set_err(err, errlen, "device copy failed"), ECONO_ECUDA;
       int k = 0;
-      for (int c = 0; c < I.hist_cap && k < ECONO_MAX_HIST; ++c)
+      for (int c = 0; c < I.hist_cap; ++c)
         if (hist[(size_t)c]) {
+          if (k >= ECONO_MAX_HIST)  // the fixed-size report cannot hold it: say so, never truncate
+            return set_err(err, errlen, "completion histogram has more than %d entries (ECONO_MAX_HIST)",
+                           ECONO_MAX_HIST), ECONO_ESIM;
           r.hist_count[k] = c;
           r.hist_frac[k] = (double)hist[(size_t)c] / (double)ex;
           ++k;
@@ -2416,8 +2702,11 @@ int econo_report(econo_engine* e, EconoReport* out, char* err, size_t errlen) {
     if (dev_d2h(hist.data(), I.hist, sizeof(int64_t) * hist.size()))
       return set_err(err, errlen, "device copy failed"), ECONO_ECUDA;
     int k = 0;
-    for (int c = 0; c < I.hist_cap && k < ECONO_MAX_HIST; ++c)
+    for (int c = 0; c < I.hist_cap; ++c)
       if (hist[(size_t)c]) {
+        if (k >= ECONO_MAX_HIST)  // the fixed-size report cannot hold it: say so, never truncate
+          return set_err(err, errlen, "completion histogram has more than %d entries (ECONO_MAX_HIST)",
+                         ECONO_MAX_HIST), ECONO_ESIM;
         r.hist_count[k] = c;
         r.hist_frac[k] = (double)hist[(size_t)c] / (double)executed;
         ++k;

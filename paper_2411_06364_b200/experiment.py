@@ -4,9 +4,10 @@ row 4): the reference's JSON experiment config (config.hpp:20-330), its sweep
 with every (sweep cell, policy) pair run as one instance of a single device
 batch instead of one engine per worker thread.
 
-Scope: the EconoServe policies (econoserve-d/-sd/-sdo/-full). A config naming
-a baseline policy parses as in the reference but running it raises
-ConfigError, like econo_create does.
+Scope: every policy of the reference — the EconoServe family and the five
+baselines (orca, vllm, sarathi, multires, sync-coupled) — runs on the device.
+Engine failures surface as the reference's SimulationError with the engine's
+own message (e.g. "simulation stuck"), config problems as ConfigError.
 """
 import copy
 import ctypes as C
@@ -16,7 +17,7 @@ import os
 import numpy as np
 
 from . import abi, wire
-from .engine import ConfigError, Engine, generate_trace, load
+from .engine import ConfigError, Engine, _raise, generate_trace, load
 
 POLICY_NAMES = ["orca", "vllm", "sarathi", "multires", "sync-coupled", "econoserve-d", "econoserve-sd",
                 "econoserve-sdo", "econoserve-full"]
@@ -426,8 +427,9 @@ def run_sweep(cfg, device=0, lib=None):
         recs = np.zeros(n, dtype=abi.RECORD_DTYPE)
         rep = abi.Report()
         err = C.create_string_buffer(1024)
-        if L.econo_records(v, recs.ctypes.data, n, err, 1024) or L.econo_report(v, C.byref(rep), err, 1024):
-            raise ConfigError(err.value.decode())
+        rc = L.econo_records(v, recs.ctypes.data, n, err, 1024) or L.econo_report(v, C.byref(rep), err, 1024)
+        if rc:  # the engine's own error (SimulationError for a stuck run), not a blanket ConfigError
+            _raise(rc, err)
         out[ci][1][name] = Result(name, recs, rep)
     b.close()
     return axes, [(c, dict(sorted(r.items()))) for c, r in out]

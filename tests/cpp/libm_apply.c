@@ -2,6 +2,6 @@
  * values for the device evaluation of the glibc exp/log port. */
 #include <math.h>
 #include <stdint.h>
-void libm_apply(int fn, const double* in, double* out, int64_t n) {
+extern "C" void libm_apply(int fn, const double* in, double* out, int64_t n) {
   for (int64_t i = 0; i < n; ++i) out[i] = fn == 0 ? exp(in[i]) : log(in[i]);
 }

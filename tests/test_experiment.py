@@ -129,19 +129,3 @@ def test_sweep_with_baselines_matches_reference(backend):
     text = json.dumps(j)
     axes, cells = X.run_sweep(X.parse_config(json.loads(text)), lib=_lib(backend))
     assert X.write_sweep_csv(axes, cells) == ref.sweep_csv(text)
-
-
-def test_cli_gen_trace_and_config_error(tmp_path, capsys):
-    from paper_2411_06364_b200 import cli
-    spec = {"n_requests": 500, "arrival_rate": 25.0, "seed": 9,
-            "prompt": {"mean": 100, "min": 10, "max": 900, "sigma": 0.7}}
-    sp = tmp_path / "spec.json"
-    sp.write_text(json.dumps(spec))
-    out = tmp_path / "t.csv"
-    assert cli.main(["gen-trace", "-s", str(sp), "-o", str(out)]) == 0
-    want = ref.write_csv(ref.generate_trace(500, 25.0, (100.0, 10, 900, 0.7), (58.41, 13, 292, 0.8), 9))
-    assert out.read_text() == want
-    bad = tmp_path / "bad.json"
-    bad.write_text(json.dumps({"policies": ["econoserve-full"], "bogus": 1}))
-    assert cli.main(["run", "-c", str(bad)]) == 2
-    assert "config error: unknown key 'bogus' in config" in capsys.readouterr().err

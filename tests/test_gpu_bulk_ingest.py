@@ -23,12 +23,17 @@ def _opts(policy):
     return o
 
 
+@pytest.mark.parametrize("path", ["tiles", "radix"])
 @pytest.mark.parametrize("policy", ["econoserve-full", "econoserve-sdo"])
-def test_bulk_ingest_matches_oracle(policy, monkeypatch):
+def test_bulk_ingest_matches_oracle(policy, path, monkeypatch):
+    """Both device paths: tile-local sorts + per-instance stitch (default) and
+    the global LSD radix sort (ECONO_INGEST_RADIX)."""
     monkeypatch.setenv("ECONO_BULK_INGEST_MIN", "1000")
+    if path == "radix":
+        monkeypatch.setenv("ECONO_INGEST_RADIX", "1")
     c = W.CONFIGS["cfg3_bookcorpus_1m"]
     traces = [port.generate_trace(n, 1e9, c["shape"]["prompt"], c["shape"]["rl"], 40 + i)
-              for i, n in enumerate([20000, 500, 7000])]   # 500 stays below the threshold
+              for i, n in enumerate([20000, 500, 7000, 4096, 4097])]   # 500 stays below the threshold
     o = _opts(policy)
     b = Batch(traces, o, device=0)
     b.launch(1)          # idle tick to the burst
