@@ -38,10 +38,11 @@
 // separate device functions (no call/stack traffic, scheduling across calls).
 #define EDEVNI __device__ __forceinline__
 #define EHD __host__ __device__ __forceinline__
-// Rare paths (compaction, the pipelining planner, preemption, overruns,
-// idle stretches) are kept out of line so the event-step code the warps
-// actually run stays dense in the instruction cache.
-#define ECOLD __device__ __noinline__
+// Rare paths (compaction, the pipelining planner, preemption, overruns, idle
+// stretches). Out of line (__noinline__) they left the hot code denser but
+// measured 7% slower (call frames, generic pointers to the shared Inst,
+// register allocation of the replay loop), so they stay inlined.
+#define ECOLD __device__ __forceinline__
 #define W 32
 #define LANE ((int)(threadIdx.x & 31))
 #define WSYNC() __syncwarp()
@@ -686,10 +687,11 @@ EDEV void addr_remove_region(Inst& I, int32_t r) {
 }
 EDEV int32_t region_new(Inst& I, int32_t owner, Tok start, Tok len) {  // all lanes get the id
   if (I.reg_free_top <= 0) { set_error(I, ERR_TABLE_OVERFLOW, owner, 2); return -1; }
+  // the free-list top and the owner's list fields load in one round
   const int32_t r = I.reg_free[I.reg_free_top - 1];
+  const int32_t tail = I.reg_tail[owner], hd = I.held[owner];
   WSYNC();
-  {  // warp-uniform; the owner's list fields are loaded before any store
-    const int32_t tail = I.reg_tail[owner], hd = I.held[owner];
+  {  // warp-uniform (every lane, same values)
     I.reg_free_top--;
     I.rg_start[r] = (int32_t)start;
     I.rg_len[r] = (int32_t)len;
@@ -946,6 +948,49 @@ EDEV int32_t gq_pos(const Inst& I, int32_t g) {  // position of g (keys unique)
     return !(hx != hg ? hx < hg : I.gr_seq[x] < sg);
   });
 }
+// place()'s re-insert at upper_bound (queues.hpp:187-197). With at most W-1
+// groups queued (the usual case) one warp-wide load of the queue serves both
+// the search and the shift.
+EDEV void gq_insert(Inst& I, int32_t g) {
+  const int32_t G = I.G;
+  if (G < W) {
+    const int32_t x = LANE < G ? I.gq[LANE] : -1;
+    const uint64_t hg = gkey_hi(I, g), sg = I.gr_seq[g];
+    bool after = false;  // key(g) < key(x): g goes before x
+    if (x >= 0) {
+      const uint64_t hx = gkey_hi(I, x);
+      after = hg != hx ? hg < hx : sg < I.gr_seq[x];
+    }
+    const unsigned m = BALLOT(after);
+    const int32_t pos = m ? FFS(m) : G;
+    WSYNC();
+    if (x >= 0 && LANE >= pos) I.gq[LANE + 1] = x;
+    WSYNC();
+    UNI(I.gq[pos] = g; I.G = G + 1);
+    return;
+  }
+  const int32_t p2 = gq_upper(I, g);
+  arr_insert(I.gq, G, p2, g);
+  UNI(I.G++);
+}
+// Removes group g from the queue (keys unique: found by identity when the
+// queue fits one warp, else by its key).
+EDEV void gq_erase(Inst& I, int32_t g) {
+  const int32_t G = I.G;
+  if (G <= W) {
+    const int32_t x = LANE < G ? I.gq[LANE] : -1;
+    const unsigned m = BALLOT(x == g && LANE < G);
+    const int32_t pos = m ? FFS(m) : G;
+    WSYNC();
+    if (LANE > pos && LANE < G) I.gq[LANE - 1] = x;
+    WSYNC();
+    UNI(I.G = G - 1);
+    return;
+  }
+  const int32_t pos = gq_pos(I, g);
+  arr_erase(I.gq, G, pos, 1);
+  UNI(I.G--);
+}
 EDEV void gq_rekey(Inst& I, int32_t g, double now) {  // place(): make_key (queues.hpp:187-193), lane 0
   if (I.ordered) {
     I.gr_db[g] = bucket_d(I, dmax(0.0, I.gr_mindl[g] - now));
@@ -998,11 +1043,7 @@ EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline
       const int32_t ndb = I.ordered ? bucket_d(I, dmax(0.0, nmd - now)) : odb;
       const int32_t nkb = I.ordered ? bucket_k(I, nmo) : okb;
       const bool moved = ndb != odb || nkb != okb;
-      if (moved) {  // the old key still locates the group
-        const int32_t pos = gq_pos(I, g);
-        arr_erase(I.gq, I.G, pos, 1);
-        UNI(I.G--);
-      }
+      if (moved) gq_erase(I, g);  // before the key fields change
       {  // warp-uniform (every lane, same values)
         if (cnt == 0) { I.gr_head[g] = id; I.gr_hd[g] = (int32_t)d; } else { I.gt_next[tail] = id; }
         I.gr_tail[g] = id;
@@ -1014,11 +1055,7 @@ EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline
         I.gr_kb[g] = nkb;
       }
       WSYNC();
-      if (moved) {
-        const int32_t p2 = gq_upper(I, g);
-        arr_insert(I.gq, I.G, p2, g);
-        UNI(I.G++);
-      }
+      if (moved) gq_insert(I, g);
       return;
     }
   }
@@ -1033,9 +1070,7 @@ EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline
         I.gr_db[g] = I.ordered ? bucket_d(I, dmax(0.0, deadline - now)) : 0;
         I.gr_kb[g] = I.ordered ? bucket_k(I, occ) : 0;
         rl_set(I, padded, g));
-  const int32_t p2 = gq_upper(I, g);
-  arr_insert(I.gq, I.G, p2, g);
-  UNI(I.G++);
+  gq_insert(I, g);
 }
 EDEV void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline, int32_t occ, double now) {
   group_insert_gt(I, id, padded, deadline, occ, now, member_demand(I, id));
@@ -1476,6 +1511,8 @@ EDEVNI int32_t select_gt(Inst& I, int32_t* nsel_out) {
           I.selg_rl[nselg] = grl;
           int32_t m = head;
           for (int32_t i = 0; i < cnt; ++i) { I.sel_ids[nsel + i] = m; m = I.gt_next[m]; }
+          rl_set(I, grl, -1);  // the group leaves the queue (erased below, in one shift)
+          I.grp_free[I.grp_free_top++] = g;
         }
         WSYNC();
         nsel += cnt;
@@ -1513,13 +1550,6 @@ EDEVNI int32_t select_gt(Inst& I, int32_t* nsel_out) {
       break;
     }
     if (whole > 0) {
-      for (int32_t i = LANE; i < whole; i += W) {
-        const int32_t g = I.gq[i];
-        rl_set(I, I.gr_rl[g], -1);
-      }
-      WSYNC();
-      /* warp-uniform */
-        for (int32_t i = 0; i < whole; ++i) I.grp_free[I.grp_free_top++] = I.gq[i];
       WSYNC();
       arr_erase(I.gq, I.G, 0, whole);
       UNI(I.G -= whole);
@@ -1607,9 +1637,14 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
   if (I.pt_count > 0) {
     // pt_admittable (engine.hpp:301-307): some queued prompt fits both budgets
     bool adm = false;
+    int adm_b = -1, adm_p = -1;  // the first bucket with a fitting class, and that class
     if (C0 >= 1 && C0 >= I.pt_min_lb) {
       if (I.ordered) {
-        for (int b = 0; b < I.nbuckets && !adm; ++b) adm = bm_prev(I, b, C0) >= 1;
+        for (int b = 0; b < I.nbuckets; ++b) {
+          const int p = bm_prev(I, b, C0);
+          if (p >= 1) { adm_b = b; adm_p = p; break; }
+        }
+        adm = adm_b >= 0;
       } else {
         adm = I.tree[I.tree_off[I.tree_levels - 1]] <= C0;
       }
@@ -1622,18 +1657,22 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
       if (!adm) {
         // nothing fits (the admittable probe above used the same bound)
       } else if (I.ordered) {
-        for (int b = 0; b < I.nbuckets && C > 0; ++b) {
-          Tok x = C;
-          for (;;) {
-            const int p = bm_prev(I, b, x);
-            if (p < 1) break;
+        // buckets before adm_b hold nothing <= C0, and adm_b's first probe at
+        // C0 is the admittable probe's answer; once the budget is below the
+        // smallest queued prompt (pt_min_lb) nothing further can fit
+        bool done = false;
+        for (int b = adm_b; b < I.nbuckets && C > 0 && !done; ++b) {
+          int p = b == adm_b ? adm_p : bm_prev(I, b, C);
+          while (p >= 1) {
             const int32_t cnt = I.cls_cnt[cls_of(I, b, p)];
             const Tok fit = udiv(C, p);
             const int32_t k = (int32_t)(fit < cnt ? fit : cnt);
             npt = cls_take(I, b, p, k, I.tmp_a, npt);
             C -= (Tok)k * p;
-            x = tmin((Tok)p - 1, C);
+            if (C < I.pt_min_lb) { done = true; break; }
+            const Tok x = tmin((Tok)p - 1, C);
             if (x < 1) break;
+            p = bm_prev(I, b, x);
           }
         }
       } else {
@@ -1756,25 +1795,57 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   UNI(I.clock += dt; I.iter++; if (B) I.pending_stall = 0.0);
   const bool pause = B && I.decode_pause;
   const double sched = (double)I.exam_count * I.sched_cost;
-  if (I.n_adm > 0 && sched > 0.0) {
-    const double share = sched / (double)I.n_adm;
-    for (int32_t i = LANE; i < I.n_adm; i += W) I.sched_share[I.adm[i]] += share;
-  }
-  // prefill + decode progress (per-request updates are independent)
+  const int32_t n_adm = I.n_adm, n_pt = I.n_ptiter;
+  const bool share_on = n_adm > 0 && sched > 0.0;
+  const double share = share_on ? sched / (double)n_adm : 0.0;
   Tok wsum_pt = 0;
-  for (int32_t i = LANE; i < I.n_ptiter; i += W) {
-    const int32_t id = I.ptiter_id[i];
-    const int32_t tk = I.ptiter_tok[i];
-    const double e = I.exec_t[id];
-    const int32_t pd = I.prefill_done[id] + tk, wr = I.written[id], oc = I.occupied[id];
-    const int32_t pr = B ? I.ptarget[id] : I.prompt[id];
-    const uint8_t f = I.flags[id];
-    I.exec_t[id] = e + dt;
-    I.prefill_done[id] = pd;
-    I.written[id] = wr + tk;
-    I.occupied[id] = oc + tk;
-    wsum_pt += tk;
-    if (pd >= pr) I.flags[id] = (uint8_t)(f | F_PREFILL_FIN);
+  if (n_adm <= W && n_pt <= W) {
+    // the scheduling-share accrual (engine.hpp:737-741) and the prefill
+    // progress (engine.hpp:763-771) touch different fields: all their loads
+    // are issued before any store (two dependent rounds instead of four)
+    const bool a_on = share_on && LANE < n_adm, p_on = LANE < n_pt;
+    const int32_t aid = a_on ? I.adm[LANE] : 0;
+    const int32_t id = p_on ? I.ptiter_id[LANE] : 0;
+    const int32_t tk = p_on ? I.ptiter_tok[LANE] : 0;
+    double ss = 0.0, e = 0.0;
+    int32_t pd = 0, wr = 0, oc = 0, pr = 0;
+    uint8_t f = 0;
+    if (a_on) ss = I.sched_share[aid];
+    if (p_on) {
+      e = I.exec_t[id];
+      pd = I.prefill_done[id] + tk;
+      wr = I.written[id];
+      oc = I.occupied[id];
+      pr = B ? I.ptarget[id] : I.prompt[id];
+      f = I.flags[id];
+    }
+    if (a_on) I.sched_share[aid] = ss + share;
+    if (p_on) {
+      I.exec_t[id] = e + dt;
+      I.prefill_done[id] = pd;
+      I.written[id] = wr + tk;
+      I.occupied[id] = oc + tk;
+      wsum_pt = tk;
+      if (pd >= pr) I.flags[id] = (uint8_t)(f | F_PREFILL_FIN);
+    }
+  } else {
+    if (share_on)
+      for (int32_t i = LANE; i < n_adm; i += W) I.sched_share[I.adm[i]] += share;
+    // prefill + decode progress (per-request updates are independent)
+    for (int32_t i = LANE; i < n_pt; i += W) {
+      const int32_t id = I.ptiter_id[i];
+      const int32_t tk = I.ptiter_tok[i];
+      const double e = I.exec_t[id];
+      const int32_t pd = I.prefill_done[id] + tk, wr = I.written[id], oc = I.occupied[id];
+      const int32_t pr = B ? I.ptarget[id] : I.prompt[id];
+      const uint8_t f = I.flags[id];
+      I.exec_t[id] = e + dt;
+      I.prefill_done[id] = pd;
+      I.written[id] = wr + tk;
+      I.occupied[id] = oc + tk;
+      wsum_pt += tk;
+      if (pd >= pr) I.flags[id] = (uint8_t)(f | F_PREFILL_FIN);
+    }
   }
   wsum_pt = wsum(wsum_pt);
   // every running GT writes exactly one token this iteration
@@ -1803,6 +1874,8 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   PHASE_ADD(13, tx1 - tx0);
   int32_t completed_now = 0, npre = 0;
   const int32_t R0 = I.R;
+  int32_t id_c0 = -1;   // the first chunk's ids and survivors: with R0 <= W the
+  unsigned keep0 = 0;   // running list is compacted from the ballot, no re-read
   for (int32_t base = 0; base < R0; base += W) {
     const int32_t i = base + LANE;
     const int32_t id = i < R0 ? I.run[i] : -1;
@@ -1830,6 +1903,10 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     if (under) I.tmp_a[npre + POPC(mu & LANEMASK_LT)] = id;
     npre += POPC(mu);
     unsigned m = BALLOT(fin);
+    if (base == 0) {
+      id_c0 = id;
+      keep0 = BALLOT(id >= 0 && !fin);
+    }
     WSYNC();
     while (m) {
       const int l = FFS(m);
@@ -1845,7 +1922,15 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
       completed_now++;
     }
   }
-  if (completed_now) run_compact(I);
+  if (completed_now) {
+    if (R0 <= W) {  // releases never change another running request's state
+      if ((keep0 >> LANE) & 1u) I.run[POPC(keep0 & LANEMASK_LT)] = id_c0;
+      WSYNC();
+      UNI(I.R = POPC(keep0));
+    } else {
+      run_compact(I);
+    }
+  }
   [[maybe_unused]] const int64_t tx2 = PHASE_NOW();
   PHASE_ADD(3, tx2 - tx1);
   // prefill transitions (engine.hpp:794-809)
