@@ -2096,7 +2096,11 @@ EDEV int64_t step_event_bound(const Inst& I) {
 // running requests' progress counters and the in-order sample aggregates, so
 // a span of them is replayed with the same sequential FP adds (never k*dt).
 // ------------------------------------------------------------------------
-EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
+// *fuse: the event iteration that ends the span consists of completions only
+// (no under-prediction, no slot deadline, nothing selectable), so the replay
+// may run it too and finish it with complete_fused() instead of a normal step.
+EDEVNI int64_t quiet_span(Inst& I, int64_t budget, bool* fuse) {
+  *fuse = false;
   const int32_t R = I.R;
   if (R == 0 || I.n_ptiter != 0 || I.n_adm != 0 || budget <= 0) return 0;
   // The independent probes are issued together (three dependent levels in
@@ -2113,10 +2117,12 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
     gd = I.gr_dem[g];
     hd = I.gr_hd[g];
   }
-  int64_t kev = INT64_MAX;
+  // distance to the first completion (true_rl <= allowance) and to the first
+  // under-prediction (allowance < true_rl, engine.hpp:812-817)
+  int64_t kc = INT64_MAX, ku = INT64_MAX, ks = INT64_MAX;
   if (id0 >= 0) {
     const int32_t tr = I.true_rl[id0], al = I.allowance[id0], ge = I.generated[id0];
-    kev = (int64_t)(tr < al ? tr : al) - ge;
+    if (tr <= al) kc = (int64_t)tr - ge; else ku = (int64_t)al - ge;
   }
   if (has_arr && ta <= I.clock + 1e-12) return 0;
   if (gt_check) {  // queues.hpp:220-263 would take >= 1 member
@@ -2136,22 +2142,26 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget) {
   // first decode-side event: completion / under-prediction / slot deadline
   for (int32_t i = W + LANE; i < R; i += W) {
     const int32_t id = I.run[i];
-    const int64_t lim = I.true_rl[id] < I.allowance[id] ? I.true_rl[id] : I.allowance[id];
-    const int64_t e = lim - I.generated[id];
-    kev = e < kev ? e : kev;
+    const int32_t tr = I.true_rl[id], al = I.allowance[id], ge = I.generated[id];
+    if (tr <= al) kc = tmin(kc, (int64_t)tr - ge); else ku = tmin(ku, (int64_t)al - ge);
   }
   for (int32_t si = LANE; si < I.n_slots; si += W) {
     const int32_t sp = I.slots[si];
     const int32_t host = I.sl_host[sp];
     if (I.state[host] == ST_RUNNING) {
       const int64_t e = (int64_t)I.sl_off[sp] - (I.generated[host] - I.gen_epoch[host]);
-      kev = e < kev ? e : kev;
+      ks = e < ks ? e : ks;
     }
   }
-  kev = wmin(kev);
-  int64_t k = kev - 1;  // the event iteration itself runs as a normal step
+  kc = wmin(kc);
+  ku = wmin(ku);
+  ks = wmin(ks);
+  const int64_t kev = tmin(kc, tmin(ku, ks));
+  int64_t k = kev - 1;  // the event iteration itself runs as a normal step ...
   if (k > budget) k = budget;
   if (I.record_samples && k > I.sm_cap - I.sm_n) k = I.sm_cap - I.sm_n;
+  // ... unless it only completes requests and fits the budget (bench path)
+  *fuse = !I.record_events && !I.record_samples && kev >= 1 && kev <= budget && kc == kev && ku > kev && ks > kev;
   return k > 0 ? k : 0;
 }
 
@@ -2232,13 +2242,63 @@ EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double c
   return k;
 }
 
-EDEVNI int64_t quiet_steps(Inst& I, int64_t k) {
+// The fused event iteration's completions (execute_iteration, engine.hpp:
+// 784-791): the replay already ran its decode progress, clock and sample
+// sums; the requests that reached true_rl complete in running order, exactly
+// as in the running-set pass, and the iteration moves from hist[0] to its
+// completion count. Under-predictions and slot deadlines cannot occur here
+// (quiet_span's fuse test).
+EDEVNI void complete_fused(Inst& I) {
+  const int32_t R0 = I.R;
+  int32_t completed_now = 0;
+  int32_t id_c0 = -1;
+  unsigned keep0 = 0;
+  for (int32_t base = 0; base < R0; base += W) {
+    const int32_t i = base + LANE;
+    const int32_t id = i < R0 ? I.run[i] : -1;
+    const bool fin = id >= 0 && I.generated[id] >= I.true_rl[id];
+    if (base == 0) {
+      id_c0 = id;
+      keep0 = BALLOT(id >= 0 && !fin);
+    }
+    unsigned m = BALLOT(fin);
+    WSYNC();
+    while (m) {
+      const int l = FFS(m);
+      m &= m - 1;
+      const int32_t cid = shfl(id, l);
+      UNI(I.state[cid] = ST_DONE; I.compl_clock[cid] = I.clock);
+      kvc_release(I, cid);
+      if (I.error) return;
+      UNI(I.occupied[cid] = 0; I.completed++);
+      logev(I, ECONO_EV_COMPLETE, cid, I.generated[cid], 0);
+      WSYNC();
+      completed_now++;
+    }
+  }
+  if (R0 <= W) {
+    if ((keep0 >> LANE) & 1u) I.run[POPC(keep0 & LANEMASK_LT)] = id_c0;
+    WSYNC();
+    UNI(I.R = POPC(keep0));
+  } else {
+    run_compact(I);
+  }
+  UNI(I.hist[0]--; I.hist[completed_now < I.hist_cap ? completed_now : I.hist_cap - 1]++;
+      I.quiet_steps--);
+}
+
+EDEVNI int64_t quiet_steps(Inst& I, int64_t k, bool fuse = false) {
   const Tok fs = I.R;
   const double dt = iteration_time(I, fs) + 0.0;
   const double clk1 = I.clock + dt;
   const double af = (double)((I.general_cap - I.free_total) + I.reserved_used) / (double)I.capacity;
   const int64_t wt0 = I.written_total;
   const double cap = (double)I.capacity;
+  if (fuse) {  // the k quiet iterations and the completing one (quiet_span's fuse)
+    const int64_t j = quiet_steps_fused(I, k + 1, fs, dt, clk1, af, wt0, cap);
+    if (j == k + 1) complete_fused(I);  // an arrival cut-off leaves the event to a normal step
+    return j;
+  }
   if (!I.record_samples) return quiet_steps_fused(I, k, fs, dt, clk1, af, wt0, cap);
   // pass 1 (every lane, identical arithmetic): the sequential clock chain and
   // the arrival cut-off — ingest would admit an arrival at the next step.

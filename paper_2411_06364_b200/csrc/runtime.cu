@@ -184,11 +184,12 @@ EDEVNI void engine_steps(Inst& I, int64_t max_steps, int64_t deadline_ns = 0) {
     }
     if (!B && I.skip && test) {
       const int64_t t0 = PROF_NOW();
-      const int64_t k = quiet_span(I, max_steps - s);
+      bool fuse = false;
+      const int64_t k = quiet_span(I, max_steps - s, &fuse);
       const int64_t t1 = PROF_NOW();
       LANE0(I.prof[0] += t1 - t0);
-      if (k > 0) {
-        s += quiet_steps(I, k);
+      if (k > 0 || fuse) {
+        s += quiet_steps(I, k, fuse);
         LANE0(I.prof[1] += PROF_NOW() - t1; I.prof[4]++);
         test = false;
         continue;
