@@ -101,6 +101,18 @@ static inline uint64_t umulhi64(uint64_t a, uint64_t b) {
 #define PHASE_ADD(k, v) ((void)0)
 #endif
 
+// Event / sample recording switches. A translation unit compiled with
+// ECONO_NOREC (csrc/kernel_norec.cu) gets a copy of the step loop with every
+// recording path removed at compile time; the runtime launches it for
+// batches that record nothing (the bench path), the generic copy otherwise.
+#ifdef ECONO_NOREC
+#define REC_EV(I) false
+#define REC_SM(I) false
+#else
+#define REC_EV(I) ((I).record_events != 0)
+#define REC_SM(I) ((I).record_samples != 0)
+#endif
+
 #define LANE0(stmt) \
   do {              \
     if (LANE == 0) { stmt; } \
@@ -293,6 +305,21 @@ EDEV T wsum(T v) {
   for (int o = W / 2; o > 0; o >>= 1) v += shfl_xor(v, o);
   return v;
 }
+// 32-bit reductions: one REDUX instruction instead of five shuffle rounds.
+EDEV int32_t wmin32(int32_t v) {
+#ifdef __CUDA_ARCH__
+  return __reduce_min_sync(0xffffffffu, v);
+#else
+  return v;
+#endif
+}
+EDEV int32_t wsum32(int32_t v) {
+#ifdef __CUDA_ARCH__
+  return __reduce_add_sync(0xffffffffu, v);
+#else
+  return v;
+#endif
+}
 
 // Shift a[pos..n) right by one and store v at pos (room for n+1 required).
 template <class T>
@@ -347,7 +374,7 @@ EDEV int32_t arr_find(const int32_t* a, int32_t n, int32_t v) {
 EDEV void logev(Inst& I, int kind, int32_t id, int64_t a, int64_t b) {  // engine.hpp:211-214
   {
     I.ev_total++;
-    if (I.record_events) {
+    if (REC_EV(I)) {
       if (I.ev_n < I.ev_cap) {
         EconoEvent& e = I.ev[I.ev_n];
         e.iter = I.iter;
@@ -948,47 +975,16 @@ EDEV int32_t gq_pos(const Inst& I, int32_t g) {  // position of g (keys unique)
     return !(hx != hg ? hx < hg : I.gr_seq[x] < sg);
   });
 }
-// place()'s re-insert at upper_bound (queues.hpp:187-197). With at most W-1
-// groups queued (the usual case) one warp-wide load of the queue serves both
-// the search and the shift.
+// place()'s re-insert at upper_bound (queues.hpp:187-197) and the removal of
+// a group by its (unique) key.
 EDEV void gq_insert(Inst& I, int32_t g) {
-  const int32_t G = I.G;
-  if (G < W) {
-    const int32_t x = LANE < G ? I.gq[LANE] : -1;
-    const uint64_t hg = gkey_hi(I, g), sg = I.gr_seq[g];
-    bool after = false;  // key(g) < key(x): g goes before x
-    if (x >= 0) {
-      const uint64_t hx = gkey_hi(I, x);
-      after = hg != hx ? hg < hx : sg < I.gr_seq[x];
-    }
-    const unsigned m = BALLOT(after);
-    const int32_t pos = m ? FFS(m) : G;
-    WSYNC();
-    if (x >= 0 && LANE >= pos) I.gq[LANE + 1] = x;
-    WSYNC();
-    UNI(I.gq[pos] = g; I.G = G + 1);
-    return;
-  }
   const int32_t p2 = gq_upper(I, g);
-  arr_insert(I.gq, G, p2, g);
+  arr_insert(I.gq, I.G, p2, g);
   UNI(I.G++);
 }
-// Removes group g from the queue (keys unique: found by identity when the
-// queue fits one warp, else by its key).
 EDEV void gq_erase(Inst& I, int32_t g) {
-  const int32_t G = I.G;
-  if (G <= W) {
-    const int32_t x = LANE < G ? I.gq[LANE] : -1;
-    const unsigned m = BALLOT(x == g && LANE < G);
-    const int32_t pos = m ? FFS(m) : G;
-    WSYNC();
-    if (LANE > pos && LANE < G) I.gq[LANE - 1] = x;
-    WSYNC();
-    UNI(I.G = G - 1);
-    return;
-  }
   const int32_t pos = gq_pos(I, g);
-  arr_erase(I.gq, G, pos, 1);
+  arr_erase(I.gq, I.G, pos, 1);
   UNI(I.G--);
 }
 EDEV void gq_rekey(Inst& I, int32_t g, double now) {  // place(): make_key (queues.hpp:187-193), lane 0
@@ -1123,7 +1119,7 @@ EDEVNI void ingest(Inst& I) {
   const int64_t last = due_end(I, first, lim);
   if (last == first) return;
   const int64_t k = last - first;
-  if (I.record_events) {
+  if (REC_EV(I)) {
     for (int64_t i = LANE; i < k; i += W) {
       const int64_t e = I.ev_n + i;
       if (e < I.ev_cap) {
@@ -1137,7 +1133,7 @@ EDEVNI void ingest(Inst& I) {
     // sync-coupled: arrivals join the waiting groups (engine.hpp:226-228)
     for (int64_t id = first; id < last; ++id)
       group_insert_gt(I, (int32_t)id, padded_of(I, id), slo_of(I, id), 0, I.clock);
-    UNI(I.arrival_cursor = last; I.ev_total += k; if (I.record_events) I.ev_n += k);
+    UNI(I.arrival_cursor = last; I.ev_total += k; if (REC_EV(I)) I.ev_n += k);
     return;
   }
   if (!B) {
@@ -1189,7 +1185,7 @@ EDEVNI void ingest(Inst& I) {
     tree_fix(I, first, last - 1);
   }
   UNI(I.arrival_cursor = last; I.pt_count += (int32_t)k; I.ev_total += k;
-        if (I.record_events) I.ev_n += k);
+        if (REC_EV(I)) I.ev_n += k);
 }
 
 // Takes up to k entries from the head of class (b,p); appends ids to out.
@@ -1254,7 +1250,7 @@ EDEVNI void dispatch_pts(Inst& I, int32_t npt) {
       I.ptiter_id[I.n_ptiter + LANE] = id;
       I.ptiter_tok[I.n_ptiter + LANE] = p;
       I.adm[I.n_adm + LANE] = id;
-      if (I.record_events && I.ev_n + LANE < I.ev_cap) {
+      if (REC_EV(I) && I.ev_n + LANE < I.ev_cap) {
         EconoEvent& e = I.ev[I.ev_n + LANE];
         e.iter = I.iter; e.clock = I.clock; e.kind = ECONO_EV_PT_DISPATCH; e.id = id; e.a = 0; e.b = 0;
       }
@@ -1264,7 +1260,7 @@ EDEVNI void dispatch_pts(Inst& I, int32_t npt) {
     WSYNC();
     UNI(I.reserved_used = used0 + (cnt > 0 ? took : 0); I.n_ptiter += cnt; I.n_adm += cnt;
           I.pts_admitted_iter += cnt; I.pt_dispatched += cnt; I.ev_total += cnt;
-          if (I.record_events) I.ev_n += cnt);
+          if (REC_EV(I)) I.ev_n += cnt);
     if (bad) { set_error(I, ERR_RESERVED_DRAW, bad_id, 0); return; }
   }
 }
@@ -1795,59 +1791,27 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   UNI(I.clock += dt; I.iter++; if (B) I.pending_stall = 0.0);
   const bool pause = B && I.decode_pause;
   const double sched = (double)I.exam_count * I.sched_cost;
-  const int32_t n_adm = I.n_adm, n_pt = I.n_ptiter;
-  const bool share_on = n_adm > 0 && sched > 0.0;
-  const double share = share_on ? sched / (double)n_adm : 0.0;
-  Tok wsum_pt = 0;
-  if (n_adm <= W && n_pt <= W) {
-    // the scheduling-share accrual (engine.hpp:737-741) and the prefill
-    // progress (engine.hpp:763-771) touch different fields: all their loads
-    // are issued before any store (two dependent rounds instead of four)
-    const bool a_on = share_on && LANE < n_adm, p_on = LANE < n_pt;
-    const int32_t aid = a_on ? I.adm[LANE] : 0;
-    const int32_t id = p_on ? I.ptiter_id[LANE] : 0;
-    const int32_t tk = p_on ? I.ptiter_tok[LANE] : 0;
-    double ss = 0.0, e = 0.0;
-    int32_t pd = 0, wr = 0, oc = 0, pr = 0;
-    uint8_t f = 0;
-    if (a_on) ss = I.sched_share[aid];
-    if (p_on) {
-      e = I.exec_t[id];
-      pd = I.prefill_done[id] + tk;
-      wr = I.written[id];
-      oc = I.occupied[id];
-      pr = B ? I.ptarget[id] : I.prompt[id];
-      f = I.flags[id];
-    }
-    if (a_on) I.sched_share[aid] = ss + share;
-    if (p_on) {
-      I.exec_t[id] = e + dt;
-      I.prefill_done[id] = pd;
-      I.written[id] = wr + tk;
-      I.occupied[id] = oc + tk;
-      wsum_pt = tk;
-      if (pd >= pr) I.flags[id] = (uint8_t)(f | F_PREFILL_FIN);
-    }
-  } else {
-    if (share_on)
-      for (int32_t i = LANE; i < n_adm; i += W) I.sched_share[I.adm[i]] += share;
-    // prefill + decode progress (per-request updates are independent)
-    for (int32_t i = LANE; i < n_pt; i += W) {
-      const int32_t id = I.ptiter_id[i];
-      const int32_t tk = I.ptiter_tok[i];
-      const double e = I.exec_t[id];
-      const int32_t pd = I.prefill_done[id] + tk, wr = I.written[id], oc = I.occupied[id];
-      const int32_t pr = B ? I.ptarget[id] : I.prompt[id];
-      const uint8_t f = I.flags[id];
-      I.exec_t[id] = e + dt;
-      I.prefill_done[id] = pd;
-      I.written[id] = wr + tk;
-      I.occupied[id] = oc + tk;
-      wsum_pt += tk;
-      if (pd >= pr) I.flags[id] = (uint8_t)(f | F_PREFILL_FIN);
-    }
+  if (I.n_adm > 0 && sched > 0.0) {
+    const double share = sched / (double)I.n_adm;
+    for (int32_t i = LANE; i < I.n_adm; i += W) I.sched_share[I.adm[i]] += share;
   }
-  wsum_pt = wsum(wsum_pt);
+  // prefill + decode progress (per-request updates are independent)
+  Tok wsum_pt = 0;
+  for (int32_t i = LANE; i < I.n_ptiter; i += W) {
+    const int32_t id = I.ptiter_id[i];
+    const int32_t tk = I.ptiter_tok[i];
+    const double e = I.exec_t[id];
+    const int32_t pd = I.prefill_done[id] + tk, wr = I.written[id], oc = I.occupied[id];
+    const int32_t pr = B ? I.ptarget[id] : I.prompt[id];
+    const uint8_t f = I.flags[id];
+    I.exec_t[id] = e + dt;
+    I.prefill_done[id] = pd;
+    I.written[id] = wr + tk;
+    I.occupied[id] = oc + tk;
+    wsum_pt += tk;
+    if (pd >= pr) I.flags[id] = (uint8_t)(f | F_PREFILL_FIN);
+  }
+  wsum_pt = wsum32((int32_t)wsum_pt);  // prompt tokens of one iteration (< reserve capacity < 2^30)
   // every running GT writes exactly one token this iteration
   UNI(I.written_total += wsum_pt + (pause ? 0 : I.R));
   EconoSample s;
@@ -2003,7 +1967,7 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
   if (npre || ncs) run_compact(I);
   {  // warp-uniform (every lane, same values)
     s.completed = completed_now;
-    if (I.record_samples) {
+    if (REC_SM(I)) {
       if (I.sm_n < I.sm_cap) I.sm[I.sm_n] = s;
       I.sm_n++;
     }
@@ -2042,7 +2006,7 @@ ECOLD void handle_idle(Inst& I) {  // engine.hpp:930-961
       const double dt = (double)k * I.t_base;
       I.clock += dt;
       I.iter += k;
-      if (I.record_samples) {
+      if (REC_SM(I)) {
         if (I.sm_n < I.sm_cap) {
           EconoSample& s = I.sm[I.sm_n];
           s.iter = I.iter;
@@ -2119,10 +2083,10 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget, bool* fuse) {
   }
   // distance to the first completion (true_rl <= allowance) and to the first
   // under-prediction (allowance < true_rl, engine.hpp:812-817)
-  int64_t kc = INT64_MAX, ku = INT64_MAX, ks = INT64_MAX;
+  int32_t kc = INT32_MAX, ku = INT32_MAX, ks = INT32_MAX;  // token counts < 2^30
   if (id0 >= 0) {
     const int32_t tr = I.true_rl[id0], al = I.allowance[id0], ge = I.generated[id0];
-    if (tr <= al) kc = (int64_t)tr - ge; else ku = (int64_t)al - ge;
+    if (tr <= al) kc = tr - ge; else ku = al - ge;
   }
   if (has_arr && ta <= I.clock + 1e-12) return 0;
   if (gt_check) {  // queues.hpp:220-263 would take >= 1 member
@@ -2143,25 +2107,29 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget, bool* fuse) {
   for (int32_t i = W + LANE; i < R; i += W) {
     const int32_t id = I.run[i];
     const int32_t tr = I.true_rl[id], al = I.allowance[id], ge = I.generated[id];
-    if (tr <= al) kc = tmin(kc, (int64_t)tr - ge); else ku = tmin(ku, (int64_t)al - ge);
+    if (tr <= al) kc = kc < tr - ge ? kc : tr - ge; else ku = ku < al - ge ? ku : al - ge;
   }
   for (int32_t si = LANE; si < I.n_slots; si += W) {
     const int32_t sp = I.slots[si];
     const int32_t host = I.sl_host[sp];
     if (I.state[host] == ST_RUNNING) {
-      const int64_t e = (int64_t)I.sl_off[sp] - (I.generated[host] - I.gen_epoch[host]);
+      const int32_t e = I.sl_off[sp] - (I.generated[host] - I.gen_epoch[host]);
       ks = e < ks ? e : ks;
     }
   }
-  kc = wmin(kc);
-  ku = wmin(ku);
-  ks = wmin(ks);
-  const int64_t kev = tmin(kc, tmin(ku, ks));
+  kc = wmin32(kc);
+  ku = wmin32(ku);
+  ks = wmin32(ks);
+  const int64_t kev = kc == INT32_MAX && ku == INT32_MAX && ks == INT32_MAX ? INT64_MAX
+                                                                          : (int64_t)(kc < ku ? (kc < ks ? kc : ks) : (ku < ks ? ku : ks));
   int64_t k = kev - 1;  // the event iteration itself runs as a normal step ...
   if (k > budget) k = budget;
-  if (I.record_samples && k > I.sm_cap - I.sm_n) k = I.sm_cap - I.sm_n;
+  if (REC_SM(I) && k > I.sm_cap - I.sm_n) k = I.sm_cap - I.sm_n;
   // ... unless it only completes requests and fits the budget (bench path)
-  *fuse = !I.record_events && !I.record_samples && kev >= 1 && kev <= budget && kc == kev && ku > kev && ks > kev;
+  // (running set within one warp: its completion scan and compaction are one
+  // ballot; with more running requests a fused release measured slower)
+  *fuse = !REC_EV(I) && !REC_SM(I) && R <= W && kev >= 1 && kev <= budget && kc == kev && ku > kev &&
+          ks > kev;
   return k > 0 ? k : 0;
 }
 
@@ -2294,12 +2262,12 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k, bool fuse = false) {
   const double af = (double)((I.general_cap - I.free_total) + I.reserved_used) / (double)I.capacity;
   const int64_t wt0 = I.written_total;
   const double cap = (double)I.capacity;
-  if (fuse) {  // the k quiet iterations and the completing one (quiet_span's fuse)
-    const int64_t j = quiet_steps_fused(I, k + 1, fs, dt, clk1, af, wt0, cap);
-    if (j == k + 1) complete_fused(I);  // an arrival cut-off leaves the event to a normal step
+  if (!REC_SM(I)) {  // one inlined replay serves both: k quiet iterations (+ the fused completing one)
+    const int64_t kk = k + (fuse ? 1 : 0);
+    const int64_t j = quiet_steps_fused(I, kk, fs, dt, clk1, af, wt0, cap);
+    if (fuse && j == kk) complete_fused(I);  // an arrival cut-off leaves the event to a normal step
     return j;
   }
-  if (!I.record_samples) return quiet_steps_fused(I, k, fs, dt, clk1, af, wt0, cap);
   // pass 1 (every lane, identical arithmetic): the sequential clock chain and
   // the arrival cut-off — ingest would admit an arrival at the next step.
   double clock = I.clock;
@@ -2316,7 +2284,7 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k, bool fuse = false) {
   // pass 2: per-iteration written fractions computed lane-parallel, summed in
   // sample order (metrics.hpp:153-162) so the FP sums match the reference.
   double aw = I.agg_written, aa = I.agg_allocated;
-  if (I.record_samples) {
+  if (REC_SM(I)) {
     if (LANE == 0) {
       double c = I.clock;
       for (int64_t j = 0; j < k; ++j) {
@@ -2364,7 +2332,7 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k, bool fuse = false) {
   }
   UNI(I.iter += k; I.steps += k; I.executed += k; I.agg_fs += fs * k;
         if ((double)fs >= 0.95 * (double)I.tfs) I.agg_tfs_hits += k;
-        I.hist[0] += k; if (I.record_samples) I.sm_n += k;
+        I.hist[0] += k; if (REC_SM(I)) I.sm_n += k;
         I.quiet_steps += k; I.quiet_spans++);
   return k;
 }
@@ -2379,7 +2347,7 @@ EDEVNI void engine_step(Inst& I) {  // Engine::step (engine.hpp:104-116)
   [[maybe_unused]] const int64_t t1 = PHASE_NOW();
   Tok fs = 0;
   for (int32_t i = LANE; i < I.n_ptiter; i += W) fs += I.ptiter_tok[i];
-  fs = wsum(fs) + ((B && I.decode_pause) ? 0 : I.R);
+  fs = wsum32((int32_t)fs) + ((B && I.decode_pause) ? 0 : I.R);
   if (fs == 0) handle_idle(I); else execute_iteration<B>(I, fs);
   PHASE_ADD(10, PHASE_NOW() - t1);
   UNI(I.steps++);

@@ -177,8 +177,8 @@ EDEVNI void engine_steps(Inst& I, int64_t max_steps, int64_t deadline_ns = 0) {
   for (int64_t s = 0; s < max_steps;) {
     if (I.error || I.completed >= I.n) break;
     if (deadline_ns && now_ns() >= deadline_ns) break;
-    if ((I.record_events && I.ev_n + step_event_bound(I) > I.ev_cap) ||
-        (I.record_samples && I.sm_n + 1 > I.sm_cap)) {
+    if ((REC_EV(I) && I.ev_n + step_event_bound(I) > I.ev_cap) ||
+        (REC_SM(I) && I.sm_n + 1 > I.sm_cap)) {
       LANE0(I.status = STATUS_DRAIN);
       break;
     }

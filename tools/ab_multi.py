@@ -58,7 +58,10 @@ def main():
     ap.add_argument("--launches", type=int, default=10)
     ap.add_argument("--check", type=int, default=8)
     ap.add_argument("--check-step", type=int, default=3002)
+    ap.add_argument("--workload", default=bench.WORKLOAD)
+    ap.add_argument("--full-run", default="", help="also time one whole single-engine run of this config per lib")
     a = ap.parse_args()
+    bench.WORKLOAD = a.workload
     traces = bench.make_traces(generate_trace, a.n, [1000 + i for i in range(a.instances)], pinned=True)
     ref_dig = None
     for r in range(a.rounds):
@@ -67,6 +70,18 @@ def main():
             ms, rps, its, tot, dig = one(lib, traces, a.slice_us, a.launches, a.check, a.check_step)
             ref_dig = ref_dig or dig
             nsteps = max(1, tot[5])
+            if a.full_run:
+                import time
+                from paper_2411_06364_b200 import abi, workloads as W
+                from paper_2411_06364_b200.engine import Engine
+                c = W.CONFIGS[a.full_run]
+                o = abi.default_options(**c["opts"])
+                o.record_events = 0
+                o.record_samples = 0
+                t = W.make_trace(a.full_run, generate_trace)
+                t0 = time.perf_counter()
+                Engine(t, o, device=0, lib=lib).run()
+                print(f"   {x}: whole {a.full_run} run {time.perf_counter() - t0:.3f} s", flush=True)
             print(f"round {r} {x}: {1e3 * ms:.1f} us/launch {rps / 1e6:.2f}M req/s  iters {its}  "
                   f"normal steps {tot[5]} at {tot[2] / nsteps:.0f} cyc, spans {tot[4]} test {tot[0] / max(1, tot[4]):.0f} "
                   f"replay {tot[1] / max(1, its):.1f} cyc/iter  state@{a.check_step} "
