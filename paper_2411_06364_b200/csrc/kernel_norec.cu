@@ -1,0 +1,28 @@
+// kernel_norec.cu — the econoserve step kernel compiled with ECONO_NOREC:
+// every event- and sample-recording path of engine.cuh is removed at compile
+// time (REC_EV / REC_SM are constant false), so the code the warps execute is
+// smaller and denser in the instruction cache. econo_batch launches it for
+// batches in which no instance records events or samples (the bench path);
+// the results are those of k_engine_steps for the same batch (the recording
+// paths only append to the logs).
+#define ECONO_NOREC 1
+#include "steps.cuh"
+
+#include <cuda_runtime.h>
+
+using namespace econo;
+
+__global__ void __launch_bounds__(32) k_engine_steps_norec(Inst* insts, int64_t max_steps, int64_t slice_ns) {
+  if (insts[blockIdx.x].base) return;  // a baseline-policy instance (k_baseline_steps)
+  const int64_t deadline = slice_ns > 0 ? now_ns() + slice_ns : 0;
+  __shared__ Inst I;
+  const int64_t t0 = PROF_NOW();
+  inst_load(I, &insts[blockIdx.x]);
+  engine_steps<false>(I, steps_for(I, max_steps), deadline);
+  LANE0(I.prof[11] += PROF_NOW() - t0; I.prof[12]++);
+  inst_store(&insts[blockIdx.x], I);
+}
+
+void launch_engine_steps_norec(Inst* insts, unsigned n_inst, int64_t max_steps, int64_t slice_ns, cudaStream_t s) {
+  k_engine_steps_norec<<<n_inst, 32, 0, s>>>(insts, max_steps, slice_ns);
+}

@@ -24,6 +24,13 @@
 #include <vector>
 
 #include "engine.cuh"
+#include "steps.cuh"
+#if !defined(ECONO_HOSTSIM)
+#include <cuda_runtime.h>
+// kernel_norec.cu: the step kernel without recording code
+void launch_engine_steps_norec(econo::Inst* insts, unsigned n_inst, int64_t max_steps, int64_t slice_ns,
+                               cudaStream_t s);
+#endif
 
 #ifndef ECONO_HOSTSIM
 #include <cuda_runtime.h>
@@ -139,69 +146,6 @@ EDEV void init_finish(Inst& I, int64_t first_bad) {
   I.grp_free_top = I.grp_cap;
   I.sl_free_top = I.slot_cap;
   I.next_group_id = 1;
-}
-
-// Engine::run()'s loop body, up to max_steps times (engine.hpp:118-122).
-// The quiet-span test is only worth running after a normal step that
-// completed nothing: a replay always stops right before an event step (or at
-// the budget), and a step after a completion finds freed KVC for the GT
-// queue head. Skipping the test is always exact — it only decides whether a
-// replay may stand in for normal steps.
-// Device wall clock (ns), for time-sliced launches. Read by lane 0 and
-// broadcast, so every break decision taken on it is warp-uniform by
-// construction (the step body's full-mask shuffles and ballots need that).
-// Call from warp-converged code only.
-EDEV int64_t now_ns() {
-#ifdef __CUDA_ARCH__
-  uint64_t t = 0;
-  if ((threadIdx.x & 31) == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return (int64_t)__shfl_sync(0xffffffffu, t, 0);
-#else
-  return 0;
-#endif
-}
-
-// max_steps < 0 encodes an absolute target (econo_batch_launch_to): advance
-// until Engine::step() has been called -max_steps times in total.
-EDEV int64_t steps_for(const Inst& I, int64_t max_steps) {
-  return max_steps >= 0 ? max_steps : (-max_steps > I.steps ? -max_steps - I.steps : 0);
-}
-
-// deadline_ns > 0 (a time-sliced launch, econo_batch_launch_slice): stop at
-// the first step boundary past the deadline; every instance then advances as
-// far as the slice allows instead of all waiting for the slowest one.
-template <bool B>
-EDEVNI void engine_steps(Inst& I, int64_t max_steps, int64_t deadline_ns = 0) {
-  LANE0(I.status = STATUS_RUN);
-  bool test = true;
-  for (int64_t s = 0; s < max_steps;) {
-    if (I.error || I.completed >= I.n) break;
-    if (deadline_ns && now_ns() >= deadline_ns) break;
-    if ((REC_EV(I) && I.ev_n + step_event_bound(I) > I.ev_cap) ||
-        (REC_SM(I) && I.sm_n + 1 > I.sm_cap)) {
-      LANE0(I.status = STATUS_DRAIN);
-      break;
-    }
-    if (!B && I.skip && test) {
-      const int64_t t0 = PROF_NOW();
-      bool fuse = false;
-      const int64_t k = quiet_span(I, max_steps - s, &fuse);
-      const int64_t t1 = PROF_NOW();
-      LANE0(I.prof[0] += t1 - t0);
-      if (k > 0 || fuse) {
-        s += quiet_steps(I, k, fuse);
-        LANE0(I.prof[1] += PROF_NOW() - t1; I.prof[4]++);
-        test = false;
-        continue;
-      }
-    }
-    const int64_t t2 = PROF_NOW();
-    const int64_t c0 = I.completed;
-    engine_step<B>(I);
-    LANE0(I.prof[2] += PROF_NOW() - t2; I.prof[5]++);
-    test = I.completed == c0;
-    ++s;
-  }
 }
 
 // finalize() per-request records (engine.hpp:963-984), one lane per request.
@@ -322,20 +266,6 @@ EHD uint32_t key_digit(uint64_t k, int consumed, int dbits) {
 }  // namespace econo
 
 #ifndef ECONO_HOSTSIM
-// Inst staged in shared memory for the launch; one warp per instance.
-__device__ __forceinline__ void inst_load(Inst& s, const Inst* g) {
-  const uint64_t* src = reinterpret_cast<const uint64_t*>(g);
-  uint64_t* dst = reinterpret_cast<uint64_t*>(&s);
-  for (int i = threadIdx.x; i < (int)(sizeof(Inst) / 8); i += 32) dst[i] = src[i];
-  __syncwarp();
-}
-__device__ __forceinline__ void inst_store(Inst* g, const Inst& s) {
-  __syncwarp();
-  const uint64_t* src = reinterpret_cast<const uint64_t*>(&s);
-  uint64_t* dst = reinterpret_cast<uint64_t*>(g);
-  for (int i = threadIdx.x; i < (int)(sizeof(Inst) / 8); i += 32) dst[i] = src[i];
-}
-
 // Per-instance init scratch: [0] first out-of-order arrival, [1] prompt sum,
 // [2] first infeasible request.
 __global__ void __launch_bounds__(256) k_init_soa(Inst* insts, const EconoTraceRecord* const* traces,
@@ -1437,6 +1367,7 @@ struct econo_batch {
   size_t bulk_bytes = 0;
   int64_t keys_total = 0;
   int64_t n_base = 0;  // baseline-policy instances (k_baseline_steps)
+  bool norec = false;  // no instance records events or samples: k_engine_steps_norec
   // trace staging buffers, kept until destroy: a cudaFree right after the
   // upload stalls for up to ~0.3 s next to a nearly full HBM (measured)
   void* stage[2] = {nullptr, nullptr};
@@ -1560,8 +1491,10 @@ void launch_steps(econo_batch* b, int64_t max_steps, void* stream, int64_t slice
   push_descs(b);
 #else
   cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
-  if (b->n_base < (int64_t)b->inst.size())
-    k_engine_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
+  if (b->n_base < (int64_t)b->inst.size()) {
+    if (b->norec) launch_engine_steps_norec(b->d_insts, (unsigned)b->inst.size(), max_steps, slice_ns, s);
+    else k_engine_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
+  }
   if (b->n_base > 0) k_baseline_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
   if (s != b->stream) {  // order the handle's stream after these launches
     cudaEventRecord(b->launched, s);
@@ -1895,12 +1828,14 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
         return rcs[(size_t)i];
       }
   }
+  b->norec = true;
   for (int32_t i = 0; i < n_inst; ++i) {
     HostInst& h = b->inst[(size_t)i];
     h.seed = opts[i].seed;
     h.pred_seed = opts[i].pred_seed;
     h.policy = opts[i].policy;
     b->n_base += h.desc.base;
+    if (!h.desc.base && (h.desc.record_events || h.desc.record_samples)) b->norec = false;
     size_t bytes = 0;
     layout(h.desc, nullptr, &bytes);
     h.arena_bytes = (bytes + 4095) & ~size_t(4095);
