@@ -102,7 +102,7 @@ static inline uint64_t umulhi64(uint64_t a, uint64_t b) {
 #endif
 
 // Event / sample recording switches. A translation unit compiled with
-// ECONO_NOREC (csrc/kernel_norec.cu) gets a copy of the step loop with every
+// ECONO_NOREC (csrc/kernel_fast.cu) gets a copy of the step loop with every
 // recording path removed at compile time; the runtime launches it for
 // batches that record nothing (the bench path), the generic copy otherwise.
 #ifdef ECONO_NOREC
@@ -111,6 +111,16 @@ static inline uint64_t umulhi64(uint64_t a, uint64_t b) {
 #else
 #define REC_EV(I) ((I).record_events != 0)
 #define REC_SM(I) ((I).record_samples != 0)
+#endif
+// The same translation unit is specialised for the ordered PT queue (class
+// lists + bitmaps; econoserve-sdo/-full): the FIFO min-tree paths drop out.
+// (ordered implies GT grouping: econoserve-sdo and -full both group.)
+#ifdef ECONO_SPEC_ORDERED
+#define ORD(I) true
+#define GRP(I) true
+#else
+#define ORD(I) ((I).ordered != 0)
+#define GRP(I) ((I).grouping != 0)
 #endif
 
 #define LANE0(stmt) \
@@ -948,7 +958,7 @@ EDEVNI void kvc_release(Inst& I, int32_t id) {
 // GT queue (queues.hpp:125-204)
 // ------------------------------------------------------------------------
 EDEV uint64_t gkey_hi(const Inst& I, int32_t g) {
-  if (!I.ordered) return 0;
+  if (!ORD(I)) return 0;
   return ((uint64_t)I.gr_db[g] << 56) | ((uint64_t)(255 - I.gr_kb[g]) << 48) |
          (0xFFFFFFFFFFFFULL - (uint64_t)I.gr_rl[g]);
 }
@@ -988,7 +998,7 @@ EDEV void gq_erase(Inst& I, int32_t g) {
   UNI(I.G--);
 }
 EDEV void gq_rekey(Inst& I, int32_t g, double now) {  // place(): make_key (queues.hpp:187-193), lane 0
-  if (I.ordered) {
+  if (ORD(I)) {
     I.gr_db[g] = bucket_d(I, dmax(0.0, I.gr_mindl[g] - now));
     I.gr_kb[g] = bucket_k(I, I.gr_maxocc[g]);
   }
@@ -1003,7 +1013,7 @@ EDEV int32_t rl_find(const Inst& I, int32_t rl) {
   return -1;
 }
 EDEV void rl_set(Inst& I, int32_t rl, int32_t g) {  // lane 0
-  if (I.grouping && rl >= 0 && rl < I.rl_cap) I.rl_map[rl] = g;
+  if (GRP(I) && rl >= 0 && rl < I.rl_cap) I.rl_map[rl] = g;
 }
 EDEV void gq_remove_at(Inst& I, int32_t pos) {  // drops the group from the queue and frees it
   const int32_t g = I.gq[pos];
@@ -1022,7 +1032,7 @@ EDEV Tok member_demand(const Inst& I, int32_t id) {  // gt_member_demand (engine
 EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline, int32_t occ, double now,
                             Tok d) {
   UNI(I.gt_next[id] = -1);
-  if (I.grouping) {
+  if (GRP(I)) {
     const int32_t g = rl_find(I, padded);
     if (g >= 0) {
       // place() (queues.hpp:187-193) re-keys the group and re-inserts it at
@@ -1036,8 +1046,8 @@ EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline
       const double md = I.gr_mindl[g];
       const double nmd = dmin(md, deadline);
       const int32_t nmo = (int32_t)tmax(mo, occ);
-      const int32_t ndb = I.ordered ? bucket_d(I, dmax(0.0, nmd - now)) : odb;
-      const int32_t nkb = I.ordered ? bucket_k(I, nmo) : okb;
+      const int32_t ndb = ORD(I) ? bucket_d(I, dmax(0.0, nmd - now)) : odb;
+      const int32_t nkb = ORD(I) ? bucket_k(I, nmo) : okb;
       const bool moved = ndb != odb || nkb != okb;
       if (moved) gq_erase(I, g);  // before the key fields change
       {  // warp-uniform (every lane, same values)
@@ -1063,8 +1073,8 @@ EDEVNI void group_insert_gt(Inst& I, int32_t id, int32_t padded, double deadline
         I.gr_hd[g] = (int32_t)d;
         I.gr_cnt[g] = 1; I.gr_dem[g] = d; I.gr_formed[g] = now; I.gr_mindl[g] = deadline;
         I.gr_maxocc[g] = occ; I.gr_seq[g] = I.gt_next_seq++;
-        I.gr_db[g] = I.ordered ? bucket_d(I, dmax(0.0, deadline - now)) : 0;
-        I.gr_kb[g] = I.ordered ? bucket_k(I, occ) : 0;
+        I.gr_db[g] = ORD(I) ? bucket_d(I, dmax(0.0, deadline - now)) : 0;
+        I.gr_kb[g] = ORD(I) ? bucket_k(I, occ) : 0;
         rl_set(I, padded, g));
   gq_insert(I, g);
 }
@@ -1142,7 +1152,7 @@ EDEVNI void ingest(Inst& I) {
     pm = wmin(pm);
     UNI(if (pm < I.pt_min_lb) I.pt_min_lb = pm);
   }
-  if (!B && I.ordered) {
+  if (!B && ORD(I)) {
     // class append in id order: peers of a class inside each warp chunk link
     // to each other; the lowest links to the class tail, the highest becomes it.
     for (int64_t base = first; base < last; base += W) {
@@ -1635,7 +1645,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
     bool adm = false;
     int adm_b = -1, adm_p = -1;  // the first bucket with a fitting class, and that class
     if (C0 >= 1 && C0 >= I.pt_min_lb) {
-      if (I.ordered) {
+      if (ORD(I)) {
         for (int b = 0; b < I.nbuckets; ++b) {
           const int p = bm_prev(I, b, C0);
           if (p >= 1) { adm_b = b; adm_p = p; break; }
@@ -1652,7 +1662,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
       Tok C = C0;  // both budgets drop by p: take iff p <= min(budgets)
       if (!adm) {
         // nothing fits (the admittable probe above used the same bound)
-      } else if (I.ordered) {
+      } else if (ORD(I)) {
         // buckets before adm_b hold nothing <= C0, and adm_b's first probe at
         // C0 is the admittable probe's answer; once the budget is below the
         // smallest queued prompt (pt_min_lb) nothing further can fit
@@ -1685,7 +1695,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
       }
     }
     if (npt == 0 && I.pt_count > 0 && I.R == 0) {  // starvation guard (engine.hpp:314-323)
-      if (I.ordered) {
+      if (ORD(I)) {
         for (int b = 0; b < I.nbuckets; ++b) {
           const int p = bm_prev(I, b, rfree);
           if (p >= 1) { npt = cls_take(I, b, p, 1, I.tmp_a, npt); break; }
@@ -2095,7 +2105,7 @@ EDEVNI int64_t quiet_span(Inst& I, int64_t budget, bool* fuse) {
   const Tok C0 = tmin(I.tfs - (Tok)R, I.reserve_cap - I.reserved_used);
   if (C0 >= 1 && I.pt_count > 0 && C0 >= I.pt_min_lb) {  // queues.hpp:279-299 would take a PT
     bool fit = false;
-    if (I.ordered) {
+    if (ORD(I)) {
       for (int b = 0; b < I.nbuckets && !fit; ++b) fit = bm_prev(I, b, C0) >= 1;
     } else {
       fit = I.tree[I.tree_off[I.tree_levels - 1]] <= C0;

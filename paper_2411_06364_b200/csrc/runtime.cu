@@ -27,8 +27,8 @@
 #include "steps.cuh"
 #if !defined(ECONO_HOSTSIM)
 #include <cuda_runtime.h>
-// kernel_norec.cu: the step kernel without recording code
-void launch_engine_steps_norec(econo::Inst* insts, unsigned n_inst, int64_t max_steps, int64_t slice_ns,
+// kernel_fast.cu: the step kernel specialised for non-recording, ordered-queue batches
+void launch_engine_steps_fast(econo::Inst* insts, unsigned n_inst, int64_t max_steps, int64_t slice_ns,
                                cudaStream_t s);
 #endif
 
@@ -1367,7 +1367,7 @@ struct econo_batch {
   size_t bulk_bytes = 0;
   int64_t keys_total = 0;
   int64_t n_base = 0;  // baseline-policy instances (k_baseline_steps)
-  bool norec = false;  // no instance records events or samples: k_engine_steps_norec
+  bool fast = false;  // no recording and ordered PT queues in every econoserve instance: k_engine_steps_fast
   // trace staging buffers, kept until destroy: a cudaFree right after the
   // upload stalls for up to ~0.3 s next to a nearly full HBM (measured)
   void* stage[2] = {nullptr, nullptr};
@@ -1492,7 +1492,7 @@ void launch_steps(econo_batch* b, int64_t max_steps, void* stream, int64_t slice
 #else
   cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
   if (b->n_base < (int64_t)b->inst.size()) {
-    if (b->norec) launch_engine_steps_norec(b->d_insts, (unsigned)b->inst.size(), max_steps, slice_ns, s);
+    if (b->fast) launch_engine_steps_fast(b->d_insts, (unsigned)b->inst.size(), max_steps, slice_ns, s);
     else k_engine_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
   }
   if (b->n_base > 0) k_baseline_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
@@ -1828,14 +1828,14 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
         return rcs[(size_t)i];
       }
   }
-  b->norec = true;
+  b->fast = true;
   for (int32_t i = 0; i < n_inst; ++i) {
     HostInst& h = b->inst[(size_t)i];
     h.seed = opts[i].seed;
     h.pred_seed = opts[i].pred_seed;
     h.policy = opts[i].policy;
     b->n_base += h.desc.base;
-    if (!h.desc.base && (h.desc.record_events || h.desc.record_samples)) b->norec = false;
+    if (!h.desc.base && (h.desc.record_events || h.desc.record_samples || !h.desc.ordered)) b->fast = false;
     size_t bytes = 0;
     layout(h.desc, nullptr, &bytes);
     h.arena_bytes = (bytes + 4095) & ~size_t(4095);

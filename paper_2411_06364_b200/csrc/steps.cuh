@@ -1,8 +1,7 @@
 // steps.cuh — the per-instance step loop (Engine::run()'s body) and the
 // shared-memory staging of an instance, shared by the two translation units
 // that instantiate the step kernel: runtime.cu (every configuration) and
-// kernel_norec.cu (compiled with ECONO_NOREC: no event/sample recording code,
-// launched for batches that record nothing).
+// kernel_fast.cu (specialised at compile time: no recording, ordered PT queue).
 #pragma once
 #include "engine.cuh"
 
