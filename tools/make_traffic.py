@@ -29,7 +29,7 @@ def main():
             continue
         per[int(r[I])][r[M]] = float(r[V].replace(",", ""))
         names[int(r[I])] = r[K].split("(")[0]
-    ids = [i for i in sorted(per) if names[i] == "k_engine_steps"][-a.launches:]
+    ids = [i for i in sorted(per) if names[i].startswith("k_engine_steps")][-a.launches:]  # generic or specialised
     dram = [per[i].get("dram__bytes_read.sum", 0) + per[i].get("dram__bytes_write.sum", 0) for i in ids]
     ns = [per[i]["gpu__time_duration.sum"] for i in ids]
     out = {"kernel": "k_engine_steps",
