@@ -114,6 +114,16 @@ static inline uint64_t umulhi64(uint64_t a, uint64_t b) {
 #endif
 // The same translation unit is specialised for the ordered PT queue (class
 // lists + bitmaps; econoserve-sdo/-full): the FIFO min-tree paths drop out.
+// ECONO_SPEC_ORACLE_FULL: econoserve-full with the oracle predictor (the
+// bench configuration): the noisy predictors' code and the non-pipelining
+// branch drop out as well.
+#ifdef ECONO_SPEC_ORACLE_FULL
+#define PRED_ORACLE(I) true
+#define FULL(I) true
+#else
+#define PRED_ORACLE(I) ((I).pred_model == ECONO_PRED_ORACLE)
+#define FULL(I) ((I).full != 0)
+#endif
 // (ordered implies GT grouping: econoserve-sdo and -full both group.)
 #ifdef ECONO_SPEC_ORDERED
 #define ORD(I) true
@@ -482,7 +492,7 @@ EDEV Tok llround_glibc(double v) {
 }
 // predict_rl (workload.hpp:228-264)
 EDEV Tok predict_rl(const Inst& I, Tok true_rl, uint64_t* x, int32_t& idx) {
-  if (I.pred_model == ECONO_PRED_ORACLE) return quantize_up(true_rl, I.pred_quantum);
+  if (PRED_ORACLE(I)) return quantize_up(true_rl, I.pred_quantum);
   if (I.pred_model == ECONO_PRED_LOGNORMAL) {
     const double v = (double)true_rl * econo_libm::exp(normal_fresh(x, idx, I.pred_sigma));  // glibc's exp
     return quantize_up(tmax(1, llround_glibc(v)), I.pred_quantum);
@@ -1580,7 +1590,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
   [[maybe_unused]] const int64_t tp1 = PHASE_NOW();
   PHASE_ADD(7, tp1 - tp0);
   // ---- KVC pipelining (econoserve-full, engine.hpp:273-297) ----
-  if (I.full && nselg > 0) {
+  if (FULL(I) && nselg > 0) {
     int32_t nm = 0;  // host members flattened into tmp_b/tmp_c, group bounds in tmp_a
     for (int32_t gi = 0; gi < nselg; ++gi) {
       {  // warp-uniform (every lane, same values)

@@ -9,13 +9,17 @@
 // k_engine_steps for the same batch.
 #define ECONO_NOREC 1
 #define ECONO_SPEC_ORDERED 1
+#ifndef FAST_KERNEL  // kernel_fast_oracle.cu includes this file with its own names
+#define FAST_KERNEL k_engine_steps_fast
+#define FAST_LAUNCH launch_engine_steps_fast
+#endif
 #include "steps.cuh"
 
 #include <cuda_runtime.h>
 
 using namespace econo;
 
-__global__ void __launch_bounds__(32) k_engine_steps_fast(Inst* insts, int64_t max_steps, int64_t slice_ns) {
+__global__ void __launch_bounds__(32) FAST_KERNEL(Inst* insts, int64_t max_steps, int64_t slice_ns) {
   if (insts[blockIdx.x].base) return;  // a baseline-policy instance (k_baseline_steps)
   const int64_t deadline = slice_ns > 0 ? now_ns() + slice_ns : 0;
   __shared__ Inst I;
@@ -26,6 +30,6 @@ __global__ void __launch_bounds__(32) k_engine_steps_fast(Inst* insts, int64_t m
   inst_store(&insts[blockIdx.x], I);
 }
 
-void launch_engine_steps_fast(Inst* insts, unsigned n_inst, int64_t max_steps, int64_t slice_ns, cudaStream_t s) {
-  k_engine_steps_fast<<<n_inst, 32, 0, s>>>(insts, max_steps, slice_ns);
+void FAST_LAUNCH(Inst* insts, unsigned n_inst, int64_t max_steps, int64_t slice_ns, cudaStream_t s) {
+  FAST_KERNEL<<<n_inst, 32, 0, s>>>(insts, max_steps, slice_ns);
 }

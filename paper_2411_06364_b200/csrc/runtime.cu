@@ -27,9 +27,12 @@
 #include "steps.cuh"
 #if !defined(ECONO_HOSTSIM)
 #include <cuda_runtime.h>
-// kernel_fast.cu: the step kernel specialised for non-recording, ordered-queue batches
+// kernel_fast.cu: the step kernel specialised for non-recording, ordered-queue batches;
+// kernel_fast_oracle.cu: the same for econoserve-full with the oracle predictor
 void launch_engine_steps_fast(econo::Inst* insts, unsigned n_inst, int64_t max_steps, int64_t slice_ns,
-                               cudaStream_t s);
+                              cudaStream_t s);
+void launch_engine_steps_fast_oracle(econo::Inst* insts, unsigned n_inst, int64_t max_steps, int64_t slice_ns,
+                                     cudaStream_t s);
 #endif
 
 #ifndef ECONO_HOSTSIM
@@ -1368,6 +1371,7 @@ struct econo_batch {
   int64_t keys_total = 0;
   int64_t n_base = 0;  // baseline-policy instances (k_baseline_steps)
   bool fast = false;  // no recording and ordered PT queues in every econoserve instance: k_engine_steps_fast
+  bool fast_oracle = false;  // ... and every one econoserve-full with the oracle predictor
   // trace staging buffers, kept until destroy: a cudaFree right after the
   // upload stalls for up to ~0.3 s next to a nearly full HBM (measured)
   void* stage[2] = {nullptr, nullptr};
@@ -1492,7 +1496,8 @@ void launch_steps(econo_batch* b, int64_t max_steps, void* stream, int64_t slice
 #else
   cudaStream_t s = stream ? (cudaStream_t)stream : b->stream;
   if (b->n_base < (int64_t)b->inst.size()) {
-    if (b->fast) launch_engine_steps_fast(b->d_insts, (unsigned)b->inst.size(), max_steps, slice_ns, s);
+    if (b->fast_oracle) launch_engine_steps_fast_oracle(b->d_insts, (unsigned)b->inst.size(), max_steps, slice_ns, s);
+    else if (b->fast) launch_engine_steps_fast(b->d_insts, (unsigned)b->inst.size(), max_steps, slice_ns, s);
     else k_engine_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
   }
   if (b->n_base > 0) k_baseline_steps<<<(unsigned)b->inst.size(), 32, 0, s>>>(b->d_insts, max_steps, slice_ns);
@@ -1829,6 +1834,7 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
       }
   }
   b->fast = true;
+  b->fast_oracle = true;
   for (int32_t i = 0; i < n_inst; ++i) {
     HostInst& h = b->inst[(size_t)i];
     h.seed = opts[i].seed;
@@ -1836,12 +1842,14 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     h.policy = opts[i].policy;
     b->n_base += h.desc.base;
     if (!h.desc.base && (h.desc.record_events || h.desc.record_samples || !h.desc.ordered)) b->fast = false;
+    if (!h.desc.base && (!h.desc.full || h.desc.pred_model != ECONO_PRED_ORACLE)) b->fast_oracle = false;
     size_t bytes = 0;
     layout(h.desc, nullptr, &bytes);
     h.arena_bytes = (bytes + 4095) & ~size_t(4095);
     seeds[2 * i] = opts[i].seed;
     seeds[2 * i + 1] = opts[i].pred_seed;
   }
+  b->fast_oracle = b->fast_oracle && b->fast;
 #ifndef ECONO_HOSTSIM
   {  // reserve the burst-ingest scratch now, before the arenas fill the GPU:
      // a late cudaMalloc next to a nearly full HBM is slow (~0.5 s measured)
