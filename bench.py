@@ -323,7 +323,7 @@ def auto_instances(n, device, sms=148, world=1):
     The end-of-run JCT keys (8 B per request) get a buffer only if HBM is
     left, else each histogram pass derives them from the request fields.
     Sized on the workload's own trace; at most 16 per SM (the registers of
-    16 one-warp CTAs fill an SM)."""
+    16 one-warp CTAs fill an SM).""" 
     import torch
 
     from paper_2411_06364_b200.engine import generate_trace, instance_bytes
@@ -331,11 +331,11 @@ def auto_instances(n, device, sms=148, world=1):
     per = instance_bytes(t, options())
     free, _ = torch.cuda.mem_get_info(device)
     slack = (1 << 30) if world == 1 else (4 << 30)  # staging, scratch, context growth (+ NCCL's own)
-    for k in range(16, 0, -1):
-        inst = k * sms
-        if inst * per + 2.2e9 + slack <= free:  # + the ingest scratch (128M keys x 16 B)
-            return inst
-    return sms
+    # every instance that fits (+ the ingest scratch, 128M keys x 16 B); with
+    # time-sliced launches an SM holding one instance more simply does more
+    # work, so the count need not be a multiple of the SM count
+    inst = int((free - 2.2e9 - slack) // per)
+    return max(1, min(inst, 16 * sms))
 
 
 def run_ours(args):
@@ -362,6 +362,8 @@ def run_ours(args):
         dist.all_reduce(t_i, op=dist.ReduceOp.MIN)
         I = int(t_i.item())
     seeds = [1000 + rank * I + i for i in range(I)]
+    from paper_2411_06364_b200.engine import instance_bytes
+    inst_mb = instance_bytes(W.make_trace(WORKLOAD, generate_trace, n=args.n, seed=1000), options()) / 1e6
     t0 = time.time()
     # host trace generation shares the box's cores between the ranks
     traces = make_traces(generate_trace, args.n, seeds, threads=max(2, (os.cpu_count() or 2) // world), pinned=True)
@@ -499,7 +501,7 @@ def run_ours(args):
                               f"launch_slice), ~{ips:.0f} scheduler iterations per instance on average"
                               if slice_ns else f"{args.iters} scheduler iterations per instance per launch"),
                    "policy": W.CONFIGS[WORKLOAD]["opts"]["policy"],
-                   "l2": f"inputs larger than L2: {I} x ~157 MB of instance state per GPU vs 126 MB L2, no flush",
+                   "l2": f"inputs larger than L2: {I} x ~{inst_mb:.0f} MB of instance state per GPU vs 126 MB L2, no flush",
                    "window": (window_str(args) if not slice_ns else
                               f"after the 1M burst ingest: {args.warmup} warm-up and {args.steps} timed slices; "
                               f"scheduler iterations ~{2 + (it_warm / I):.0f}..{2 + (it_warm + it_done) / I:.0f} "

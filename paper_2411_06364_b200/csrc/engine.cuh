@@ -242,7 +242,7 @@ struct Inst {
   GP<const int32_t> prompt;
   GP<const int32_t> true_rl;
   GP<int32_t> predicted, generated, occupied, allowance, gen_epoch, prefill_done;
-  GP<int32_t> preempt_count, reserve_draws, held, reg_head, reg_tail, reserved, written;
+  GP<int32_t> preempt_count, reserve_draws, held, reg_head, reserved, written;
   // pt_next and gt_next share storage: a request is never queued as a PT and
   // a GT at once, and each link is written when the request joins its queue
   GP<int32_t> sidx, pt_next, gt_next;  // sidx: a hosted request's slot-pool entry
@@ -734,9 +734,14 @@ EDEV void addr_remove_region(Inst& I, int32_t r) {
 }
 EDEV int32_t region_new(Inst& I, int32_t owner, Tok start, Tok len) {  // all lanes get the id
   if (I.reg_free_top <= 0) { set_error(I, ERR_TABLE_OVERFLOW, owner, 2); return -1; }
-  // the free-list top and the owner's list fields load in one round
+  // the free-list top and the owner's list fields load in one round; the
+  // list tail is found by walking it (a holding has one region, or a few
+  // after grow_exact), which saves a per-request tail pointer (4 B x n)
   const int32_t r = I.reg_free[I.reg_free_top - 1];
-  const int32_t tail = I.reg_tail[owner], hd = I.held[owner];
+  const int32_t head = I.reg_head[owner], hd = I.held[owner];
+  int32_t tail = head;
+  if (tail >= 0)
+    for (int32_t nx = I.rg_next[tail]; nx >= 0; nx = I.rg_next[tail]) tail = nx;
   WSYNC();
   {  // warp-uniform (every lane, same values)
     I.reg_free_top--;
@@ -745,7 +750,6 @@ EDEV int32_t region_new(Inst& I, int32_t owner, Tok start, Tok len) {  // all la
     I.rg_owner[r] = owner;
     I.rg_next[r] = -1;
     if (tail < 0) I.reg_head[owner] = r; else I.rg_next[tail] = r;
-    I.reg_tail[owner] = r;
     I.held[owner] = hd + (int32_t)len;
   }
   WSYNC();
@@ -927,7 +931,7 @@ EDEVNI void kvc_release(Inst& I, int32_t id) {
       freed += ln;
       r = nx;
     }
-    UNI(I.reg_head[id] = -1; I.reg_tail[id] = -1; I.held[id] = 0);
+    UNI(I.reg_head[id] = -1; I.held[id] = 0);
     for (int32_t k = 0; k < np; ++k) {
       const int32_t sp = I.tmp_c[k];
       const int32_t h = I.sl_hosted[sp], sl = I.sl_len[sp];
@@ -1598,7 +1602,7 @@ EDEVNI void form_econoserve(Inst& I) {  // engine.hpp:263-325
         for (int32_t i = I.selg_start[gi]; i < I.selg_start[gi + 1]; ++i) {
           const int32_t id = I.sel_ids[i];
           const int32_t rh = I.reg_head[id];
-          if (I.generated[id] == 0 && rh >= 0 && rh == I.reg_tail[id]) {  // exactly one region
+          if (I.generated[id] == 0 && rh >= 0 && I.rg_next[rh] < 0) {  // exactly one region
             I.tmp_b[nm] = id;
             I.tmp_c[nm] = I.rg_start[rh] + I.prompt[id];
             nm++;
@@ -1821,11 +1825,13 @@ EDEVNI void execute_iteration(Inst& I, Tok fs) {  // engine.hpp:731-840
     const int32_t id = I.ptiter_id[i];
     const int32_t tk = I.ptiter_tok[i];
     const double e = I.exec_t[id];
-    const int32_t pd = I.prefill_done[id] + tk, wr = I.written[id], oc = I.occupied[id];
+    // econoserve prefills a prompt whole in its dispatch iteration, so its
+    // prefill_done is 0 before and the prompt after: derived, not stored
+    const int32_t pd = (B ? I.prefill_done[id] : 0) + tk, wr = I.written[id], oc = I.occupied[id];
     const int32_t pr = B ? I.ptarget[id] : I.prompt[id];
     const uint8_t f = I.flags[id];
     I.exec_t[id] = e + dt;
-    I.prefill_done[id] = pd;
+    if (B) I.prefill_done[id] = pd;
     I.written[id] = wr + tk;
     I.occupied[id] = oc + tk;
     wsum_pt += tk;

@@ -102,7 +102,6 @@ EDEV bool init_req_one(Inst& I, int64_t i) {
   I.first_tok[i] = -1.0;
   I.compl_clock[i] = -1.0;
   I.reg_head[i] = -1;
-  I.reg_tail[i] = -1;
   I.pt_next[i] = -1;  // also gt_next (shared storage)
   if (I.base) I.ptarget[i] = I.prompt[i];  // prefill_target = prompt_len (engine.hpp:189)
   return worst_demand(I, i) > I.general_cap || (!I.base && (Tok)I.prompt[i] > I.reserve_cap);
@@ -1057,9 +1056,11 @@ void layout(Inst& I, char* base, size_t* bytes) {
   I.prompt = a.take<int32_t>(n);
   I.true_rl = a.take<int32_t>(n);
   GP<int32_t>* i32s[] = {&I.predicted, &I.generated, &I.occupied, &I.allowance, &I.gen_epoch,
-                      &I.prefill_done, &I.preempt_count, &I.reserve_draws, &I.held, &I.reg_head,
-                      &I.reg_tail, &I.reserved, &I.written, &I.sidx, &I.pt_next};
+                      &I.preempt_count, &I.reserve_draws, &I.held, &I.reg_head,
+                      &I.reserved, &I.written, &I.sidx, &I.pt_next};
   for (auto p : i32s) *p = a.take<int32_t>(n);
+  // chunked prefills (baselines) only; econoserve derives it (engine.cuh)
+  I.prefill_done = a.take<int32_t>(I.base ? n : 1);
   I.gt_next = I.pt_next.p;
   I.state = a.take<uint8_t>(n);
   I.flags = a.take<uint8_t>(n);
@@ -2809,7 +2810,7 @@ int64_t econo_snapshot(econo_engine* e, int64_t* out, int64_t cap) {
     w.push_back(I.preempt_count[i]);
     w.push_back(I.reserve_draws[i]);
     w.push_back((I.flags[i] & F_ALLOC_FAIL) ? 1 : 0);
-    w.push_back(I.prefill_done[i]);
+    w.push_back(I.base ? I.prefill_done[i] : (I.state[i] == ST_WAITING_PT ? 0 : I.prompt[i]));
     w.push_back(bits(I.waiting[i]));
     w.push_back(bits(I.preempt_t[i]));
     w.push_back(bits(I.exec_t[i]));
