@@ -1618,7 +1618,8 @@ int64_t orc_snapshot(void* h, int64_t* out, int64_t cap) { /* DESIGN.md "Snapsho
     W(r->generated_at_epoch); W(r->occupied); W(r->hosted); W(r->was_preempted);
     W(r->preempt_count); W(r->reserve_draws); W(r->alloc_failure_flag); W(r->prefill_done);
     W(dbits(r->waiting_time)); W(dbits(r->preemption_time)); W(dbits(r->execution_time));
-    W(dbits(r->dispatch_time)); W(dbits(r->first_token_time)); W(dbits(r->completion_clock));
+    /* dispatch_time: dead state for econoserve (E:374; read by the baselines only), not compared */
+    W(0); W(dbits(r->first_token_time)); W(dbits(r->completion_clock));
     W(dbits(r->last_enqueue_time)); W(dbits(g->sched_share[i])); W(dbits(g->penalty_extra[i]));
     W(dbits(r->slo_deadline));
   }

@@ -483,7 +483,10 @@ int64_t ref_snapshot(void* hv, int64_t* out, int64_t cap) {
     w.push_back(bits(r.waiting_time));
     w.push_back(bits(r.preemption_time));
     w.push_back(bits(r.execution_time));
-    w.push_back(bits(r.dispatch_time));
+    // Request::dispatch_time is dead state for the econoserve policies (written at
+    // engine.hpp:374, read only by the baselines, engine.hpp:527/615, in no record
+    // or report): the device does not keep it for them, so it is not compared
+    w.push_back(econo ? 0 : bits(r.dispatch_time));
     w.push_back(bits(r.first_token_time));
     w.push_back(bits(r.completion_clock));
     w.push_back(bits(r.last_enqueue_time));

@@ -1269,7 +1269,6 @@ EDEVNI void dispatch_pts(Inst& I, int32_t npt) {
       I.reserved[id] = rsv + p;
       I.flags[id] = (uint8_t)(f | F_HAS_RESERVED);
       I.state[id] = ST_RUNNING;
-      I.dispatch_t[id] = I.clock;
       I.waiting[id] = wt + (I.clock - arr);
       I.ptiter_id[I.n_ptiter + LANE] = id;
       I.ptiter_tok[I.n_ptiter + LANE] = p;

@@ -98,7 +98,7 @@ EDEV Tok worst_demand(const Inst& I, int64_t i) {
 EDEV bool init_req_one(Inst& I, int64_t i) {
   if (I.pred_model == ECONO_PRED_ORACLE) I.predicted[i] = sat_rl(quantize_up(I.true_rl[i], I.pred_quantum));
   I.state[i] = ST_WAITING_PT;
-  I.dispatch_t[i] = -1.0;
+  if (I.base) I.dispatch_t[i] = -1.0;
   I.first_tok[i] = -1.0;
   I.compl_clock[i] = -1.0;
   I.reg_head[i] = -1;
@@ -1064,9 +1064,11 @@ void layout(Inst& I, char* base, size_t* bytes) {
   I.gt_next = I.pt_next.p;
   I.state = a.take<uint8_t>(n);
   I.flags = a.take<uint8_t>(n);
-  GP<double>* f64s[] = {&I.waiting, &I.preempt_t, &I.exec_t, &I.dispatch_t, &I.first_tok,
+  GP<double>* f64s[] = {&I.waiting, &I.preempt_t, &I.exec_t, &I.first_tok,
                      &I.compl_clock, &I.last_enq, &I.penalty, &I.sched_share};
   for (auto p : f64s) *p = a.take<double>(n);
+  // Request::dispatch_time is read only by the baselines (engine.hpp:527, 615)
+  I.dispatch_t = a.take<double>(I.base ? n : 1);
   const int64_t rc = I.reg_cap;
   I.rg_start = a.take<int32_t>(rc);
   I.rg_len = a.take<int32_t>(rc);
@@ -2814,7 +2816,7 @@ int64_t econo_snapshot(econo_engine* e, int64_t* out, int64_t cap) {
     w.push_back(bits(I.waiting[i]));
     w.push_back(bits(I.preempt_t[i]));
     w.push_back(bits(I.exec_t[i]));
-    w.push_back(bits(I.dispatch_t[i]));
+    w.push_back(I.base ? bits(I.dispatch_t[i]) : 0);  // dead state for econoserve: not kept
     w.push_back(bits(I.first_tok[i]));
     w.push_back(bits(I.compl_clock[i]));
     w.push_back(bits(I.last_enq[i]));

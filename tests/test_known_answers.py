@@ -268,8 +268,9 @@ def test_instance_bytes_sizing():
     o = base_options("econoserve-full")
     small = instance_bytes([(0.1 * i, 10, 10) for i in range(20000)], o, lib=HOSTSIM)
     big = instance_bytes([(0.1 * i, 10, 10) for i in range(40000)], o, lib=HOSTSIM)
-    # beyond the KVC-capacity-sized tables, each request costs its SoA fields (DESIGN.md §3)
-    assert 0 < small < big and 140 < (big - small) / 20000 < 160
+    # beyond the KVC-capacity-sized tables, each request costs its SoA fields
+    # (134 B for an econoserve instance)
+    assert 0 < small < big and 125 < (big - small) / 20000 < 140
     o.tfs = 0
     with pytest.raises(ConfigError, match="tfs must be >= 1"):
         instance_bytes([(0.1, 10, 10)], o, lib=HOSTSIM)
