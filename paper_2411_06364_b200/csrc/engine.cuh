@@ -2174,58 +2174,13 @@ EDEV void quiet_request(Inst& I, int32_t id, double e, int64_t k, double clk1) {
 // in ONE loop, so the k-step span costs ~k dependent DADDs instead of one
 // pass per chain. The per-iteration written fractions are computed W at a
 // time across lanes and broadcast (shuffles are off the dependency chain).
-// The fused event iteration's completions (execute_iteration, engine.hpp:
-// 784-791): the replay already ran its decode progress, clock and sample
-// sums; the requests that reached true_rl (mfin, over the running set that
-// fits one warp: quiet_span's fuse gate) complete in running order exactly as
-// in the running-set pass. Under-predictions and slot deadlines cannot occur
-// here (quiet_span's fuse test).
-EDEVNI void complete_fused(Inst& I, int32_t my, unsigned mfin) {
-  const unsigned keep = BALLOT(my >= 0 && !((mfin >> LANE) & 1u));
-  unsigned m = mfin;
-  WSYNC();
-  while (m) {
-    const int l = FFS(m);
-    m &= m - 1;
-    const int32_t cid = shfl(my, l);
-    UNI(I.state[cid] = ST_DONE; I.compl_clock[cid] = I.clock);
-    kvc_release(I, cid);
-    if (I.error) return;
-    UNI(I.occupied[cid] = 0; I.completed++);
-    logev(I, ECONO_EV_COMPLETE, cid, I.generated[cid], 0);
-    WSYNC();
-  }
-  if ((keep >> LANE) & 1u) I.run[POPC(keep & LANEMASK_LT)] = my;
-  WSYNC();
-  UNI(I.R = POPC(keep));
-}
-
-// The replay without per-iteration samples (the bench path): every chain the
-// reference advances once per iteration — clock, the in-order sample sums of
-// metrics.hpp:153-162, and each running request's execution_time — advances
-// in ONE loop, so the k-step span costs ~k dependent DADDs instead of one
-// pass per chain. The per-iteration written fractions are computed W at a
-// time across lanes and broadcast (shuffles are off the dependency chain).
-// The first W running requests' fields load before the chain, so their
-// latency hides under it. With fuse, the k-th iteration is the fused
-// completion event (quiet_span) and runs complete_fused when it is reached.
 EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double clk1, double af,
-                                 int64_t wt0, double cap, bool fuse) {
+                                 int64_t wt0, double cap) {
   const bool has_arr = I.arrival_cursor < I.n;
   const double ta = has_arr ? I.arrival[I.arrival_cursor] : 0.0;
   const int32_t R = I.R;
-  const int64_t kk = k;
   const int32_t my = LANE < R ? I.run[LANE] : -1;
-  double e = 0.0, ft = 0.0;
-  int32_t g0 = 0, oc = 0, wr = 0, tr = 0;
-  if (my >= 0) {
-    e = I.exec_t[my];
-    g0 = I.generated[my];
-    oc = I.occupied[my];
-    wr = I.written[my];
-    ft = I.first_tok[my];
-    tr = I.true_rl[my];
-  }
+  double e = my >= 0 ? I.exec_t[my] : 0.0;
   double clock = I.clock, aw = I.agg_written, aa = I.agg_allocated;
   int64_t j = 0;
   if (!has_arr) {
@@ -2265,31 +2220,64 @@ EDEVNI int64_t quiet_steps_fused(Inst& I, int64_t k, Tok fs, double dt, double c
     }
   }
   k = j;
-  if (my >= 0) {  // quiet_request from the preloaded fields
-    I.exec_t[my] = e;
-    if (g0 == 0 && ft < 0.0) I.first_tok[my] = clk1;
-    I.generated[my] = g0 + (int32_t)k;
-    I.occupied[my] = oc + (int32_t)k;
-    I.written[my] = wr + (int32_t)k;
-  }
+  if (my >= 0) quiet_request(I, my, e, k, clk1);
   for (int32_t i = W + LANE; i < R; i += W) {
     const int32_t id = I.run[i];
     double e2 = I.exec_t[id];
     for (int64_t t = 0; t < k; ++t) e2 += dt;
     quiet_request(I, id, e2, k, clk1);
   }
-  // a fused completion event reached (an arrival cut-off leaves it to a normal step)
-  const bool fused = fuse && k == kk;
-  const unsigned mfin = BALLOT(fused && my >= 0 && g0 + (int32_t)k >= tr);
-  const int32_t ev = fused ? 1 : 0, c = POPC(mfin);
   WSYNC();
   UNI(I.clock = clock; I.written_total = wt0 + k * fs; I.agg_written = aw; I.agg_allocated = aa;
         I.iter += k; I.steps += k; I.executed += k; I.agg_fs += fs * k;
         if ((double)fs >= 0.95 * (double)I.tfs) I.agg_tfs_hits += k;
-        I.hist[0] += k - ev; if (fused) I.hist[c < I.hist_cap ? c : I.hist_cap - 1]++;
-        I.quiet_steps += k - ev; I.quiet_spans++);
-  if (fused) complete_fused(I, my, mfin);
+        I.hist[0] += k; I.quiet_steps += k; I.quiet_spans++);
   return k;
+}
+
+// The fused event iteration's completions (execute_iteration, engine.hpp:
+// 784-791): the replay already ran its decode progress, clock and sample
+// sums; the requests that reached true_rl complete in running order, exactly
+// as in the running-set pass, and the iteration moves from hist[0] to its
+// completion count. Under-predictions and slot deadlines cannot occur here
+// (quiet_span's fuse test).
+EDEVNI void complete_fused(Inst& I) {
+  const int32_t R0 = I.R;
+  int32_t completed_now = 0;
+  int32_t id_c0 = -1;
+  unsigned keep0 = 0;
+  for (int32_t base = 0; base < R0; base += W) {
+    const int32_t i = base + LANE;
+    const int32_t id = i < R0 ? I.run[i] : -1;
+    const bool fin = id >= 0 && I.generated[id] >= I.true_rl[id];
+    if (base == 0) {
+      id_c0 = id;
+      keep0 = BALLOT(id >= 0 && !fin);
+    }
+    unsigned m = BALLOT(fin);
+    WSYNC();
+    while (m) {
+      const int l = FFS(m);
+      m &= m - 1;
+      const int32_t cid = shfl(id, l);
+      UNI(I.state[cid] = ST_DONE; I.compl_clock[cid] = I.clock);
+      kvc_release(I, cid);
+      if (I.error) return;
+      UNI(I.occupied[cid] = 0; I.completed++);
+      logev(I, ECONO_EV_COMPLETE, cid, I.generated[cid], 0);
+      WSYNC();
+      completed_now++;
+    }
+  }
+  if (R0 <= W) {
+    if ((keep0 >> LANE) & 1u) I.run[POPC(keep0 & LANEMASK_LT)] = id_c0;
+    WSYNC();
+    UNI(I.R = POPC(keep0));
+  } else {
+    run_compact(I);
+  }
+  UNI(I.hist[0]--; I.hist[completed_now < I.hist_cap ? completed_now : I.hist_cap - 1]++;
+      I.quiet_steps--);
 }
 
 EDEVNI int64_t quiet_steps(Inst& I, int64_t k, bool fuse = false) {
@@ -2299,8 +2287,12 @@ EDEVNI int64_t quiet_steps(Inst& I, int64_t k, bool fuse = false) {
   const double af = (double)((I.general_cap - I.free_total) + I.reserved_used) / (double)I.capacity;
   const int64_t wt0 = I.written_total;
   const double cap = (double)I.capacity;
-  if (!REC_SM(I))  // one inlined replay serves both: k quiet iterations (+ the fused completing one)
-    return quiet_steps_fused(I, k + (fuse ? 1 : 0), fs, dt, clk1, af, wt0, cap, fuse);
+  if (!REC_SM(I)) {  // one inlined replay serves both: k quiet iterations (+ the fused completing one)
+    const int64_t kk = k + (fuse ? 1 : 0);
+    const int64_t j = quiet_steps_fused(I, kk, fs, dt, clk1, af, wt0, cap);
+    if (fuse && j == kk) complete_fused(I);  // an arrival cut-off leaves the event to a normal step
+    return j;
+  }
   // pass 1 (every lane, identical arithmetic): the sequential clock chain and
   // the arrival cut-off — ingest would admit an arrival at the next step.
   double clock = I.clock;
