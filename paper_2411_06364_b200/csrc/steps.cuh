@@ -19,8 +19,8 @@ namespace econo {
 // Call from warp-converged code only.
 EDEV int64_t now_ns() {
 #ifdef __CUDA_ARCH__
-  uint64_t t = 0;
-  if ((threadIdx.x & 31) == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  uint64_t t;  // every lane reads (no divergent branch); lane 0's value is the one used
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return (int64_t)__shfl_sync(0xffffffffu, t, 0);
 #else
   return 0;
@@ -53,10 +53,10 @@ EDEVNI void engine_steps(Inst& I, int64_t max_steps, int64_t deadline_ns = 0) {
       bool fuse = false;
       const int64_t k = quiet_span(I, max_steps - s, &fuse);
       const int64_t t1 = PROF_NOW();
-      LANE0(I.prof[0] += t1 - t0);
+      UNI(I.prof[0] += t1 - t0);  // counters: any lane's clock delta will do (no divergence)
       if (k > 0 || fuse) {
         s += quiet_steps(I, k, fuse);
-        LANE0(I.prof[1] += PROF_NOW() - t1; I.prof[4]++);
+        UNI(I.prof[1] += PROF_NOW() - t1; I.prof[4]++);
         test = false;
         continue;
       }
@@ -64,7 +64,7 @@ EDEVNI void engine_steps(Inst& I, int64_t max_steps, int64_t deadline_ns = 0) {
     const int64_t t2 = PROF_NOW();
     const int64_t c0 = I.completed;
     engine_step<B>(I);
-    LANE0(I.prof[2] += PROF_NOW() - t2; I.prof[5]++);
+    UNI(I.prof[2] += PROF_NOW() - t2; I.prof[5]++);
     test = I.completed == c0;
     ++s;
   }
