@@ -203,6 +203,7 @@ struct Inst {
   int32_t nbd, nbk, record_events, record_samples, skip, _pad1;
   int32_t pmax, nbuckets, bm_words, bm_l2;    // PT class table (ordered mode)
   int32_t tree_levels, rl_cap;
+  int32_t tr_pmin, tr_pmax, tr_rmin, tr_rmax;  // trace prompt / response length ranges (device init; burst-ingest class window)
   int32_t tree_off[8], tree_len[8];            // 32-ary min tree (FIFO mode)
   int32_t reg_cap, grp_cap, slot_cap, run_cap, ptiter_cap, adm_cap, scr_cap, hist_cap, sel_cap, _pad2;
   int64_t tfs, capacity, block, reserve_cap, general_cap, pred_quantum;

@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(256) k_init_soa(Inst* insts, const EconoTraceR
   unsigned long long* sc = scr + 4 * ii;
   int64_t psum = 0;
   long long bad = LLONG_MAX, lbad = LLONG_MAX;
+  int32_t pmn = INT32_MAX, pmx = 0, rmn = INT32_MAX, rmx = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I.n; i += (int64_t)gridDim.x * blockDim.x) {
     bool ob, lb;
     int64_t p;
@@ -285,6 +286,25 @@ __global__ void __launch_bounds__(256) k_init_soa(Inst* insts, const EconoTraceR
     psum += p;
     if (ob && i < bad) bad = i;
     if (lb && i < lbad) lbad = i;
+    if (!lb) {
+      const int32_t pp = (int32_t)p, rr = (int32_t)tr[i].true_rl;
+      pmn = pp < pmn ? pp : pmn;
+      pmx = pp > pmx ? pp : pmx;
+      rmn = rr < rmn ? rr : rmn;
+      rmx = rr > rmx ? rr : rmx;
+    }
+  }
+  pmn = __reduce_min_sync(0xffffffffu, pmn);
+  pmx = __reduce_max_sync(0xffffffffu, pmx);
+  rmn = __reduce_min_sync(0xffffffffu, rmn);
+  rmx = __reduce_max_sync(0xffffffffu, rmx);
+  if ((threadIdx.x & 31) == 0) {
+    if (pmn < INT32_MAX) {
+      atomicMin(&I.tr_pmin, pmn);
+      atomicMax(&I.tr_pmax, pmx);
+      atomicMin(&I.tr_rmin, rmn);
+      atomicMax(&I.tr_rmax, rmx);
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     psum += __shfl_xor_sync(0xffffffffu, psum, o);
@@ -402,6 +422,9 @@ struct BulkJob {
   int64_t first, k, off, hoff;   // arrivals [first, first+k); key offset; histogram offset
   unsigned long long minp;       // min prompt of the batch
   unsigned long long bcnt[ECONO_MAX_BOUNDS + 2];
+  int32_t wb0, wnb, wp0, wnp;    // k_ingest_ranges: class window buckets [wb0, wb0+wnb) x prompts [wp0, wp0+wnp)
+  int32_t werr;                  // set when an arrival falls outside the window (k_ingest_stitch<true> reports it)
+  int32_t sstride;               // segment slots per tile/range: a range holds at most one segment per class of its window
 };
 constexpr int kBulkTile = 4096;
 constexpr int64_t kBulkBudget = (int64_t)128 << 20;  // keys per ingest group (4 x 4 B of temp each: 2 GB)
@@ -810,7 +833,206 @@ __global__ void __launch_bounds__(256) k_ingest_tiles(Inst* insts, BulkJob* jobs
   if (threadIdx.x < ECONO_MAX_BOUNDS + 2 && sb[threadIdx.x]) atomicAdd(&J.bcnt[threadIdx.x], sb[threadIdx.x]);
 }
 
+// ---------------------------------------------------------------------------
+// Burst ingest by range scans (the default when the class table fits shared
+// memory): no sort at all. One warp owns a range of kRangeI ids and walks it
+// from the last 32-id chunk to the first with a per-class table in shared
+// memory, tab[c] = (arrivals of class c seen so far in the range) << 16 |
+// (local index of the earliest of them). For each chunk:
+//   succ(id) = the next lane of the same class (__match_any_sync peers), else
+//              the class's earliest id in the later chunks (tab), else -1;
+//   pt_next[id] = succ (one coalesced 128-byte store per chunk);
+//   the chunk's lowest lane of each class becomes the class's earliest id.
+// A class seen for the first time has its range-last id in that chunk: it
+// gets a segment record (appended warp-aggregated) that the end of the range
+// completes with the class's first id and count from tab. The stitch then
+// links the ranges exactly as it links the tiles of k_ingest_tiles.
+// The table covers only the job's class window (k_bulk_plan: the deadline
+// buckets the batch's slack range can reach x the trace's prompt range; at
+// cfg3 one bucket x 655 prompts = 2.6 KB), so shared memory does not bound
+// the warps per SM, and a range holds at most one segment per window class.
+// HBM traffic per arrival: 16 B read (arrival, true_rl, prompt) + 4 B written
+// (pt_next) + the segment records (8 B written and re-read per class present
+// in a range: < 1 B per arrival at cfg3's class spread).
+// ---------------------------------------------------------------------------
+constexpr int kRangeI = 32768;
+constexpr int kRangeU = 8;   // chunks whose fields are loaded before they are scanned
+EDEV uint64_t rseg_pack(uint32_t c, uint32_t f, uint32_t l, uint32_t n) {
+  return ((uint64_t)c << 48) | ((uint64_t)f << 32) | ((uint64_t)l << 16) | (uint64_t)n;
+}
+
+// J.tiles: ranges; J.off: the job's first range * kRangeI in `segs`; J.hoff: its first range in `nseg`.
+// Dynamic shared memory: 4 B x window classes. WB >= the bits of a window
+// class index (the ballot count of the multisplit; compile-time: no branches).
+template <int WB>
+__global__ void __launch_bounds__(32) k_ingest_ranges(Inst* insts, BulkJob* jobs, uint64_t* segs, int32_t* nseg) {
+  BulkJob& J = jobs[blockIdx.y];
+  if ((int)blockIdx.x >= J.tiles) return;
+  Inst& I = insts[J.inst];
+  extern __shared__ uint32_t rtab[];
+  const int lane = threadIdx.x;
+  const uint32_t pm1 = (uint32_t)I.pmax + 1;
+  // the table covers the job's class window only (k_bulk_plan): t = (b - wb0) * wnp + (p - wp0)
+  const int wb0 = J.wb0, wp0 = J.wp0, wnp = J.wnp, wn = J.wnb * J.wnp;
+  for (int c = lane; c < wn; c += 32) rtab[c] = 0;
+  const int64_t r0 = (int64_t)blockIdx.x * kRangeI;
+  const int n = (int)(J.k - r0 < kRangeI ? J.k - r0 : kRangeI);
+  const int64_t gbase = J.first + r0;  // global id of local index 0
+  const int32_t g32 = (int32_t)gbase;  // ids < 2^31
+  // the bucket_d / slo_of operands in registers (same operations as engine.cuh)
+  const double now = I.clock, scale = I.slo_scale, tp = I.t_p, tg = I.t_g;
+  const int nbd = I.nbd;
+  __shared__ double sdb[ECONO_MAX_BOUNDS];
+  if (lane < ECONO_MAX_BOUNDS) sdb[lane] = I.dbounds[lane];
+  __syncwarp();  // the zeroed table and the bounds, visible to every lane
+  const double* A = I.arrival.p + gbase;
+  const int32_t* P = I.prompt.p + gbase;
+  const int32_t* RL = I.true_rl.p + gbase;
+  int32_t* NX = I.pt_next.p + gbase;
+  uint64_t* out = segs + J.off + (int64_t)blockIdx.x * J.sstride;
+  const unsigned below = (1u << lane) - 1u, above = ~((2u << lane) - 1u);
+  int ns = 0;  // segment records appended (warp-uniform)
+  bool werr = false;
+  // PT classes of a group of arrivals: (deadline bucket of max(0, slo - clock),
+  // prompt). bucket_d's "first bound the slack is below" as a warp-uniform
+  // loop over the bounds (highest first), every arrival of the group at once.
+  auto classes = [&](const double* a, const int32_t* p, const int32_t* r, uint32_t* cc, const bool* val) {
+    double sl[kRangeU];
+    uint32_t b[kRangeU];
+#pragma unroll
+    for (int u = 0; u < kRangeU; ++u) {
+      sl[u] = dmax(0.0, (a[u] + scale * (tp + tg * (double)r[u])) - now);
+      b[u] = (uint32_t)nbd;
+    }
+#pragma unroll 1
+    for (int q = nbd - 1; q >= 0; --q) {
+      const double d = sdb[q];
+#pragma unroll
+      for (int u = 0; u < kRangeU; ++u) b[u] = sl[u] < d ? (uint32_t)q : b[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kRangeU; ++u) {
+      const uint32_t t = (b[u] - (uint32_t)wb0) * (uint32_t)wnp + (uint32_t)(p[u] - wp0);
+      // outside the window (impossible by k_bulk_plan's bound): flagged, kept inside the table
+      if (val[u] && t >= (uint32_t)wn) werr = true;
+      cc[u] = t < (uint32_t)wn ? t : 0u;
+    }
+  };
+  // the lanes of a chunk holding the same window class c (v: the lane holds
+  // an arrival). WB > 0: a warp multisplit, one ballot per class bit;
+  // WB == 0: __match_any_sync (it serialises over the ~30 distinct classes
+  // of a chunk). Computed for a whole group before its serial scan (ILP).
+  auto peers_of = [&](uint32_t c, bool v) -> unsigned {
+    if (WB == 0) return __match_any_sync(0xffffffffu, v ? c : 0xFFFFFFFFu);
+    unsigned d = __ballot_sync(0xffffffffu, v);  // lanes whose validity or some class bit differs
+    d = v ? ~d : d;
+#pragma unroll
+    for (int i = 0; i < (WB > 0 ? WB : 1); ++i) {
+      unsigned bb;
+      asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
+          "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}"
+          : "=r"(bb) : "r"(c), "r"(1u << i));
+      const unsigned m = (c & (1u << i)) ? 0xFFFFFFFFu : 0u;
+      d |= bb ^ m;
+    }
+    return ~d;
+  };
+  // one 32-id chunk of the backward scan: chunk k, nx = &pt_next[this lane's id]
+  auto scan = [&](int k, uint32_t c, bool v, int32_t* nx, unsigned peers) {
+    const int e = k * 32 + lane;
+    const uint32_t T = v ? rtab[c] : 0u;
+    const unsigned up = peers & above;
+    const int32_t succ = up ? g32 + (k * 32 + __ffs(up) - 1) : (T ? g32 + (int32_t)(T & 0xFFFFu) : -1);
+    if (v) __stcs(nx, succ);
+    __syncwarp();
+    if (v && (peers & below) == 0u) rtab[c] = (((T >> 16) + (uint32_t)__popc(peers)) << 16) | (uint32_t)e;
+    const bool fresh = v && T == 0u && up == 0u;  // the range's last id of a class seen for the first time
+    const unsigned fb = __ballot_sync(0xffffffffu, fresh);
+    if (fresh) out[ns + __popc(fb & below)] = rseg_pack(c, 0, (uint32_t)e, 0);
+    ns += __popc(fb);
+    __syncwarp();
+  };
+  const int nch = (n + 31) >> 5;
+  const int g0 = nch % kRangeU ? nch % kRangeU : kRangeU;  // chunks in the top group
+  {  // the top group: possibly fewer chunks, its top chunk possibly partial (checked path)
+    double a[kRangeU];
+    int32_t p[kRangeU], r[kRangeU];
+    uint32_t cc[kRangeU];
+    bool val[kRangeU];
+#pragma unroll
+    for (int u = 0; u < kRangeU; ++u) {
+      const int e = (nch - 1 - u) * 32 + lane;
+      const bool v = u < g0 && e < n;
+      val[u] = v;
+      a[u] = v ? __ldcs(A + e) : 0.0;
+      p[u] = v ? __ldcs(P + e) : 0;
+      r[u] = v ? __ldcs(RL + e) : 0;
+    }
+    classes(a, p, r, cc, val);
+#pragma unroll
+    for (int u = 0; u < kRangeU; ++u) {
+      const int e = (nch - 1 - u) * 32 + lane;
+      if (u < g0) scan(nch - 1 - u, e < n ? cc[u] : 0xFFFFFFFFu, e < n, NX + e, peers_of(cc[u], e < n));
+    }
+  }
+  // full groups of kRangeU chunks below it, each loaded one group ahead of its
+  // scan so that the HBM latency overlaps the scan; per-lane pointers with
+  // constant per-chunk offsets (no 64-bit index arithmetic per access)
+  int k0 = nch - 1 - g0;
+  if (k0 >= 0) {
+    double a[kRangeU], a2[kRangeU];
+    int32_t p[kRangeU], r[kRangeU], p2[kRangeU], r2[kRangeU];
+    auto load = [&](int kt, double* AA, int32_t* PP, int32_t* RR) {
+      const int e = kt * 32 + lane;
+      const double* pa = A + e;
+      const int32_t* pp = P + e;
+      const int32_t* pr = RL + e;
+#pragma unroll
+      for (int u = 0; u < kRangeU; ++u) {
+        AA[u] = __ldcs(pa - 32 * u);
+        PP[u] = __ldcs(pp - 32 * u);
+        RR[u] = __ldcs(pr - 32 * u);
+      }
+    };
+    auto group = [&](int kt, const double* AA, const int32_t* PP, const int32_t* RR) {
+      uint32_t cc[kRangeU];
+      bool val[kRangeU];
+#pragma unroll
+      for (int u = 0; u < kRangeU; ++u) val[u] = true;
+      classes(AA, PP, RR, cc, val);
+      int32_t* nx = NX + (kt * 32 + lane);
+      unsigned pe[kRangeU];
+#pragma unroll
+      for (int u = 0; u < kRangeU; ++u) pe[u] = peers_of(cc[u], true);
+#pragma unroll
+      for (int u = 0; u < kRangeU; ++u) scan(kt - u, cc[u], true, nx - 32 * u, pe[u]);
+    };
+    load(k0, a, p, r);
+    for (;;) {  // two groups per trip: the buffers swap roles without register moves
+      if (k0 >= kRangeU) load(k0 - kRangeU, a2, p2, r2);
+      group(k0, a, p, r);
+      if ((k0 -= kRangeU) < 0) break;
+      if (k0 >= kRangeU) load(k0 - kRangeU, a, p, r);
+      group(k0, a2, p2, r2);
+      if ((k0 -= kRangeU) < 0) break;
+    }
+  }
+  __syncwarp();
+  for (int q = lane; q < ns; q += 32) {  // complete the records: global class, first id and count
+    const uint64_t s = out[q];
+    const uint32_t t = (uint32_t)(s >> 48), T = rtab[t];
+    const uint32_t c = ((uint32_t)wb0 + t / (uint32_t)wnp) * pm1 + (uint32_t)wp0 + t % (uint32_t)wnp;
+    out[q] = rseg_pack(c, T & 0xFFFFu, (uint32_t)(s >> 16) & 0xFFFFu, T >> 16);
+  }
+  if (lane == 0) nseg[J.hoff + blockIdx.x] = ns;
+  if (__any_sync(0xffffffffu, werr) && lane == 0) atomicExch(&J.werr, 1);
+  // the batch's bucket counts and smallest prompt come from the class counts (k_ingest_stitch<true>)
+}
+
 // One CTA per job; dynamic shared memory: 3 x ncls int32 (+ bucket sums).
+// RANGES: the segments of k_ingest_ranges (rseg_pack, kRangeI ids per range),
+// else those of k_ingest_tiles (seg_pack, kTileI ids per tile).
+template <bool RANGES>
 __global__ void __launch_bounds__(512) k_ingest_stitch(Inst* insts, const BulkJob* jobs, const uint64_t* segs,
                                                        const int32_t* nseg) {
   const BulkJob& J = jobs[blockIdx.x];
@@ -825,23 +1047,46 @@ __global__ void __launch_bounds__(512) k_ingest_stitch(Inst* insts, const BulkJo
     cnt[c] = 0;
   }
   __syncthreads();
+  constexpr int64_t span = RANGES ? kRangeI : kTileI;
   for (int t = J.tiles - 1; t >= 0; --t) {
     const int ns = nseg[J.hoff + t];
-    const int64_t base = J.first + (int64_t)t * kTileI;
+    const int64_t base = J.first + (int64_t)t * span;
     for (int q = threadIdx.x; q < ns; q += blockDim.x) {
-      const uint64_t pk = segs[J.off + (int64_t)t * kTileI + q];
-      const int c = (int)(pk >> 37);
-      const int32_t gf = (int32_t)(base + ((pk >> 25) & 4095)), gl = (int32_t)(base + ((pk >> 13) & 4095));
+      const uint64_t pk = segs[J.off + (int64_t)t * J.sstride + q];
+      int c;
+      int32_t gf, gl, m;
+      if (RANGES) {
+        c = (int)(pk >> 48);
+        gf = (int32_t)(base + ((pk >> 32) & 0xFFFF));
+        gl = (int32_t)(base + ((pk >> 16) & 0xFFFF));
+        m = (int32_t)(pk & 0xFFFF);
+      } else {
+        c = (int)(pk >> 37);
+        gf = (int32_t)(base + ((pk >> 25) & 4095));
+        gl = (int32_t)(base + ((pk >> 13) & 4095));
+        m = (int32_t)(pk & 8191);
+      }
       const int32_t nx = first[c];
       if (nx >= 0) I.pt_next[gl] = nx; else tail[c] = gl;
       first[c] = gf;
-      cnt[c] += (int32_t)(pk & 8191);
+      cnt[c] += m;
     }
     __syncthreads();
   }
   const int pm1 = I.pmax + 1;
+  __shared__ int32_t sbc[ECONO_MAX_BOUNDS + 2];  // RANGES: bucket counts and the smallest prompt, from the class counts
+  __shared__ int32_t smin;
+  if (RANGES) {
+    if (threadIdx.x < ECONO_MAX_BOUNDS + 2) sbc[threadIdx.x] = 0;
+    if (threadIdx.x == 0) smin = INT32_MAX;
+    __syncthreads();
+  }
   for (int c = threadIdx.x; c < ncls; c += blockDim.x) {
     if (cnt[c] == 0) continue;
+    if (RANGES) {
+      atomicAdd(&sbc[c / pm1], cnt[c]);
+      atomicMin(&smin, c % pm1);
+    }
     const int32_t old_tail = I.cls_tail[c];
     if (old_tail >= 0) I.pt_next[old_tail] = first[c]; else I.cls_head[c] = first[c];
     I.cls_tail[c] = tail[c];
@@ -853,11 +1098,21 @@ __global__ void __launch_bounds__(512) k_ingest_stitch(Inst* insts, const BulkJo
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // the ingest scalars (k_bulk_finish)
+    if (RANGES && J.werr && !I.error) {  // an arrival outside k_bulk_plan's class window
+      I.error = ERR_TABLE_OVERFLOW;
+      I.err_val = 99;
+      I.err_id = (int32_t)J.first;
+    }
     I.arrival_cursor = J.first + J.k;
     I.pt_count += (int32_t)J.k;
     I.ev_total += J.k;
-    if ((int64_t)J.minp < I.pt_min_lb) I.pt_min_lb = (int64_t)J.minp;
-    for (int b = 0; b < I.nbuckets; ++b) I.bcnt[b] += (int32_t)J.bcnt[b];
+    if (RANGES) {
+      if ((int64_t)smin < I.pt_min_lb) I.pt_min_lb = (int64_t)smin;
+      for (int b = 0; b < I.nbuckets; ++b) I.bcnt[b] += sbc[b];
+    } else {
+      if ((int64_t)J.minp < I.pt_min_lb) I.pt_min_lb = (int64_t)J.minp;
+      for (int b = 0; b < I.nbuckets; ++b) I.bcnt[b] += (int32_t)J.bcnt[b];
+    }
   }
 }
 
@@ -873,6 +1128,15 @@ __global__ void k_bulk_finish(Inst* insts, const BulkJob* jobs) {
   for (int b = 0; b < I.nbuckets; ++b) I.bcnt[b] += (int32_t)J.bcnt[b];
 }
 // Per instance: the arrivals ingest() would admit at the current clock.
+// Per instance: the arrivals ingest() would admit at the current clock
+// (plan[4i], plan[4i+1]) and the window of PT classes they can fall in
+// (plan[4i+2]: buckets lo | hi << 32, plan[4i+3]: prompts lo | hi << 32).
+// slack = max(0, arrival + slo_scale * (t_p + t_g * rl) - clock) is monotone
+// in the arrival and in rl separately (IEEE operations round monotonically),
+// and bucket_d is monotone in the slack, so the buckets at the four corners
+// of [first arrival, last arrival] x [min rl, max rl] bound every arrival's
+// bucket; the prompts lie in the trace's range. Anything non-finite: the
+// whole class table.
 __global__ void k_bulk_plan(const Inst* insts, int64_t* plan) {
   const Inst& I = insts[blockIdx.x];
   if (threadIdx.x != 0) return;
@@ -888,8 +1152,32 @@ __global__ void k_bulk_plan(const Inst* insts, int64_t* plan) {
       k = lo - first;
     }
   }
-  plan[2 * blockIdx.x] = first;
-  plan[2 * blockIdx.x + 1] = k;
+  int64_t blo = 0, bhi = I.nbd, plo = 1, phi = I.pmax;
+  if (k > 0 && I.tr_pmin <= I.tr_pmax && I.tr_rmin <= I.tr_rmax) {
+    const double as[2] = {I.arrival[first], I.arrival[first + k - 1]};
+    const int32_t rs[2] = {I.tr_rmin, I.tr_rmax};
+    bool finite = true;
+    int64_t mn = I.nbd, mx = 0;
+    for (int x = 0; x < 2; ++x)
+      for (int y = 0; y < 2; ++y) {
+        const double v = (as[x] + I.slo_scale * (I.t_p + I.t_g * (double)rs[y])) - I.clock;
+        finite = finite && isfinite(v);
+        const int b = bucket_d(I, dmax(0.0, v));
+        mn = b < mn ? b : mn;
+        mx = b > mx ? b : mx;
+      }
+    if (finite) {
+      blo = mn;
+      bhi = mx;
+    }
+    plo = I.tr_pmin;
+    phi = I.tr_pmax < I.pmax ? I.tr_pmax : I.pmax;
+    if (plo > phi) plo = phi;
+  }
+  plan[4 * blockIdx.x] = first;
+  plan[4 * blockIdx.x + 1] = k;
+  plan[4 * blockIdx.x + 2] = blo | (bhi << 32);
+  plan[4 * blockIdx.x + 3] = plo | (phi << 32);
 }
 
 // Partial sums, grid-wide: block (x, instance) reduces a strided slice of
@@ -1243,6 +1531,8 @@ int configure(Inst& I, const EconoOptions* o, const EconoTraceRecord* t, int64_t
   I.buffer_ratio = o->buffer_ratio;
   I.free_total = I.general_cap;
   I.pt_min_lb = INT64_MAX;
+  I.tr_pmin = I.tr_rmin = INT32_MAX;  // k_init_soa narrows them
+  I.tr_pmax = I.tr_rmax = 0;
   I.ovf_id = INT64_MAX;  // no saturated prediction
   I.ovf_dem = 0;
   I.skip = (getenv("ECONO_NO_SKIP") || I.base) ? 0 : 1;
@@ -2173,10 +2463,10 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms = [](auto a, auto b2) { return std::chrono::duration<double, std::milli>(b2 - a).count(); };
   const auto t0 = now();
-  void* dplan = batch_scratch(b, SCR_PLAN, sizeof(int64_t) * 2 * (size_t)ni);
+  void* dplan = batch_scratch(b, SCR_PLAN, sizeof(int64_t) * 4 * (size_t)ni);
   if (!dplan) return set_err(err, errlen, "allocation failed"), ECONO_ECUDA;
   k_bulk_plan<<<(unsigned)ni, 32, 0, b->stream>>>(b->d_insts, (int64_t*)dplan);
-  std::vector<int64_t> plan(2 * (size_t)ni);
+  std::vector<int64_t> plan(4 * (size_t)ni);
   int rc = sync_batch(b, err, errlen);
   if (!rc && dev_d2h(plan.data(), dplan, sizeof(int64_t) * plan.size())) rc = ECONO_ECUDA;
   if (rc) return rc;
@@ -2186,13 +2476,20 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
   int bits = 1;
   for (int32_t i = 0; i < ni; ++i) {
     const Inst& I = b->inst[(size_t)i].desc;
-    const int64_t k = plan[2 * (size_t)i + 1];
+    const int64_t k = plan[4 * (size_t)i + 1];
     const uint64_t ncls = (uint64_t)I.nbuckets * (uint64_t)(I.pmax + 1);
     if (k < thr || k < 1 || ncls > 0xffffffffULL) continue;
     BulkJob J;
     memset(&J, 0, sizeof(J));
     J.inst = i;
-    J.first = plan[2 * (size_t)i];
+    J.first = plan[4 * (size_t)i];
+    {
+      const int64_t bw = plan[4 * (size_t)i + 2], pw = plan[4 * (size_t)i + 3];
+      J.wb0 = (int32_t)(bw & 0xffffffff);
+      J.wnb = (int32_t)(bw >> 32) - J.wb0 + 1;
+      J.wp0 = (int32_t)(pw & 0xffffffff);
+      J.wnp = (int32_t)(pw >> 32) - J.wp0 + 1;
+    }
     J.k = k;
     J.tiles = (int32_t)((k + kBulkTile - 1) / kBulkTile);
     J.minp = ~0ULL;
@@ -2207,17 +2504,27 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
       max_ncls = imax(max_ncls, (int64_t)I.nbuckets * (I.pmax + 1));
     }
     const size_t smem = 12 * (size_t)max_ncls;
+    // ranges (default) when the range scan's class table fits shared memory;
+    // ECONO_INGEST_TILES forces the tile-sort path, ECONO_INGEST_RADIX the global sort
+    size_t rsmem = 0;  // the largest class window
+    for (const BulkJob& J : jobs) rsmem = std::max(rsmem, 4 * (size_t)J.wnb * (size_t)J.wnp);
+    const bool ranges = !getenv("ECONO_INGEST_TILES") && rsmem <= 160 * 1024;
+    const int64_t span = ranges ? kRangeI : kTileI;
     if (!getenv("ECONO_INGEST_RADIX") && max_ncls <= 65536 && smem <= 200 * 1024) {
       const int64_t budget = bulk_budget();
       std::vector<size_t> gs;
       int64_t max_off = 0, max_t = 0;
+      for (BulkJob& J : jobs) {
+        J.tiles = (int32_t)((J.k + span - 1) / span);
+        J.sstride = ranges ? (int32_t)std::min<int64_t>(span, std::max<int64_t>(1, (int64_t)J.wnb * J.wnp)) : (int32_t)span;
+      }
       for (size_t g0 = 0; g0 < jobs.size();) {  // groups of jobs within the scratch budget
         size_t g1 = g0;
         int64_t off = 0, tl = 0;
-        while (g1 < jobs.size() && (g1 == g0 || off + (int64_t)jobs[g1].tiles * kTileI <= budget)) {
-          jobs[g1].off = off;   // segment slots: tile-aligned
-          jobs[g1].hoff = tl;   // per-tile segment counts
-          off += (int64_t)jobs[g1].tiles * kTileI;
+        while (g1 < jobs.size() && (g1 == g0 || off + (int64_t)jobs[g1].tiles * jobs[g1].sstride <= budget)) {
+          jobs[g1].off = off;   // segment slots: sstride per tile/range
+          jobs[g1].hoff = tl;   // per-tile/range segment counts
+          off += (int64_t)jobs[g1].tiles * jobs[g1].sstride;
           tl += jobs[g1].tiles;
           ++g1;
         }
@@ -2242,20 +2549,41 @@ int econo_batch_ingest(econo_batch* b, char* err, size_t errlen) {
       void* dj = base + sb + nb;
       const auto t1 = now();
       dev_h2d(dj, jobs.data(), sizeof(BulkJob) * jobs.size());
-      cudaFuncSetAttribute(k_ingest_stitch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_ingest_stitch<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_ingest_stitch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_ingest_ranges<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
+      cudaFuncSetAttribute(k_ingest_ranges<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
+      cudaFuncSetAttribute(k_ingest_ranges<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
+      cudaFuncSetAttribute(k_ingest_ranges<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
+      cudaFuncSetAttribute(k_ingest_ranges<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
+      cudaFuncSetAttribute(k_ingest_ranges<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
       for (size_t g = 0; g + 1 < gs.size(); ++g) {
         const int32_t nj = (int32_t)(gs[g + 1] - gs[g]);
         int32_t tmax = 0;
         for (size_t q = gs[g]; q < gs[g + 1]; ++q) tmax = std::max(tmax, jobs[q].tiles);
         BulkJob* J = (BulkJob*)dj + gs[g];
-        k_ingest_tiles<<<dim3((unsigned)tmax, (unsigned)nj), 256, 0, b->stream>>>(b->d_insts, J, segs, nseg);
-        k_ingest_stitch<<<(unsigned)nj, 512, smem, b->stream>>>(b->d_insts, J, segs, nseg);
+        if (ranges) {
+          int wb = 1;  // bits of the largest window class index
+          for (size_t q = gs[g]; q < gs[g + 1]; ++q)
+            while (wb < 16 && ((int64_t)1 << wb) < (int64_t)jobs[q].wnb * jobs[q].wnp) ++wb;
+          const dim3 grid((unsigned)tmax, (unsigned)nj);
+          if (getenv("ECONO_INGEST_MATCH")) k_ingest_ranges<0><<<grid, 32, rsmem, b->stream>>>(b->d_insts, J, segs, nseg);
+          else if (wb <= 4) k_ingest_ranges<4><<<grid, 32, rsmem, b->stream>>>(b->d_insts, J, segs, nseg);
+          else if (wb <= 8) k_ingest_ranges<8><<<grid, 32, rsmem, b->stream>>>(b->d_insts, J, segs, nseg);
+          else if (wb <= 10) k_ingest_ranges<10><<<grid, 32, rsmem, b->stream>>>(b->d_insts, J, segs, nseg);
+          else if (wb <= 12) k_ingest_ranges<12><<<grid, 32, rsmem, b->stream>>>(b->d_insts, J, segs, nseg);
+          else k_ingest_ranges<16><<<grid, 32, rsmem, b->stream>>>(b->d_insts, J, segs, nseg);
+          k_ingest_stitch<true><<<(unsigned)nj, 512, smem, b->stream>>>(b->d_insts, J, segs, nseg);
+        } else {
+          k_ingest_tiles<<<dim3((unsigned)tmax, (unsigned)nj), 256, 0, b->stream>>>(b->d_insts, J, segs, nseg);
+          k_ingest_stitch<false><<<(unsigned)nj, 512, smem, b->stream>>>(b->d_insts, J, segs, nseg);
+        }
       }
       rc = sync_batch(b, err, errlen);
       if (!rc) rc = cuda_check(err, errlen, "bulk ingest");
       if (verbose)
-        fprintf(stderr, "[econo] bulk ingest (tiles): plan+alloc %.1f ms, kernels %.1f ms (%zu jobs, %zu groups)\n",
-                ms(t0, t1), ms(t1, now()), jobs.size(), gs.size() - 1);
+        fprintf(stderr, "[econo] bulk ingest (%s): plan+alloc %.1f ms, kernels %.1f ms (%zu jobs, %zu groups)\n",
+                ranges ? "ranges" : "tiles", ms(t0, t1), ms(t1, now()), jobs.size(), gs.size() - 1);
       return rc;
     }
   }
