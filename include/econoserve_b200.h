@@ -263,6 +263,21 @@ int64_t econo_instance_bytes(const EconoTraceRecord* trace, int64_t n, const Eco
 int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* n, int32_t n_inst,
                        const EconoOptions* opts /* n_inst entries */, int device,
                        econo_batch** out, char* err, size_t errlen);
+/* A trace as three arrays (the instance's own device layout): the same
+ * content as EconoTraceRecord[n] (workload.hpp:20-24) with the lengths in
+ * 32 bits (the device path requires them in [1, 2^30) anyway). */
+typedef struct EconoTraceSoA {
+  const double* arrival_time;
+  const int32_t* prompt_len;
+  const int32_t* true_rl;
+} EconoTraceSoA;
+/* econo_batch_create for traces given as arrays: each array is copied
+ * straight into the instance's structure-of-arrays in HBM (16 B per request
+ * over PCIe instead of the record's 24 B, no staging or conversion pass).
+ * Same validation, messages and resulting state as econo_batch_create. */
+int econo_batch_create_soa(const EconoTraceSoA* traces, const int64_t* n, int32_t n_inst,
+                           const EconoOptions* opts /* n_inst entries */, int device,
+                           econo_batch** out, char* err, size_t errlen);
 /* Launches one device pass that advances every live instance by up to
  * max_steps steps on `stream` (a cudaStream_t, NULL = the handle's stream).
  * Asynchronous: no host synchronisation. */

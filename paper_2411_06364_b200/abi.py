@@ -211,6 +211,46 @@ def copy_options(o):
     return c
 
 
+class TraceSoA(C.Structure):
+    """EconoTraceSoA: a trace as three arrays (include/econoserve_b200.h)."""
+    _fields_ = [("arrival_time", C.c_void_p), ("prompt_len", C.c_void_p), ("true_rl", C.c_void_p)]
+
+
+class SoaTrace:
+    """A trace held as three contiguous columns — arrival_time f64, prompt_len
+    i32, true_rl i32 — the instance's device layout (econo_batch_create_soa
+    copies them into HBM as they are: 16 B per request). `out`: optional
+    preallocated (e.g. page-locked) column buffers."""
+
+    def __init__(self, arrival, prompt, true_rl):
+        self.arrival = np.ascontiguousarray(arrival, dtype=np.float64)
+        self.prompt = np.ascontiguousarray(prompt, dtype=np.int32)
+        self.true_rl = np.ascontiguousarray(true_rl, dtype=np.int32)
+        assert len(self.arrival) == len(self.prompt) == len(self.true_rl)
+
+    @classmethod
+    def from_records(cls, trace, out=None):
+        t = trace_array(trace)
+        if out is None:
+            return cls(t["arrival_time"], t["prompt_len"].astype(np.int32), t["true_rl"].astype(np.int32))
+        a, p, r = out
+        a[:] = t["arrival_time"]
+        p[:] = t["prompt_len"]
+        r[:] = t["true_rl"]
+        return cls(a, p, r)
+
+    def records(self):
+        t = np.zeros(len(self), dtype=TRACE_DTYPE)
+        t["arrival_time"], t["prompt_len"], t["true_rl"] = self.arrival, self.prompt, self.true_rl
+        return t
+
+    def __len__(self):
+        return len(self.arrival)
+
+    def struct(self):
+        return TraceSoA(self.arrival.ctypes.data, self.prompt.ctypes.data, self.true_rl.ctypes.data)
+
+
 def trace_array(trace):
     """Accepts a structured numpy array, a list of (arrival, prompt, rl) tuples,
     or three columns; returns a contiguous TRACE_DTYPE array."""

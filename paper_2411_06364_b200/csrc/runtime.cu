@@ -65,6 +65,14 @@ EDEV void init_soa_one(Inst& I, const EconoTraceRecord* tr, int64_t i, bool* ord
   *len_bad = tr[i].prompt_len < 1 || tr[i].prompt_len >= ((int64_t)1 << 30) || tr[i].true_rl < 1 ||
              tr[i].true_rl >= ((int64_t)1 << 30);
 }
+// Phase 1 for a trace uploaded as arrays (econo_batch_create_soa): the same
+// checks on the instance's own SoA.
+EDEV void init_check_one(const Inst& I, int64_t i, bool* order_bad, int64_t* prompt, bool* len_bad) {
+  const int32_t p = I.prompt[i], r = I.true_rl[i];
+  *order_bad = i > 0 && I.arrival[i] < I.arrival[i - 1];
+  *prompt = p;
+  *len_bad = p < 1 || p >= (1 << 30) || r < 1 || r >= (1 << 30);
+}
 // Phase 2 (per instance): calibration t_p / t_g (engine.hpp:171-176); the
 // prompt sum is an exact integer, equal to the reference's sequential
 // double sum of integers below 2^53.
@@ -270,6 +278,9 @@ EHD uint32_t key_digit(uint64_t k, int consumed, int dbits) {
 #ifndef ECONO_HOSTSIM
 // Per-instance init scratch: [0] first out-of-order arrival, [1] prompt sum,
 // [2] first infeasible request.
+// SOA: the trace arrays were uploaded straight into the instance's SoA
+// (econo_batch_create_soa): only the checks run.
+template <bool SOA>
 __global__ void __launch_bounds__(256) k_init_soa(Inst* insts, const EconoTraceRecord* const* traces,
                                                   unsigned long long* scr, int32_t inst0) {
   const int32_t ii = inst0 + (int32_t)blockIdx.y;
@@ -282,12 +293,13 @@ __global__ void __launch_bounds__(256) k_init_soa(Inst* insts, const EconoTraceR
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I.n; i += (int64_t)gridDim.x * blockDim.x) {
     bool ob, lb;
     int64_t p;
-    init_soa_one(I, tr, i, &ob, &p, &lb);
+    if (SOA) init_check_one(I, i, &ob, &p, &lb);
+    else init_soa_one(I, tr, i, &ob, &p, &lb);
     psum += p;
     if (ob && i < bad) bad = i;
     if (lb && i < lbad) lbad = i;
     if (!lb) {
-      const int32_t pp = (int32_t)p, rr = (int32_t)tr[i].true_rl;
+      const int32_t pp = (int32_t)p, rr = SOA ? I.true_rl[i] : (int32_t)tr[i].true_rl;
       pmn = pp < pmn ? pp : pmn;
       pmx = pp > pmx ? pp : pmx;
       rmn = rr < rmn ? rr : rmn;
@@ -2075,8 +2087,10 @@ int64_t econo_instance_bytes(const EconoTraceRecord* trace, int64_t n, const Eco
   return (int64_t)((bytes + 4095) & ~size_t(4095));
 }
 
-int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns, int32_t n_inst,
-                       const EconoOptions* opts, int device, econo_batch** out, char* err, size_t errlen) {
+// traces (records) or soa (arrays): exactly one is non-null.
+static int batch_create(const EconoTraceRecord* const* traces, const EconoTraceSoA* soa, const int64_t* ns,
+                        int32_t n_inst, const EconoOptions* opts, int device, econo_batch** out, char* err,
+                        size_t errlen) {
   *out = nullptr;
   if (n_inst < 1) return set_err(err, errlen, "n_inst must be >= 1"), ECONO_ECONFIG;
   for (int32_t i = 0; i < n_inst; ++i) {
@@ -2113,7 +2127,16 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
 #ifdef ECONO_HOSTSIM
           rcs[(size_t)i] = configure(b->inst[(size_t)i].desc, &opts[i], traces[i], ns[i], e2, sizeof(e2));
 #else  // the record checks run on the device (k_init_soa)
-          rcs[(size_t)i] = configure(b->inst[(size_t)i].desc, &opts[i], traces[i], ns[i], e2, sizeof(e2), false);
+          if (soa && opts[i].policy == ECONO_POLICY_ORCA && opts[i].max_output_len <= 0) {
+            // Orca's derived max_output_len is the one host scan configure needs: records for it
+            std::vector<EconoTraceRecord> rec((size_t)ns[i]);
+            for (int64_t k = 0; k < ns[i]; ++k)
+              rec[(size_t)k] = EconoTraceRecord{soa[i].arrival_time[k], soa[i].prompt_len[k], soa[i].true_rl[k]};
+            rcs[(size_t)i] = configure(b->inst[(size_t)i].desc, &opts[i], rec.data(), ns[i], e2, sizeof(e2), false);
+          } else {
+            rcs[(size_t)i] = configure(b->inst[(size_t)i].desc, &opts[i], soa ? nullptr : traces[i], ns[i], e2,
+                                       sizeof(e2), false);
+          }
 #endif
           if (rcs[(size_t)i]) msgs[(size_t)i] = e2;
         }
@@ -2248,13 +2271,16 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     // the previous group), so staging never costs more than 2 x chunk bytes
     // of HBM however many instances the batch holds. Pinned host buffers copy
     // at full link speed; pageable ones go through the driver's bounce buffer.
+    // Arrays (econo_batch_create_soa) are copied straight into each
+    // instance's SoA: 16 B per request, no staging, checks only.
+    const size_t rec = soa ? sizeof(double) + 2 * sizeof(int32_t) : sizeof(EconoTraceRecord);
     size_t largest = 0, total = 0;
     for (int32_t i = 0; i < n_inst; ++i) {
-      largest = std::max(largest, sizeof(EconoTraceRecord) * (size_t)ns[i]);
-      total += sizeof(EconoTraceRecord) * (size_t)ns[i];
+      largest = std::max(largest, rec * (size_t)ns[i]);
+      total += rec * (size_t)ns[i];
     }
     const size_t chunk = std::min(total, std::max(largest, (size_t)256 << 20));
-    const int nbuf = total > chunk ? 2 : 1;
+    const int nbuf = soa ? 0 : (total > chunk ? 2 : 1);
     void* stage[2] = {nullptr, nullptr};
     for (int k = 0; k < nbuf; ++k)
       if (dev_alloc(&stage[k], chunk)) {
@@ -2267,11 +2293,11 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
     for (int32_t i = 0; i < n_inst;) {
       int32_t j = i;
       size_t used = 0;
-      while (j < n_inst && used + sizeof(EconoTraceRecord) * (size_t)ns[j] <= chunk) used += sizeof(EconoTraceRecord) * (size_t)ns[j++];
+      while (j < n_inst && used + rec * (size_t)ns[j] <= chunk) used += rec * (size_t)ns[j++];
       groups.emplace_back(i, j);
       i = j;
     }
-    for (size_t g = 0; g < groups.size(); ++g) {
+    for (size_t g = 0; g < groups.size() && !soa; ++g) {
       size_t o = 0;
       for (int32_t i = groups[g].first; i < groups[g].second; ++i) {
         d_traces[(size_t)i] = (const EconoTraceRecord*)((char*)stage[g % nbuf] + o);
@@ -2305,17 +2331,34 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
       cudaEventCreateWithFlags(&converted[k], cudaEventDisableTiming);
     }
     for (size_t g = 0; g < groups.size(); ++g) {
-      const int k = (int)(g % nbuf);
-      if (g >= (size_t)nbuf) cudaStreamWaitEvent(cs, converted[k], 0);  // buffer k free again
-      for (int32_t i = groups[g].first; i < groups[g].second; ++i)
-        cudaMemcpyAsync(const_cast<EconoTraceRecord*>(d_traces[(size_t)i]), traces[i],
-                        sizeof(EconoTraceRecord) * (size_t)ns[i], cudaMemcpyHostToDevice, cs);
+      const int k = (int)(g % 2);
+      if (soa) {
+        for (int32_t i = groups[g].first; i < groups[g].second; ++i) {
+          const Inst& D = b->inst[(size_t)i].desc;
+          const size_t m = (size_t)ns[i];
+          cudaMemcpyAsync(const_cast<double*>(D.arrival.p), soa[i].arrival_time, sizeof(double) * m,
+                          cudaMemcpyHostToDevice, cs);
+          cudaMemcpyAsync(const_cast<int32_t*>(D.prompt.p), soa[i].prompt_len, sizeof(int32_t) * m,
+                          cudaMemcpyHostToDevice, cs);
+          cudaMemcpyAsync(const_cast<int32_t*>(D.true_rl.p), soa[i].true_rl, sizeof(int32_t) * m,
+                          cudaMemcpyHostToDevice, cs);
+        }
+      } else {
+        if (g >= (size_t)nbuf) cudaStreamWaitEvent(cs, converted[k % nbuf], 0);  // buffer free again
+        for (int32_t i = groups[g].first; i < groups[g].second; ++i)
+          cudaMemcpyAsync(const_cast<EconoTraceRecord*>(d_traces[(size_t)i]), traces[i],
+                          sizeof(EconoTraceRecord) * (size_t)ns[i], cudaMemcpyHostToDevice, cs);
+      }
       cudaEventRecord(copied[k], cs);
       cudaStreamWaitEvent(b->stream, copied[k], 0);
       const int32_t cnt = groups[g].second - groups[g].first;
       const unsigned gx = (unsigned)imin(imax(1, (nmax + 255) / 256), 1184 / imax(1, cnt / 8 + 1) + 1);
-      k_init_soa<<<dim3(gx, (unsigned)cnt), 256, 0, b->stream>>>(b->d_insts, (const EconoTraceRecord* const*)dt,
-                                                                 (unsigned long long*)dsc, groups[g].first);
+      if (soa)
+        k_init_soa<true><<<dim3(gx, (unsigned)cnt), 256, 0, b->stream>>>(
+            b->d_insts, (const EconoTraceRecord* const*)dt, (unsigned long long*)dsc, groups[g].first);
+      else
+        k_init_soa<false><<<dim3(gx, (unsigned)cnt), 256, 0, b->stream>>>(
+            b->d_insts, (const EconoTraceRecord* const*)dt, (unsigned long long*)dsc, groups[g].first);
       cudaEventRecord(converted[k], b->stream);
     }
     cudaStreamSynchronize(b->stream);
@@ -2369,6 +2412,29 @@ int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns,
   }
   *out = b;
   return ECONO_OK;
+}
+
+int econo_batch_create(const EconoTraceRecord* const* traces, const int64_t* ns, int32_t n_inst,
+                       const EconoOptions* opts, int device, econo_batch** out, char* err, size_t errlen) {
+  return batch_create(traces, nullptr, ns, n_inst, opts, device, out, err, errlen);
+}
+
+int econo_batch_create_soa(const EconoTraceSoA* traces, const int64_t* ns, int32_t n_inst, const EconoOptions* opts,
+                           int device, econo_batch** out, char* err, size_t errlen) {
+#ifdef ECONO_HOSTSIM  // the host build takes records: convert
+  std::vector<std::vector<EconoTraceRecord>> recs((size_t)(n_inst > 0 ? n_inst : 0));
+  std::vector<const EconoTraceRecord*> ptrs(recs.size());
+  for (int32_t i = 0; i < n_inst; ++i) {
+    recs[(size_t)i].resize((size_t)(ns[i] > 0 ? ns[i] : 0));
+    for (int64_t k = 0; k < ns[i]; ++k)
+      recs[(size_t)i][(size_t)k] = EconoTraceRecord{traces[i].arrival_time[k], traces[i].prompt_len[k],
+                                                    traces[i].true_rl[k]};
+    ptrs[(size_t)i] = recs[(size_t)i].data();
+  }
+  return batch_create(ptrs.data(), nullptr, ns, n_inst, opts, device, out, err, errlen);
+#else
+  return batch_create(nullptr, traces, ns, n_inst, opts, device, out, err, errlen);
+#endif
 }
 
 int econo_batch_launch(econo_batch* b, int64_t max_steps, void* stream) {

@@ -26,7 +26,7 @@ if os.environ.get("ECONO_LIB"):
 SYMBOLS = [
     "econo_default_options", "econo_create", "econo_step", "econo_run", "econo_records",
     "econo_report", "econo_events", "econo_samples", "econo_scalars", "econo_snapshot",
-    "econo_destroy", "econo_instance_bytes", "econo_batch_create", "econo_batch_launch", "econo_batch_launch_slice",
+    "econo_destroy", "econo_instance_bytes", "econo_batch_create", "econo_batch_create_soa", "econo_batch_launch", "econo_batch_launch_slice",
     "econo_batch_launch_to", "econo_batch_sync",
     "econo_batch_scalars", "econo_batch_engine", "econo_batch_partials", "econo_batch_destroy",
     "econo_generate_trace", "econo_batch_checkpoint", "econo_batch_restore", "econo_batch_debug",
@@ -86,6 +86,8 @@ def load(path=None):
     L.econo_instance_bytes.restype = i64
     L.econo_batch_create.argtypes = [C.POINTER(vp), C.POINTER(i64), i32, C.POINTER(abi.Options),
                                      C.c_int, C.POINTER(vp), cp, sz]
+    L.econo_batch_create_soa.argtypes = [C.POINTER(abi.TraceSoA), C.POINTER(i64), i32, C.POINTER(abi.Options),
+                                         C.c_int, C.POINTER(vp), cp, sz]
     L.econo_batch_launch.argtypes = [vp, i64, vp]
     L.econo_batch_launch_slice.argtypes = [vp, i64, i64, vp]
     L.econo_batch_launch_to.argtypes = [vp, i64, i64, vp]
@@ -248,17 +250,26 @@ class Batch:
     device form of run_sweep's engine pool (sweep.hpp:112-149)."""
 
     def __init__(self, traces, options, device=0, lib=None):
+        """traces: records (TRACE_DTYPE arrays, econo_batch_create) or, all of
+        them, abi.SoaTrace columns (econo_batch_create_soa: 16 B per request
+        copied straight into the device layout)."""
         self._L = load(lib)
-        self.traces = [abi.trace_array(t) for t in traces]
+        soa = len(traces) > 0 and all(isinstance(t, abi.SoaTrace) for t in traces)
+        self.traces = list(traces) if soa else [abi.trace_array(t) for t in traces]
         if not isinstance(options, (list, tuple)):
             options = [options] * len(self.traces)
         self.options = (abi.Options * len(self.traces))(*options)
-        ptrs = (C.c_void_p * len(self.traces))(*[t.ctypes.data for t in self.traces])
         ns = (C.c_int64 * len(self.traces))(*[len(t) for t in self.traces])
         h = C.c_void_p()
         err = C.create_string_buffer(1024)
-        rc = self._L.econo_batch_create(ptrs, ns, len(self.traces), self.options, device,
-                                        C.byref(h), err, 1024)
+        if soa:
+            arr = (abi.TraceSoA * len(self.traces))(*[t.struct() for t in self.traces])
+            rc = self._L.econo_batch_create_soa(arr, ns, len(self.traces), self.options, device,
+                                                C.byref(h), err, 1024)
+        else:
+            ptrs = (C.c_void_p * len(self.traces))(*[t.ctypes.data for t in self.traces])
+            rc = self._L.econo_batch_create(ptrs, ns, len(self.traces), self.options, device,
+                                            C.byref(h), err, 1024)
         if rc:
             _raise(rc, err)
         self.h = h

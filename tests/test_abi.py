@@ -50,7 +50,8 @@ def c_layout(struct, fields):
 @pytest.mark.parametrize("cname,pyt", [("EconoTraceRecord", abi.TraceRecord), ("EconoOptions", abi.Options),
                                        ("EconoEvent", abi.Event), ("EconoSample", abi.Sample),
                                        ("EconoRecord", abi.Record), ("EconoReport", abi.Report),
-                                       ("EconoScalars", abi.Scalars), ("EconoLengthDist", abi.LengthDist)])
+                                       ("EconoScalars", abi.Scalars), ("EconoLengthDist", abi.LengthDist),
+                                       ("EconoTraceSoA", abi.TraceSoA)])
 def test_struct_layouts_match_header(cname, pyt):
     names = [f for f, _ in pyt._fields_]
     got = c_layout(cname, names)
