@@ -350,18 +350,8 @@ __global__ void __launch_bounds__(32) k_init_scalar(Inst* insts, const uint64_t*
   inst_store(&insts[blockIdx.x], I);
 }
 
-// The instance's Inst is staged in shared memory: its SoA pointers are GP<T>
-// (__isGlobal), so the per-request stores cannot alias it and the compiler
-// keeps the pointers in registers instead of reloading them from global
-// memory after every store (a global Inst may alias them).
 __global__ void __launch_bounds__(256) k_init_req(Inst* insts, unsigned long long* scr) {
-  __shared__ Inst I;
-  {
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(&insts[blockIdx.y]);
-    uint64_t* dst = reinterpret_cast<uint64_t*>(&I);
-    for (int k = threadIdx.x; k < (int)(sizeof(Inst) / 8); k += blockDim.x) dst[k] = src[k];
-    __syncthreads();
-  }
+  Inst& I = insts[blockIdx.y];
   if (I.error) return;
   unsigned long long* sc = scr + 4 * blockIdx.y;
   const int64_t ext = init_table_extent(I);
