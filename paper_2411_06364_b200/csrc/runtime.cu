@@ -2190,12 +2190,7 @@ static int batch_create(const EconoTraceRecord* const* traces, const EconoTraceS
     size_t total = 0;
     for (auto& h : b->inst) total += h.arena_bytes;
     void* blk;
-#ifdef ECONO_HOSTSIM
     if (dev_alloc(&blk, total)) {
-#else  // zeroed group by group on the device, overlapped with the trace upload (below)
-    if (cudaMalloc(&blk, total) != cudaSuccess) {
-      (void)cudaGetLastError();
-#endif
       econo_batch_destroy(b);
       return set_err(err, errlen, "device allocation of %zu bytes failed", total), ECONO_ECUDA;
     }
@@ -2330,39 +2325,15 @@ static int batch_create(const EconoTraceRecord* const* traces, const EconoTraceS
       nmax = imax(nmax, h.desc.n);
       emax = imax(emax, h.desc.n + h.desc.general_cap + (int64_t)h.desc.nbuckets * (h.desc.pmax + 1) + 64);
     }
-    cudaStream_t cs, zs;
+    cudaStream_t cs;
     cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&zs, cudaStreamNonBlocking);
     cudaEvent_t copied[2], converted[2];
     for (int k = 0; k < 2; ++k) {
       cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&converted[k], cudaEventDisableTiming);
     }
-    // The arenas start zeroed: a memset per instance group on its own stream
-    // runs ahead of the upload (HBM ~100x faster than PCIe), and each group's
-    // copies and checks wait only for that group's memset.
-    std::vector<cudaEvent_t> zeroed(groups.size());
-    for (size_t g = 0; g < groups.size(); ++g) {
-      const HostInst& h0 = b->inst[(size_t)groups[g].first];
-      size_t zb = 0;
-      for (int32_t i = groups[g].first; i < groups[g].second; ++i) zb += b->inst[(size_t)i].arena_bytes;
-      cudaMemsetAsync(h0.arena, 0, zb, zs);
-      cudaEventCreateWithFlags(&zeroed[g], cudaEventDisableTiming);
-      cudaEventRecord(zeroed[g], zs);
-    }
-    auto destroy_upload = [&] {
-      for (int k = 0; k < 2; ++k) {
-        cudaEventDestroy(copied[k]);
-        cudaEventDestroy(converted[k]);
-      }
-      for (auto& e : zeroed) cudaEventDestroy(e);
-      cudaStreamDestroy(cs);
-      cudaStreamDestroy(zs);
-    };
     for (size_t g = 0; g < groups.size(); ++g) {
       const int k = (int)(g % 2);
-      cudaStreamWaitEvent(cs, zeroed[g], 0);
-      cudaStreamWaitEvent(b->stream, zeroed[g], 0);
       if (soa) {
         for (int32_t i = groups[g].first; i < groups[g].second; ++i) {
           const Inst& D = b->inst[(size_t)i].desc;
@@ -2400,14 +2371,22 @@ static int batch_create(const EconoTraceRecord* const* traces, const EconoTraceS
         if (sc1[4 * (size_t)i + 3] < (unsigned long long)ns[i]) {
           set_err(err, errlen, "request %lld: prompt_len and response_len must be in [1, 2^30)",
                   (long long)sc1[4 * (size_t)i + 3]);
-          destroy_upload();
+          for (int k = 0; k < 2; ++k) {
+            cudaEventDestroy(copied[k]);
+            cudaEventDestroy(converted[k]);
+          }
+          cudaStreamDestroy(cs);
           for (int k = 0; k < nbuf; ++k) dev_free(stage[k]);
           econo_batch_destroy(b);
           return ECONO_ECONFIG;
         }
     }
     const auto t1 = now();
-    destroy_upload();
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(copied[k]);
+      cudaEventDestroy(converted[k]);
+    }
+    cudaStreamDestroy(cs);
     b->stage[0] = stage[0];
     b->stage[1] = stage[1];
     const unsigned gx2 = (unsigned)imin(imax(1, (emax + 255) / 256), 1184 / imax(1, n_inst / 8 + 1) + 1);
